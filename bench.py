@@ -1,0 +1,404 @@
+#!/usr/bin/env python
+"""Benchmark of the TPO hot path (BASELINE.json metric: tensor products/sec vs
+L_max, % of roofline).
+
+Workload (BASELINE.json configs[1]): S2-grid Gaunt TP, L_max sweep 1..10,
+batch 65,536 x 1 channel per GPU, L3 = 2L.  One step = one pass of the sweep
+(ten launches of the fused tcgen05 kernel, one per L) over inputs resident in
+HBM.  L2 (126 MB) is flushed between steps by writing a 256 MiB buffer; the
+flush is outside the CUDA-event-timed region.  Multi-GPU (torchrun): every
+rank processes its own 65,536-sample shard (weak scaling, no collective on
+the data path); per-rank device times are max-reduced and a per-shard
+checksum is all-gathered after the timed region.
+
+`--impl reference` times the reference CPU algorithm instead: the fp64 oracle
+port of proj/src/{sphere,gtp}.cpp (the reference itself cannot be built here,
+Eigen 3 is missing) on all host cores, on a bounded sample of the same sweep.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "tensor products/sec vs L_max for CGTP/grid-GTP/Fourier-GTP/MTP; % of roofline"
+UNIT = "TP/s"
+SEED = 20240901
+LS = list(range(1, 11))
+BATCH = 65536
+
+
+def grid_flops_per_tp(L: int) -> int:
+    """Dense-GEMM algorithmic flops of one grid GTP:
+    2 G (2 Din + Dout), G = (2L+1)(4L+1) product-grid points."""
+    G = (2 * L + 1) * (4 * L + 1)
+    return 2 * G * (2 * (L + 1) ** 2 + (2 * L + 1) ** 2)
+
+
+def grid_bytes_per_tp(L: int) -> int:
+    return 4 * (2 * (L + 1) ** 2 + (2 * L + 1) ** 2)
+
+
+def load_peaks() -> dict:
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return {"hbm_gbs": d["hbm_gbs"], "bf16_tflops": d["bf16_tflops"], "source": "measured"}
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "source": "fallback"}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self) -> dict:
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def cpu_reference(Ls, seconds_per_L: float, nthreads: int, steps: int = 1):
+    """Reference CPU algorithm (fp64 oracle port of the grid GTP) on host cores.
+    Returns (TP/s over the sweep, sample description)."""
+    import numpy as np
+
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import oracle  # noqa: E402  (allowed here: the CPU baseline leg)
+
+    rng = np.random.default_rng(SEED)
+    per_tp = {}
+    samples = {}
+    for L in Ls:
+        d = (L + 1) ** 2
+        n = max(nthreads, 64)
+        while True:
+            x = rng.standard_normal((n, 1, d))
+            y = rng.standard_normal((n, 1, d))
+            t0 = time.perf_counter()
+            for _ in range(steps):
+                oracle.batch_mimo("gtp_grid", L, x, y, nthreads=nthreads)
+            dt = (time.perf_counter() - t0) / steps
+            if dt >= seconds_per_L or n >= BATCH:
+                break
+            n = min(BATCH, int(n * max(2.0, 1.2 * seconds_per_L / max(dt, 1e-6))))
+        per_tp[L] = dt / n
+        samples[L] = n
+    # whole sweep with BATCH TPs per L, as on the GPU
+    sweep_time = sum(BATCH * per_tp[L] for L in Ls)
+    value = len(Ls) * BATCH / sweep_time
+    return value, samples, per_tp
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--batch", type=int, default=BATCH)
+    ap.add_argument("--cpu-seconds", type=float, default=1.0, help="CPU baseline seconds per L")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extras", action="store_true", help="skip the per-kind side measurements")
+    args = ap.parse_args()
+    world, rank, local = dist_setup()
+
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+        return
+
+    import numpy as np
+    import torch
+
+    import paper_2506_13523_b200 as tpo
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+    ctx = tpo.context(local)
+    stream = torch.cuda.current_stream(dev)
+    B = args.batch
+    g = torch.Generator(device=dev)
+    g.manual_seed(SEED + 1000 * rank)
+    xs = {L: torch.randn((B, (L + 1) ** 2), generator=g, device=dev) for L in LS}
+    ys = {L: torch.randn((B, (L + 1) ** 2), generator=g, device=dev) for L in LS}
+    outs = {L: torch.empty((B, (2 * L + 1) ** 2), device=dev) for L in LS}
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MiB > 126 MB L2
+
+    def step(evs=None):
+        for i, L in enumerate(LS):
+            if evs is not None:
+                evs[i].record(stream)
+            tpo.gtp_grid(xs[L], ys[L], L, L, 2 * L, out=outs[L])
+        if evs is not None:
+            evs[len(LS)].record(stream)
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = ctx.launches
+    per_L = {L: 0.0 for L in LS}
+    total_ms = 0.0
+    with ClockSampler(local) as clk:
+        wall0 = time.perf_counter()
+        for _ in range(args.steps):
+            flush.zero_()  # evict L2 (untimed)
+            evs = [torch.cuda.Event(enable_timing=True) for _ in range(len(LS) + 1)]
+            step(evs)
+            evs[-1].synchronize()
+            for i, L in enumerate(LS):
+                per_L[L] += evs[i].elapsed_time(evs[i + 1])
+            total_ms += evs[0].elapsed_time(evs[-1])
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - wall0
+    launches = ctx.launches - launches0
+    if world > 1:
+        t = torch.tensor([total_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+        dist.barrier()
+    torch.cuda.synchronize()
+    ms_per_step = total_ms / args.steps
+    value = world * len(LS) * B / (ms_per_step / 1e3)
+
+    # result gather after the timed region: per-shard checksums over NCCL
+    cks = torch.stack([outs[L].double().sum() for L in LS]).float()
+    if world > 1:
+        allc = [torch.empty_like(cks) for _ in range(world)]
+        dist.all_gather(allc, cks)
+        checks = [c.cpu().tolist() for c in allc]
+    else:
+        checks = [cks.cpu().tolist()]
+
+    peaks = load_peaks()
+    tc_peak = peaks["bf16_tflops"] / 3.0  # 3xFP16 split on the fp16/bf16 tensor pipe
+    per = {}
+    for L in LS:
+        ms = per_L[L] / args.steps
+        fl = grid_flops_per_tp(L) * B
+        by = grid_bytes_per_tp(L) * B
+        tf = fl / (ms / 1e3) / 1e12
+        gbs = by / (ms / 1e3) / 1e9
+        t_roof = max(by / (peaks["hbm_gbs"] * 1e9), fl / (tc_peak * 1e12))
+        per[str(L)] = {"ms": round(ms, 5), "tp_per_s": round(B / (ms / 1e3), 1), "tflops": round(tf, 2),
+                       "gbs": round(gbs, 1), "roofline_frac": round(t_roof / (ms / 1e3), 4)}
+    # dominant kernel = largest share of the step
+    domL = max(LS, key=lambda L: per_L[L])
+    dom_ms = per_L[domL] / args.steps
+    traffic = None
+    tf_path = ROOT / "profiles" / "ncu_traffic.json"
+    if tf_path.exists():
+        try:
+            traffic = json.loads(tf_path.read_text()).get(f"gtp_grid_L{domL}")
+        except Exception:
+            traffic = None
+    roofline = {
+        "bound": "tensor",
+        "kernel": f"gtp_grid_tc_kernel L={domL} (3xFP16 tcgen05)",
+        "achieved": round(grid_flops_per_tp(domL) * B / (dom_ms / 1e3) / 1e12, 2),
+        "peak": round(tc_peak, 1),
+        "unit": "TFLOP/s",
+        "frac": round(grid_flops_per_tp(domL) * B / (dom_ms / 1e3) / 1e12 / tc_peak, 4),
+        "traffic": traffic,
+        "peak_note": f"{peaks['source']} bf16 tensor peak {peaks['bf16_tflops']} TF/s / 3 (3xFP16 split); "
+                     f"algorithmic flops = dense 2*G*(2Din+Dout) per TP x {B} TPs per launch",
+        "share_of_step": round(dom_ms / ms_per_step, 3),
+    }
+
+    # e2e through the C ABI with host buffers (pinned), H2D + kernel + D2H per step
+    e2e = None
+    if rank == 0 or world > 1:
+        import ctypes as C
+
+        hx = {L: xs[L].cpu().pin_memory() for L in LS}
+        hy = {L: ys[L].cpu().pin_memory() for L in LS}
+        ho = {L: torch.empty(outs[L].shape, pin_memory=True) for L in LS}
+        lib = tpo.lib()
+
+        def e2e_step():
+            for L in LS:
+                tpo.check(lib.tpo_run_host_f32(ctx.handle, tpo.KINDS["gtp_grid"], L, L, 2 * L, -1,
+                                               hx[L].data_ptr(), hy[L].data_ptr(), ho[L].data_ptr(), B, 1, 0))
+
+        for _ in range(2):
+            e2e_step()
+        n_e2e = max(2, min(args.steps, 5))
+        t0 = time.perf_counter()
+        for _ in range(n_e2e):
+            e2e_step()
+        et = (time.perf_counter() - t0) / n_e2e
+        if world > 1:
+            t = torch.tensor([et], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            et = float(t.item())
+        e2e = {"value": round(world * len(LS) * B / et, 1), "unit": UNIT,
+               "h2d_bytes_per_step": int(sum(2 * B * (L + 1) ** 2 * 4 for L in LS)),
+               "d2h_bytes_per_step": int(sum(B * (2 * L + 1) ** 2 * 4 for L in LS)),
+               "ms_per_step": round(et * 1e3, 3), "path": "tpo_run_host_f32 (C ABI, pinned host buffers)"}
+
+    extras = None
+    if not args.no_extras and rank == 0:
+        extras = side_measurements(tpo, dev, stream, flush)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        nth = os.cpu_count() or 1
+        v, samples, _ = cpu_reference(LS, args.cpu_seconds, nth)
+        cpu = {"value": round(v, 1), "unit": UNIT, "cores": nth, "kind": "port",
+               "sample": f"fp64 oracle port of gtp_grid_select, L=1..10, per-L samples {samples}, "
+                         f"scaled to {B} TPs per L"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": max(args.warmup, 3), "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32 (3xFP16 tcgen05, fp32 accumulate)",
+            "data": f"synthetic N(0,1) irreps on device, seed {SEED}+1000*rank",
+            "config": {"workload": "S2-grid GTP L_max sweep 1-10, batch 65536 x 1 channel per GPU, L3=2L "
+                                   "(BASELINE.json configs[1])",
+                       "batch_per_gpu": B, "L": LS, "l2": "flushed between steps (256 MiB write, untimed)",
+                       "parallelism": f"dp{world} (independent shards, no data-path collective)"},
+            "per_L": per, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "clocks": clk.summary(), "wall_s_timed": round(wall, 3), "checksums": checks,
+            "extras": extras,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def side_measurements(tpo, dev, stream, flush):
+    """Throughput of the other three TPO kinds on BASELINE configs (device time)."""
+    import torch
+
+    def timeit(fn, reps=5):
+        for _ in range(2):
+            fn()
+        tot = 0.0
+        for _ in range(reps):
+            flush.zero_()
+            a = torch.cuda.Event(enable_timing=True); b = torch.cuda.Event(enable_timing=True)
+            a.record(stream); fn(); b.record(stream); b.synchronize()
+            tot += a.elapsed_time(b)
+        return tot / reps
+
+    res = {}
+    g = torch.Generator(device=dev); g.manual_seed(7)
+    for kind, L, B in (("gtp_fourier", 6, 65536), ("mtp", 6, 65536), ("gtp_grid", 6, 65536)):
+        x = torch.randn((B, (L + 1) ** 2), generator=g, device=dev)
+        y = torch.randn((B, (L + 1) ** 2), generator=g, device=dev)
+        o = torch.empty((B, (2 * L + 1) ** 2), device=dev)
+        ms = timeit(lambda: tpo.run(kind, x, y, L, L, 2 * L, out=o))
+        res[f"{kind}_L{L}_B{B}"] = {"ms": round(ms, 4), "tp_per_s": round(B / ms * 1e3, 1)}
+    # channel-wise CGTP, config C4 shape (L=3, 128 channels, y shared) on a 2^14-edge chunk
+    L, C, B = 3, 128, 1 << 14
+    x = torch.randn((B, C, 16), generator=g, device=dev)
+    y = torch.randn((B, 16), generator=g, device=dev)
+    o = torch.empty((B, C, 256), device=dev)
+    ms = timeit(lambda: tpo.cgtp(x, y, L, L, out=o))
+    byts = B * (C * 16 * 4 + 16 * 4 + C * 256 * 4)
+    res[f"cgtp_L3_C128_B{B}"] = {"ms": round(ms, 4), "edges_per_s": round(B / ms * 1e3, 1),
+                                  "channel_tp_per_s": round(B * C / ms * 1e3, 1),
+                                  "gbs": round(byts / ms / 1e6, 1)}
+    return res
+
+
+def run_reference(args, world, rank):
+    if world > 1 and rank != 0:
+        return
+    nth = os.cpu_count() or 1
+    # warm the table caches (untimed), then K steps of a bounded sample
+    cpu_reference(LS, 0.01, nth)
+    vals = []
+    t0 = time.perf_counter()
+    for _ in range(max(args.warmup, 0)):
+        cpu_reference(LS, 0.05, nth)
+    for _ in range(args.steps):
+        v, samples, _ = cpu_reference(LS, args.cpu_seconds / 4, nth)
+        vals.append(v)
+    wall = time.perf_counter() - t0
+    value = statistics.median(vals)
+    sample = (f"fp64 oracle port of gtp_grid_select (reference CPU algorithm, proj/src/sphere.cpp + gtp.cpp), "
+              f"L=1..10, per-L samples {samples}, scaled to {BATCH} TPs per L")
+    line = {
+        "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(len(LS) * BATCH / value * 1e3, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": f"synthetic N(0,1), seed {SEED}",
+        "config": {"workload": "S2-grid GTP L_max sweep 1-10, batch 65536 x 1 channel (BASELINE.json configs[1])",
+                   "batch_per_gpu": BATCH, "L": LS},
+        "impl": "reference",
+        "cpu_baseline": {"value": round(value, 1), "unit": UNIT, "cores": nth, "kind": "port", "sample": sample},
+        "e2e": {"value": round(value, 1), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "wall_s": round(wall, 2),
+    }
+    print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,118 @@
+/*
+ * tpo_capi.h -- C ABI of the B200-native TPO hot path (libtpo_b200.so).
+ *
+ * Drop-in boundary for the reference so3tpo operator API
+ * (/root/reference/proj/include/tpo/{cgtp,gtp,mtp}.hpp).  The reference has
+ * one-TP-per-call, fp64, Eigen-typed entry points and no FFI for the hot path
+ * (its only binding is pybind11, proj/bindings/py_core.cpp:74-109); the
+ * entry points below are what that binding (and the C++ API in
+ * include/tpo/*.hpp) calls instead.  Plain pointers and sizes only.
+ *
+ * Data layout: every irreps vector is a single-copy
+ * tower 0..L, flat, degree-major, m = -l..l inside a degree
+ * (proj/include/tpo/irreps.hpp:61-62).  Batched tensors are row-major
+ *   x   [batch][channels][(L1+1)^2]            fp32
+ *   y   [batch][(L2+1)^2]   if y_shared         fp32
+ *       [batch][channels][(L2+1)^2] otherwise
+ *   out [batch][channels][tpo_out_dim(kind, L1, L2, L3)]   fp32
+ * Device-pointer entry points are asynchronous on `stream` (a cudaStream_t,
+ * NULL = legacy default stream).  Host-pointer entry points (`_host`) copy
+ * in, launch, copy out and synchronize.
+ *
+ * Errors: every call returns TPO_OK (0) or a positive status; the message is
+ * in tpo_last_error() (thread-local).  Status mirrors the reference's
+ * exceptions: TPO_EINVAL <-> std::invalid_argument (e.g.
+ * proj/src/cgtp.cpp:75,148-150, proj/src/gtp.cpp:198,209-210,
+ * proj/src/mtp.cpp:49-51,104-105), TPO_ERANGE <-> std::out_of_range
+ * (proj/src/irreps.cpp:65-68), TPO_ERUNTIME <-> runtime_error/logic_error
+ * (table self-checks, proj/src/gtp.cpp:105-106,137-138,175-177),
+ * TPO_ECUDA for CUDA failures (no reference analogue).
+ * There is no CPU fallback: without a usable sm_100 device every compute
+ * entry point fails with TPO_ECUDA.
+ */
+#ifndef TPO_CAPI_H
+#define TPO_CAPI_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TPO_OK 0
+#define TPO_EINVAL 1
+#define TPO_ERANGE 2
+#define TPO_ERUNTIME 3
+#define TPO_ECUDA 4
+
+/* product kinds (proj/include/tpo/bench.hpp:12 BenchImpl x expressivity.hpp Kind) */
+#define TPO_KIND_CGTP 0        /* cgtp_mimo, path-sparse     proj/src/cgtp.cpp:145-177 */
+#define TPO_KIND_GTP_GRID 1    /* gtp_grid / grid_select     proj/src/gtp.cpp:197-260 */
+#define TPO_KIND_GTP_FOURIER 2 /* gtp_fourier                proj/src/gtp.cpp:217-327 */
+#define TPO_KIND_MTP 3         /* mtp                        proj/src/mtp.cpp:99-117   */
+
+typedef struct tpo_ctx tpo_ctx;
+
+/* Library / context ------------------------------------------------------ */
+const char* tpo_last_error(void);
+const char* tpo_version(void);
+/* Creates a context bound to CUDA device `device`; device tables (CG term
+ * lists, quadrature/GEMM operands, Fourier tables) are built lazily per
+ * (kind, L1, L2, L3) and cached for the context lifetime, like the
+ * reference's process-lifetime memo caches (proj/src/wigner.cpp:64-81). */
+int tpo_ctx_create(int device, tpo_ctx** out);
+int tpo_ctx_destroy(tpo_ctx* ctx);
+/* Number of kernel launches issued through this context so far. */
+int64_t tpo_ctx_launches(const tpo_ctx* ctx);
+
+/* Shapes ------------------------------------------------------------------ */
+/* (L+1)^2 */
+int64_t tpo_tower_dim(int L);
+/* cgtp: sum over valid paths of (2 l3 + 1)  (= (L1+1)^2 (L2+1)^2), L3 ignored;
+ * gtp_grid / gtp_fourier / mtp: (L3+1)^2.  Negative status on bad args. */
+int64_t tpo_out_dim(int kind, int L1, int L2, int L3);
+/* MTP carrier degree ceil(max(L1,L2,L3)/2), proj/src/mtp.cpp:94-97 */
+int tpo_mtp_l_tilde(int L1, int L2, int L3);
+
+/* Batched device-pointer entry points ------------------------------------ */
+/* replaces tpo::cgtp_mimo(x, y, CgtpImpl::sparse) -- proj/include/tpo/cgtp.hpp:52-54 */
+int tpo_cgtp_mimo_f32(tpo_ctx* ctx, int L1, int L2, const float* x, const float* y, float* out,
+                      int64_t batch, int64_t channels, int y_shared, void* stream);
+/* replaces tpo::gtp_grid(x, y, L3) -- proj/include/tpo/gtp.hpp:15-16 */
+int tpo_gtp_grid_f32(tpo_ctx* ctx, int L1, int L2, int L3, const float* x, const float* y,
+                     float* out, int64_t batch, int64_t channels, int y_shared, void* stream);
+/* replaces tpo::gtp_fourier(x, y, L3) -- proj/include/tpo/gtp.hpp:80-81 */
+int tpo_gtp_fourier_f32(tpo_ctx* ctx, int L1, int L2, int L3, const float* x, const float* y,
+                        float* out, int64_t batch, int64_t channels, int y_shared, void* stream);
+/* replaces tpo::mtp(x, y, L3, MtpImpl::sparse, nullptr, l_tilde_override)
+ * -- proj/include/tpo/mtp.hpp:41-43 ; l_tilde < 0 picks the minimal carrier */
+int tpo_mtp_f32(tpo_ctx* ctx, int L1, int L2, int L3, int l_tilde, const float* x,
+                const float* y, float* out, int64_t batch, int64_t channels, int y_shared,
+                void* stream);
+/* replaces tpo::weighted_gtp(x, y, a, b, c, L3) -- proj/include/tpo/gtp.hpp:21-24 ;
+ * a[L1+1], b[L2+1], c[L3+1] are HOST arrays of per-degree weights */
+int tpo_weighted_gtp_f32(tpo_ctx* ctx, int L1, int L2, int L3, const double* a,
+                         const double* b, const double* c, const float* x, const float* y,
+                         float* out, int64_t batch, int64_t channels, int y_shared, void* stream);
+
+/* Generic dispatch by kind (l_tilde only used by MTP). */
+int tpo_run_f32(tpo_ctx* ctx, int kind, int L1, int L2, int L3, int l_tilde, const float* x,
+                const float* y, float* out, int64_t batch, int64_t channels, int y_shared,
+                void* stream);
+/* Same with HOST buffers: H2D copy, launch, D2H copy, synchronize.  Scratch
+ * device buffers are owned by the context and reused across calls. */
+int tpo_run_host_f32(tpo_ctx* ctx, int kind, int L1, int L2, int L3, int l_tilde,
+                     const float* x_host, const float* y_host, float* out_host, int64_t batch,
+                     int64_t channels, int y_shared);
+
+/* Kernel selection for GTP-grid (for tests/bench): 0 auto, 1 force the fused
+ * tcgen05 kernel (fails if the shape does not fit), 2 force the SIMT
+ * separable kernel.  Returns the previous setting. */
+int tpo_set_gtp_grid_path(tpo_ctx* ctx, int path);
+/* Which GTP-grid kernel the last tpo_gtp_grid_f32 call used (1 tc, 2 simt). */
+int tpo_last_gtp_grid_path(const tpo_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,138 @@
+"""B200-native SO(3) tensor-product operations (CGTP, S2-grid GTP,
+Fourier GTP, MTP) behind the reference so3tpo operator API.
+
+Batched device API (torch tensors on an sm_100 device, fp32, contiguous):
+
+    out = cgtp(x, y, L1, L2)                       # tpo::cgtp_mimo
+    out = gtp_grid(x, y, L1, L2, L3)               # tpo::gtp_grid
+    out = gtp_fourier(x, y, L1, L2, L3)            # tpo::gtp_fourier
+    out = mtp(x, y, L1, L2, L3, l_tilde=-1)        # tpo::mtp
+    out = weighted_gtp(x, y, a, b, c, L1, L2, L3)  # tpo::weighted_gtp
+
+x is [B, Din1] or [B, C, Din1]; y is [B, Din2] (shared across the C
+channels when x has a channel axis) or [B, C, Din2].  Results are
+[B, (C,) Dout].  Every call goes through the C ABI of libtpo_b200.so on
+torch's current CUDA stream; nothing falls back to the CPU.
+
+The one-product-per-call, irreps-string API of the reference's Python
+module lives in :mod:`paper_2506_13523_b200.so3tpo`.
+"""
+from __future__ import annotations
+
+from ._lib import KINDS, Context, TpoError, check, context, lib
+
+__all__ = [
+    "cgtp", "gtp_grid", "gtp_fourier", "mtp", "weighted_gtp", "run", "out_dim", "tower_dim",
+    "mtp_l_tilde", "Context", "TpoError", "context", "lib", "KINDS",
+]
+
+
+def tower_dim(L: int) -> int:
+    return (L + 1) * (L + 1)
+
+
+def out_dim(kind: str, L1: int, L2: int, L3: int = 0) -> int:
+    r = int(lib().tpo_out_dim(KINDS[kind], L1, L2, L3))
+    if r < 0:
+        check(-r)
+    return r
+
+
+def mtp_l_tilde(L1: int, L2: int, L3: int) -> int:
+    return int(lib().tpo_mtp_l_tilde(L1, L2, L3))
+
+
+def _prep(x, y, L1, L2, kind, L3):
+    import torch
+
+    if not (isinstance(x, torch.Tensor) and isinstance(y, torch.Tensor)):
+        raise TypeError("x and y must be torch tensors")
+    if not x.is_cuda or not y.is_cuda:
+        raise ValueError("inputs must live on a CUDA device (no CPU path)")
+    if x.dtype != torch.float32 or y.dtype != torch.float32:
+        raise ValueError("inputs must be float32")
+    d1, d2 = tower_dim(L1), tower_dim(L2)
+    if x.dim() == 2:
+        B, C = x.shape[0], 1
+        if x.shape[1] != d1:
+            raise ValueError(f"x has {x.shape[1]} components, irreps dim is {d1}")
+        if tuple(y.shape) != (B, d2):
+            raise ValueError(f"y must be [{B}, {d2}]")
+        y_shared = 0
+    elif x.dim() == 3:
+        B, C = x.shape[0], x.shape[1]
+        if x.shape[2] != d1:
+            raise ValueError(f"x has {x.shape[2]} components, irreps dim is {d1}")
+        if tuple(y.shape) == (B, d2):
+            y_shared = 1
+        elif tuple(y.shape) == (B, C, d2):
+            y_shared = 0
+        else:
+            raise ValueError(f"y must be [{B}, {d2}] or [{B}, {C}, {d2}]")
+    else:
+        raise ValueError("x must be [B, Din] or [B, C, Din]")
+    if y.device != x.device:
+        raise ValueError("x and y must be on the same device")
+    x = x.contiguous()
+    y = y.contiguous()
+    dout = out_dim(kind, L1, L2, L3)
+    shape = (B, dout) if x.dim() == 2 else (B, C, dout)
+    out = torch.empty(shape, dtype=torch.float32, device=x.device)
+    stream = torch.cuda.current_stream(x.device).cuda_stream
+    return x, y, out, B, C, y_shared, stream
+
+
+def run(kind: str, x, y, L1: int, L2: int, L3: int = 0, l_tilde: int = -1, out=None):
+    """Generic batched dispatch through tpo_run_f32."""
+    x, y, o, B, C, ys, stream = _prep(x, y, L1, L2, kind, L3)
+    if out is not None:
+        if out.shape != o.shape or out.dtype != o.dtype or not out.is_contiguous():
+            raise ValueError("out has the wrong shape/dtype or is not contiguous")
+        o = out
+    ctx = context(x.device.index)
+    check(lib().tpo_run_f32(ctx.handle, KINDS[kind], L1, L2, L3, l_tilde, x.data_ptr(), y.data_ptr(),
+                            o.data_ptr(), B, C, ys, stream))
+    return o
+
+
+def cgtp(x, y, L1: int, L2: int, out=None):
+    """Batched tpo::cgtp_mimo (proj/src/cgtp.cpp:145-177); output layout is
+    the reference's path order (l1, l2, l3 ascending)."""
+    return run("cgtp", x, y, L1, L2, 0, -1, out)
+
+
+def gtp_grid(x, y, L1: int, L2: int, L3: int, out=None):
+    """Batched tpo::gtp_grid (proj/src/gtp.cpp:197-204, 228-260)."""
+    return run("gtp_grid", x, y, L1, L2, L3, -1, out)
+
+
+def gtp_fourier(x, y, L1: int, L2: int, L3: int, out=None):
+    """Batched tpo::gtp_fourier (proj/src/gtp.cpp:217-224, 262-327)."""
+    return run("gtp_fourier", x, y, L1, L2, L3, -1, out)
+
+
+def mtp(x, y, L1: int, L2: int, L3: int, l_tilde: int = -1, out=None):
+    """Batched tpo::mtp (proj/src/mtp.cpp:99-117)."""
+    return run("mtp", x, y, L1, L2, L3, l_tilde, out)
+
+
+def weighted_gtp(x, y, a, b, c, L1: int, L2: int, L3: int):
+    """Batched tpo::weighted_gtp: c (.) gtp(a (.) x, b (.) y) with per-degree
+    weights (proj/src/gtp.cpp:206-215)."""
+    import ctypes as C
+
+    import numpy as np
+
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    b = np.ascontiguousarray(b, dtype=np.float64)
+    c = np.ascontiguousarray(c, dtype=np.float64)
+    if len(c) != L3 + 1:
+        raise ValueError("weighted_gtp: c must have L3+1 entries")
+    if len(a) < L1 + 1 or len(b) < L2 + 1:
+        raise ValueError("weighted_gtp: weight vector shorter than input degrees")
+    x, y, o, B, Cc, ys, stream = _prep(x, y, L1, L2, "gtp_grid", L3)
+    ctx = context(x.device.index)
+    ptr = lambda v: v.ctypes.data_as(C.c_void_p)  # noqa: E731
+    check(lib().tpo_weighted_gtp_f32(ctx.handle, L1, L2, L3, ptr(a), ptr(b), ptr(c), x.data_ptr(),
+                                     y.data_ptr(), o.data_ptr(), B, Cc, ys, stream))
+    return o

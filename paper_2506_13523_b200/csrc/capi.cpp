@@ -1,0 +1,303 @@
+// extern "C" boundary of libtpo_b200.so (declared in include/tpo_capi.h).
+#include "tpo_capi.h"
+
+#include <algorithm>
+#include <cmath>
+#include <string>
+#include <vector>
+
+#include "host/context.hpp"
+
+using tpo_b200::Context;
+using tpo_b200::CudaFailure;
+using tpo_b200::InvalidArgument;
+using tpo_b200::RowSpec;
+
+struct tpo_ctx {
+  explicit tpo_ctx(int dev) : impl(dev) {}
+  Context impl;
+};
+
+namespace {
+
+constexpr int kMaxL = 32;  // inputs; outputs up to 2 * kMaxL
+thread_local std::string g_err;
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return TPO_OK;
+  } catch (const InvalidArgument& e) {
+    g_err = e.what();
+    return TPO_EINVAL;
+  } catch (const std::invalid_argument& e) {
+    g_err = e.what();
+    return TPO_EINVAL;
+  } catch (const std::out_of_range& e) {
+    g_err = e.what();
+    return TPO_ERANGE;
+  } catch (const CudaFailure& e) {
+    g_err = e.what();
+    return TPO_ECUDA;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return TPO_ERUNTIME;
+  }
+}
+
+void check_args(const tpo_ctx* ctx, int L1, int L2, const void* x, const void* y, const void* out,
+                int64_t batch, int64_t channels) {
+  if (!ctx) throw InvalidArgument("tpo: null context");
+  if (L1 < 0 || L2 < 0) throw InvalidArgument("irreps: degree must be >= 0");
+  if (L1 > kMaxL || L2 > kMaxL)
+    throw InvalidArgument("tpo: input degree above the supported maximum of " + std::to_string(kMaxL));
+  if (batch < 0) throw InvalidArgument("tpo: batch must be >= 0");
+  if (channels < 1) throw InvalidArgument("tpo: channels must be >= 1");
+  if (batch > 0 && (!x || !y || !out)) throw InvalidArgument("tpo: null data pointer");
+}
+
+void check_L3(int L3, const char* who) {
+  if (L3 < 0) throw InvalidArgument(std::string(who) + ": L3 must be >= 0");
+  if (L3 > 2 * kMaxL) throw InvalidArgument(std::string(who) + ": L3 above the supported maximum");
+}
+
+RowSpec rows_of(const float* x, const float* y, float* out, int64_t batch, int64_t channels, int y_shared) {
+  RowSpec rs{};
+  rs.x = x;
+  rs.y = y;
+  rs.out = out;
+  rs.rows = batch * channels;
+  rs.channels = channels;
+  rs.y_shared = y_shared ? 1 : 0;
+  return rs;
+}
+
+void launched(tpo_ctx* ctx, cudaError_t e, const char* what) {
+  tpo_b200::cuda_check(e, what);
+  ctx->impl.launches.fetch_add(1);
+}
+
+int min_lt(int L1, int L2, int L3) { return (std::max({L1, L2, L3}) + 1) / 2; }
+
+void run_cgtp(tpo_ctx* ctx, int L1, int L2, const RowSpec& rs, cudaStream_t s) {
+  const auto& t = ctx->impl.cgtp(L1, L2);
+  // keep each launch under 2^31 blocks (rows/16 * chunks)
+  const int64_t max_rows = std::max<int64_t>(16, (2147483647LL / std::max(t.nchunks, 1)) / 16 * 16);
+  for (int64_t r0 = 0; r0 < rs.rows; r0 += max_rows) {
+    RowSpec sub = rs;
+    sub.rows = std::min(max_rows, rs.rows - r0);
+    sub.x = rs.x + r0 * t.din1;
+    sub.out = rs.out + r0 * t.dout;
+    if (rs.y_shared) {
+      if (r0 % rs.channels) throw InvalidArgument("cgtp: batch too large for one call");
+      sub.y = rs.y + (r0 / rs.channels) * t.din2;
+    } else {
+      sub.y = rs.y + r0 * t.din2;
+    }
+    launched(ctx, tpo_b200::launch_cgtp(t, sub, s), "cgtp kernel");
+  }
+}
+
+void run_grid(tpo_ctx* ctx, int L1, int L2, int L3, const RowSpec& rs, cudaStream_t s) {
+  Context& c = ctx->impl;
+  if (c.grid_path != 2) {
+    const auto& e = c.grid_tc(L1, L2, L3);
+    if (e.fits) {
+      c.last_grid_path = 1;
+      launched(ctx, tpo_b200::launch_gtp_grid_tc(e.t, rs, c.num_sms(), s), "gtp_grid tcgen05 kernel");
+      return;
+    }
+    if (c.grid_path == 1) throw InvalidArgument("gtp_grid: shape does not fit the tcgen05 tiling");
+  }
+  c.last_grid_path = 2;
+  launched(ctx, tpo_b200::launch_gtp_grid_simt(c.grid_simt(L1, L2, L3), rs, c.num_sms(), s),
+           "gtp_grid simt kernel");
+}
+
+void run_kind(tpo_ctx* ctx, int kind, int L1, int L2, int L3, int lt, const float* x, const float* y,
+              float* out, int64_t batch, int64_t channels, int y_shared, cudaStream_t s) {
+  check_args(ctx, L1, L2, x, y, out, batch, channels);
+  ctx->impl.activate();
+  const RowSpec rs = rows_of(x, y, out, batch, channels, y_shared);
+  switch (kind) {
+    case TPO_KIND_CGTP:
+      if (rs.rows > 0) run_cgtp(ctx, L1, L2, rs, s);
+      return;
+    case TPO_KIND_GTP_GRID:
+      check_L3(L3, "gtp_grid");
+      if (rs.rows > 0) run_grid(ctx, L1, L2, L3, rs, s);
+      return;
+    case TPO_KIND_GTP_FOURIER:
+      check_L3(L3, "gtp_fourier");
+      if (rs.rows > 0)
+        launched(ctx, tpo_b200::launch_gtp_fourier(ctx->impl.fourier(L1, L2, L3), rs, ctx->impl.num_sms(), s),
+                 "gtp_fourier kernel");
+      return;
+    case TPO_KIND_MTP: {
+      check_L3(L3, "mtp");
+      const int lmin = min_lt(L1, L2, L3);
+      int l = lmin;
+      if (lt >= 0) {
+        if (lt < lmin) throw InvalidArgument("mtp: l_tilde below the minimal carrier degree");
+        if (lt > kMaxL) throw InvalidArgument("mtp: l_tilde above the supported maximum");
+        l = lt;
+      }
+      if (rs.rows > 0)
+        launched(ctx, tpo_b200::launch_mtp(ctx->impl.mtp(L1, L2, L3, l), rs, ctx->impl.num_sms(), s),
+                 "mtp kernel");
+      return;
+    }
+    default:
+      throw InvalidArgument("tpo: unknown kind " + std::to_string(kind));
+  }
+}
+
+int64_t out_dim(int kind, int L1, int L2, int L3) {
+  if (L1 < 0 || L2 < 0) throw InvalidArgument("irreps: degree must be >= 0");
+  if (kind == TPO_KIND_CGTP) return static_cast<int64_t>(L1 + 1) * (L1 + 1) * (L2 + 1) * (L2 + 1);
+  if (kind < 0 || kind > TPO_KIND_MTP) throw InvalidArgument("tpo: unknown kind");
+  if (L3 < 0) throw InvalidArgument("tpo: L3 must be >= 0");
+  return static_cast<int64_t>(L3 + 1) * (L3 + 1);
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* tpo_last_error(void) { return g_err.c_str(); }
+const char* tpo_version(void) { return "tpo_b200 0.1 (sm_100a)"; }
+
+int tpo_ctx_create(int device, tpo_ctx** out) {
+  return guarded([&] {
+    if (!out) throw InvalidArgument("tpo_ctx_create: null out pointer");
+    *out = nullptr;
+    *out = new tpo_ctx(device);
+  });
+}
+
+int tpo_ctx_destroy(tpo_ctx* ctx) {
+  return guarded([&] { delete ctx; });
+}
+
+int64_t tpo_ctx_launches(const tpo_ctx* ctx) { return ctx ? ctx->impl.launches.load() : -TPO_EINVAL; }
+
+int64_t tpo_tower_dim(int L) { return L < 0 ? -TPO_EINVAL : static_cast<int64_t>(L + 1) * (L + 1); }
+
+int64_t tpo_out_dim(int kind, int L1, int L2, int L3) {
+  int64_t r = 0;
+  const int st = guarded([&] { r = out_dim(kind, L1, L2, L3); });
+  return st ? -st : r;
+}
+
+int tpo_mtp_l_tilde(int L1, int L2, int L3) { return min_lt(L1, L2, L3); }
+
+int tpo_cgtp_mimo_f32(tpo_ctx* ctx, int L1, int L2, const float* x, const float* y, float* out, int64_t batch,
+                      int64_t channels, int y_shared, void* stream) {
+  return guarded([&] {
+    run_kind(ctx, TPO_KIND_CGTP, L1, L2, 0, -1, x, y, out, batch, channels, y_shared,
+             static_cast<cudaStream_t>(stream));
+  });
+}
+
+int tpo_gtp_grid_f32(tpo_ctx* ctx, int L1, int L2, int L3, const float* x, const float* y, float* out,
+                     int64_t batch, int64_t channels, int y_shared, void* stream) {
+  return guarded([&] {
+    run_kind(ctx, TPO_KIND_GTP_GRID, L1, L2, L3, -1, x, y, out, batch, channels, y_shared,
+             static_cast<cudaStream_t>(stream));
+  });
+}
+
+int tpo_gtp_fourier_f32(tpo_ctx* ctx, int L1, int L2, int L3, const float* x, const float* y, float* out,
+                        int64_t batch, int64_t channels, int y_shared, void* stream) {
+  return guarded([&] {
+    run_kind(ctx, TPO_KIND_GTP_FOURIER, L1, L2, L3, -1, x, y, out, batch, channels, y_shared,
+             static_cast<cudaStream_t>(stream));
+  });
+}
+
+int tpo_mtp_f32(tpo_ctx* ctx, int L1, int L2, int L3, int l_tilde, const float* x, const float* y, float* out,
+                int64_t batch, int64_t channels, int y_shared, void* stream) {
+  return guarded([&] {
+    run_kind(ctx, TPO_KIND_MTP, L1, L2, L3, l_tilde, x, y, out, batch, channels, y_shared,
+             static_cast<cudaStream_t>(stream));
+  });
+}
+
+int tpo_run_f32(tpo_ctx* ctx, int kind, int L1, int L2, int L3, int l_tilde, const float* x, const float* y,
+                float* out, int64_t batch, int64_t channels, int y_shared, void* stream) {
+  return guarded([&] {
+    run_kind(ctx, kind, L1, L2, L3, l_tilde, x, y, out, batch, channels, y_shared,
+             static_cast<cudaStream_t>(stream));
+  });
+}
+
+int tpo_weighted_gtp_f32(tpo_ctx* ctx, int L1, int L2, int L3, const double* a, const double* b, const double* c,
+                         const float* x, const float* y, float* out, int64_t batch, int64_t channels, int y_shared,
+                         void* stream) {
+  return guarded([&] {
+    // proj/src/gtp.cpp:206-215: c (.) gtp(a (.) x, b (.) y)
+    check_args(ctx, L1, L2, x, y, out, batch, channels);
+    check_L3(L3, "weighted_gtp");
+    if (!a || !b || !c) throw InvalidArgument("weighted_gtp: weight vector shorter than input degrees");
+    ctx->impl.activate();
+    const cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const int64_t rows = batch * channels;
+    if (rows == 0) return;
+    const int64_t yrows = y_shared ? batch : rows;
+    const int64_t d1 = (L1 + 1) * (L1 + 1), d2 = (L2 + 1) * (L2 + 1);
+    float *xs = nullptr, *ys = nullptr, *wd = nullptr;
+    const size_t nw = static_cast<size_t>(L1 + 1 + L2 + 1 + L3 + 1);
+    tpo_b200::cuda_check(cudaMallocAsync(reinterpret_cast<void**>(&xs), rows * d1 * sizeof(float), s), "malloc");
+    tpo_b200::cuda_check(cudaMallocAsync(reinterpret_cast<void**>(&ys), yrows * d2 * sizeof(float), s), "malloc");
+    tpo_b200::cuda_check(cudaMallocAsync(reinterpret_cast<void**>(&wd), nw * sizeof(float), s), "malloc");
+    std::vector<float> wh;
+    for (int i = 0; i <= L1; ++i) wh.push_back(static_cast<float>(a[i]));
+    for (int i = 0; i <= L2; ++i) wh.push_back(static_cast<float>(b[i]));
+    for (int i = 0; i <= L3; ++i) wh.push_back(static_cast<float>(c[i]));
+    tpo_b200::cuda_check(cudaMemcpyAsync(wd, wh.data(), nw * sizeof(float), cudaMemcpyHostToDevice, s), "copy");
+    tpo_b200::cuda_check(cudaStreamSynchronize(s), "sync");  // wh is pageable stack memory
+    launched(ctx, tpo_b200::launch_scale_degrees(x, xs, rows, L1, wd, s), "scale");
+    launched(ctx, tpo_b200::launch_scale_degrees(y, ys, yrows, L2, wd + L1 + 1, s), "scale");
+    const RowSpec rs = rows_of(xs, ys, out, batch, channels, y_shared);
+    run_grid(ctx, L1, L2, L3, rs, s);
+    launched(ctx, tpo_b200::launch_scale_degrees(out, out, rows, L3, wd + L1 + 1 + L2 + 1, s), "scale");
+    cudaFreeAsync(xs, s);
+    cudaFreeAsync(ys, s);
+    cudaFreeAsync(wd, s);
+  });
+}
+
+int tpo_run_host_f32(tpo_ctx* ctx, int kind, int L1, int L2, int L3, int l_tilde, const float* x_host,
+                     const float* y_host, float* out_host, int64_t batch, int64_t channels, int y_shared) {
+  return guarded([&] {
+    check_args(ctx, L1, L2, x_host, y_host, out_host, batch, channels);
+    const int64_t dout = out_dim(kind, L1, L2, L3);
+    Context& c = ctx->impl;
+    c.activate();
+    const int64_t rows = batch * channels;
+    if (rows == 0) return;
+    const int64_t yrows = y_shared ? batch : rows;
+    const size_t nx = rows * (L1 + 1) * (L1 + 1), ny = yrows * (L2 + 1) * (L2 + 1), no = rows * dout;
+    float* dx = c.scratch(0, nx);
+    float* dy = c.scratch(1, ny);
+    float* dout_p = c.scratch(2, no);
+    const cudaStream_t s = c.host_stream();
+    tpo_b200::cuda_check(cudaMemcpyAsync(dx, x_host, nx * sizeof(float), cudaMemcpyHostToDevice, s), "H2D x");
+    tpo_b200::cuda_check(cudaMemcpyAsync(dy, y_host, ny * sizeof(float), cudaMemcpyHostToDevice, s), "H2D y");
+    run_kind(ctx, kind, L1, L2, L3, l_tilde, dx, dy, dout_p, batch, channels, y_shared, s);
+    tpo_b200::cuda_check(cudaMemcpyAsync(out_host, dout_p, no * sizeof(float), cudaMemcpyDeviceToHost, s), "D2H");
+    tpo_b200::cuda_check(cudaStreamSynchronize(s), "sync");
+  });
+}
+
+int tpo_set_gtp_grid_path(tpo_ctx* ctx, int path) {
+  if (!ctx || path < 0 || path > 2) return -TPO_EINVAL;
+  const int prev = ctx->impl.grid_path;
+  ctx->impl.grid_path = path;
+  return prev;
+}
+
+int tpo_last_gtp_grid_path(const tpo_ctx* ctx) { return ctx ? ctx->impl.last_grid_path : -TPO_EINVAL; }
+
+}  // extern "C"

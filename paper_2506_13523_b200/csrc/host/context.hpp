@@ -1,0 +1,82 @@
+// tpo_ctx: per-device context owning device-resident tables (built lazily
+// per shape, cached for the context lifetime like the reference's memo
+// caches, proj/src/wigner.cpp:64-81 / proj/src/gtp.cpp:25-32,183-195) and
+// scratch buffers for the host-pointer entry points.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <array>
+#include <atomic>
+#include <cstdint>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../kernels/kernels.hpp"
+
+namespace tpo_b200 {
+
+// error types mapped to TPO_* status codes by capi.cpp
+struct InvalidArgument : std::invalid_argument {
+  using std::invalid_argument::invalid_argument;
+};
+struct CudaFailure : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+void cuda_check(cudaError_t e, const char* what);
+
+struct GridTcEntry {
+  bool fits = false;
+  GridTcTables t{};
+};
+
+class Context {
+ public:
+  explicit Context(int device);
+  ~Context();
+
+  int device() const { return device_; }
+  int num_sms() const { return num_sms_; }
+  void activate() const;
+
+  const CgtpTables& cgtp(int L1, int L2);
+  const GridTcEntry& grid_tc(int L1, int L2, int L3);
+  const GridSimtTables& grid_simt(int L1, int L2, int L3);
+  const FourierDevTables& fourier(int L1, int L2, int L3);
+  const MtpDevTables& mtp(int L1, int L2, int L3, int lt);
+  const float* degree_weights(const std::vector<double>& w);  // small per-call device array
+
+  // scratch for host entry points / weighted products (grown on demand)
+  float* scratch(int slot, size_t floats);
+  cudaStream_t host_stream() const { return host_stream_; }
+
+  std::atomic<int64_t> launches{0};
+  int grid_path = 0;       // 0 auto, 1 tcgen05, 2 simt
+  int last_grid_path = 0;
+
+ private:
+  template <class T>
+  T* upload(const std::vector<T>& v);
+  void* dev_alloc(size_t bytes);
+
+  int device_ = 0;
+  int num_sms_ = 148;
+  cudaStream_t host_stream_ = nullptr;
+  std::mutex mu_;
+  std::vector<void*> allocs_;
+  std::map<std::array<int, 2>, CgtpTables> cgtp_;
+  std::map<std::array<int, 3>, GridTcEntry> grid_tc_;
+  std::map<std::array<int, 3>, GridSimtTables> grid_simt_;
+  std::map<std::array<int, 3>, FourierDevTables> fourier_;
+  std::map<std::array<int, 4>, MtpDevTables> mtp_;
+  std::map<std::vector<double>, const float*> weights_;
+  std::array<void*, 4> scratch_{};
+  std::array<size_t, 4> scratch_cap_{};
+};
+
+}  // namespace tpo_b200

@@ -1,0 +1,115 @@
+// Device-table descriptors and launchers for the four TPO kernels.
+// Tables are built on the host (host/context.cpp) and live in device memory
+// owned by the tpo_ctx; launchers are asynchronous on the given stream.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace tpo_b200 {
+
+// Row indexing shared by all kernels: row r in [0, rows) is (b, c) with
+// rows = batch * channels; x row = r, y row = y_shared ? r / channels : r.
+struct RowSpec {
+  const float* x;
+  const float* y;
+  float* out;
+  int64_t rows;
+  int64_t channels;
+  int y_shared;
+};
+
+// ---------------------------------------------------------------- CGTP
+// For output chunk q (kCgtpChunk consecutive outputs), terms are stored
+// term-major: term t of output (q*kCgtpChunk + i) at
+// terms[chunk_off[q] + t*kCgtpChunk + i], packed {i1 | i2 << 16, coef bits}.
+constexpr int kCgtpChunk = 128;
+struct CgtpTables {
+  int din1, din2, dout, nchunks;
+  const uint2* terms;
+  const int* chunk_off;  // [nchunks]
+  const int* chunk_nt;   // [nchunks] padded term count
+};
+cudaError_t launch_cgtp(const CgtpTables& t, const RowSpec& rs, cudaStream_t s);
+
+// ---------------------------------------------------------------- GTP grid, tcgen05
+// Operands pre-split into fp16 hi/lo and pre-tiled in the UMMA canonical
+// K-major layout, one contiguous block per grid chunk:
+//   s[c]  : [2 (hi,lo)][nc rows (grid pts)][kp] canonical, R = nc
+//   a[c]  : [2 (hi,lo)][dout_pad rows (outputs)][nc] canonical, R = dout_pad
+struct GridTcTables {
+  int din1, din2, k1p, k2p;  // input dims, K padded to 16
+  int nc, nchunks;           // grid points per chunk, chunks
+  int dout_eff;              // outputs computed (degrees <= min(L3, band))
+  int dout_total;            // (L3+1)^2 written (zeros past the band)
+  int dout_pad;              // dout_eff padded to 16
+  int a_shift;               // device A = A * 2^a_shift
+  int tmem_cols;             // power of two >= dout_pad + 2*nc
+  int smem_bytes;
+  int same_s;                // s2 == s1 (L1 == L2)
+  const uint8_t* s1;
+  const uint8_t* s2;
+  const uint8_t* a;
+  uint32_t s1_chunk_bytes, s2_chunk_bytes, a_chunk_bytes;
+  // shared-memory carve-up (byte offsets)
+  uint32_t off_x, off_y, off_s1, off_s2, off_p, off_a;
+};
+cudaError_t launch_gtp_grid_tc(const GridTcTables& t, const RowSpec& rs, int num_sms, cudaStream_t s);
+int gtp_grid_tc_max_smem();
+
+// ---------------------------------------------------------------- GTP grid, SIMT separable
+struct GridSimtTables {
+  int L1, L2, band, L3e, dout_total;  // L3e = min(L3, band)
+  int nt, np;
+  const float* lam;   // [(band+1)(band+2)/2][nt]
+  const float* cs;    // [2*band+1][np]
+  const float* wq;    // [nt] = w_j * 2pi/np
+  float out_scale;    // 1
+};
+cudaError_t launch_gtp_grid_simt(const GridSimtTables& t, const RowSpec& rs, int num_sms, cudaStream_t s);
+
+// ---------------------------------------------------------------- GTP Fourier
+// Encode gather lists per spectrum mode (u,v) of the (2L+1)^2 input spectra,
+// direct 2D convolution on the Hermitian half-plane of the (4L+1)^2 product
+// spectrum, decode gather lists per output coefficient.
+struct FourierDevTables {
+  int L, L1, L2, L3, dout_total, dout_eff;
+  int nenc1, nenc2;        // entries in the encode lists for x / y
+  const int* enc1_off;     // [(2L+1)^2 + 1] CSR over modes, entries (input idx, w)
+  const int* enc1_idx;
+  const float2* enc1_w;
+  const int* enc2_off;
+  const int* enc2_idx;
+  const float2* enc2_w;
+  const int* dec_off;      // [dout_eff + 1] CSR, entries (half-plane mode idx, w, conj flag in idx sign)
+  const int* dec_idx;
+  const float2* dec_w;
+  int nhalf;               // number of half-plane product modes
+  const int2* half_uv;     // [nhalf] (U, V)
+};
+cudaError_t launch_gtp_fourier(const FourierDevTables& t, const RowSpec& rs, int num_sms, cudaStream_t s);
+
+// ---------------------------------------------------------------- MTP
+struct MtpDevTables {
+  int lt, dt, din1, din2, dout_total, dout_eff;
+  // embed: per carrier cell (m1,m2) a CSR list of (input idx, coef)
+  const int* emb1_off;  // [dt*dt + 1]
+  const int* emb1_idx;
+  const float* emb1_c;
+  const int* emb2_off;
+  const int* emb2_idx;
+  const float* emb2_c;
+  // extract: per output coefficient a CSR list of (cell idx, coef)
+  const int* ext_off;   // [dout_eff + 1]
+  const int* ext_idx;
+  const float* ext_c;
+};
+cudaError_t launch_mtp(const MtpDevTables& t, const RowSpec& rs, int num_sms, cudaStream_t s);
+
+// ---------------------------------------------------------------- weighted epilogue helpers
+// x[r][(l,m)] *= w[l] (per-degree scaling, proj/src/gtp.cpp:34-44)
+cudaError_t launch_scale_degrees(const float* in, float* out, int64_t rows, int L, const float* w,
+                                 cudaStream_t s);
+
+}  // namespace tpo_b200

@@ -1,0 +1,54 @@
+"""CPU-side checks of the C-ABI library: it loads without a GPU, exports every
+symbol include/tpo_capi.h declares, and validates arguments / reports errors
+without touching a device (no compute calls here)."""
+import ctypes
+import re
+from pathlib import Path
+
+import pytest
+
+ROOT = Path(__file__).resolve().parents[1]
+
+
+def declared_symbols():
+    text = (ROOT / "include" / "tpo_capi.h").read_text()
+    return sorted(set(re.findall(r"\b(tpo_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_header_symbols_exported():
+    import paper_2506_13523_b200._lib as L
+
+    lib = ctypes.CDLL(str(L.LIB_PATH))
+    syms = declared_symbols()
+    assert len(syms) >= 15
+    for s in syms:
+        assert hasattr(lib, s), s
+    assert set(syms) == set(L.EXPORTED)
+
+
+def test_shapes_without_gpu():
+    import paper_2506_13523_b200 as tpo
+
+    assert tpo.out_dim("cgtp", 2, 2) == 81 and tpo.out_dim("cgtp", 3, 3) == 256
+    assert tpo.out_dim("gtp_grid", 3, 3, 6) == 49
+    assert tpo.out_dim("mtp", 6, 6, 12) == 169
+    assert tpo.mtp_l_tilde(4, 4, 8) == 4 and tpo.mtp_l_tilde(2, 1, 3) == 2
+    with pytest.raises(ValueError):
+        tpo.out_dim("gtp_grid", 2, 2, -1)
+    with pytest.raises(ValueError):
+        tpo.out_dim("cgtp", -1, 2)
+
+
+def test_no_silent_cpu_path():
+    """Without a usable sm_100 device, context creation fails loudly."""
+    import torch
+
+    import paper_2506_13523_b200 as tpo
+
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    with pytest.raises((tpo.TpoError, ValueError)):
+        tpo.Context(0)
+    x = torch.zeros((2, 9)); y = torch.zeros((2, 9))
+    with pytest.raises(ValueError):
+        tpo.gtp_grid(x, y, 2, 2, 4)  # CPU tensors are rejected, never computed on host

@@ -1,0 +1,248 @@
+"""GPU parity: every kernel through the C ABI vs the fp64 CPU oracle.
+
+Contract (north star / SURVEY.md 8(d)): per tensor product, normwise
+max|gpu - ref| / max|ref| <= 1e-5 with the oracle evaluated in fp64 on the
+same fp32-rounded inputs.
+"""
+import math
+
+import numpy as np
+import pytest
+
+TOL = 1e-5  # normwise relative error per TP, fp32 contract
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def tpo():
+    import torch
+
+    assert torch.cuda.is_available()
+    import paper_2506_13523_b200 as m
+
+    return m
+
+
+def _inputs(B, L1, L2, seed, C=None, shared=False):
+    rng = np.random.default_rng(seed)
+    if C is None:
+        x = rng.standard_normal((B, (L1 + 1) ** 2)).astype(np.float32)
+        y = rng.standard_normal((B, (L2 + 1) ** 2)).astype(np.float32)
+    else:
+        x = rng.standard_normal((B, C, (L1 + 1) ** 2)).astype(np.float32)
+        y = rng.standard_normal((B, (L2 + 1) ** 2) if shared else (B, C, (L2 + 1) ** 2)).astype(np.float32)
+    return x, y
+
+
+def _gpu(tpo, kind, x, y, L1, L2, L3, lt=-1):
+    import torch
+
+    xt = torch.from_numpy(x).cuda()
+    yt = torch.from_numpy(y).cuda()
+    out = tpo.run(kind, xt, yt, L1, L2, L3, lt)
+    torch.cuda.synchronize()
+    return out.cpu().numpy().astype(np.float64)
+
+
+def _ref_single(orc, kind, x, y, L1, L2, L3, lt=-1):
+    t1, t2 = orc.tower(L1), orc.tower(L2)
+    x = x.astype(np.float64); y = y.astype(np.float64)
+    if kind == "cgtp":
+        return orc.cgtp_mimo(t1, x, t2, y)
+    if kind == "gtp_grid":
+        return orc.gtp_grid(t1, x, t2, y, L3)
+    if kind == "gtp_fourier":
+        return orc.gtp_fourier(t1, x, t2, y, L3)
+    return orc.mtp(t1, x, t2, y, L3, lt_override=lt)
+
+
+def _normwise(out, ref):
+    out = out.reshape(-1, out.shape[-1]); ref = ref.reshape(-1, ref.shape[-1])
+    scale = np.maximum(np.abs(ref).max(axis=1), 1e-300)
+    return float((np.abs(out - ref).max(axis=1) / scale).max())
+
+
+def _check_batch(tpo, orc, kind, L, B, seed, L3=None):
+    L3 = 2 * L if L3 is None else L3
+    x, y = _inputs(B, L, L, seed)
+    out = _gpu(tpo, kind, x, y, L, L, L3)
+    ref = orc.batch_mimo(kind, L, x.astype(np.float64)[:, None], y.astype(np.float64)[:, None])[:, 0]
+    err = _normwise(out, ref)
+    assert err <= TOL, (kind, L, err)
+    return err
+
+
+# ---------------------------------------------------------------- per kind, L sweep
+@pytest.mark.parametrize("L", list(range(0, 11)))
+def test_gtp_grid_tcgen05(tpo, orc, L):
+    ctx = tpo.context()
+    ctx.set_grid_path("tc")
+    try:
+        _check_batch(tpo, orc, "gtp_grid", L, 1000, 100 + L)
+        assert ctx.last_grid_path == "tcgen05"
+    finally:
+        ctx.set_grid_path("auto")
+
+
+@pytest.mark.parametrize("L", [1, 3, 6, 11, 13, 16])
+def test_gtp_grid_simt(tpo, orc, L):
+    ctx = tpo.context()
+    ctx.set_grid_path("simt")
+    try:
+        _check_batch(tpo, orc, "gtp_grid", L, 64 if L > 10 else 300, 200 + L)
+        assert ctx.last_grid_path == "simt"
+    finally:
+        ctx.set_grid_path("auto")
+
+
+@pytest.mark.parametrize("L", [0, 1, 2, 3, 4, 6, 8])
+def test_cgtp(tpo, orc, L):
+    _check_batch(tpo, orc, "cgtp", L, 257, 300 + L)
+
+
+@pytest.mark.parametrize("L", [12, 16])
+def test_cgtp_large(tpo, orc, L):
+    _check_batch(tpo, orc, "cgtp", L, 8, 310 + L)
+
+
+@pytest.mark.parametrize("L", [0, 1, 2, 4, 6, 8, 10, 16])
+def test_gtp_fourier(tpo, orc, L):
+    _check_batch(tpo, orc, "gtp_fourier", L, 129 if L <= 8 else 16, 400 + L)
+
+
+@pytest.mark.parametrize("L", [0, 1, 2, 3, 6, 10, 16])
+def test_mtp(tpo, orc, L):
+    _check_batch(tpo, orc, "mtp", L, 129 if L <= 8 else 16, 500 + L)
+
+
+# ---------------------------------------------------------------- shapes / edge cases
+def test_ragged_batch_and_empty(tpo, orc):
+    for kind in ("gtp_grid", "cgtp", "gtp_fourier", "mtp"):
+        for B in (1, 127, 129):
+            _check_batch(tpo, orc, kind, 2, B, 600 + B)
+        import torch
+
+        x = torch.empty((0, 9), device="cuda"); y = torch.empty((0, 9), device="cuda")
+        assert tpo.run(kind, x, y, 2, 2, 4).shape[0] == 0
+
+
+@pytest.mark.parametrize("kind", ["cgtp", "gtp_grid", "gtp_fourier", "mtp"])
+def test_unequal_degrees(tpo, orc, kind):
+    L1, L2, L3 = 3, 1, 3
+    x, y = _inputs(40, L1, L2, 700)
+    out = _gpu(tpo, kind, x, y, L1, L2, L3)
+    ref = np.stack([_ref_single(orc, kind, x[b], y[b], L1, L2, L3) for b in range(40)])
+    assert _normwise(out, ref) <= TOL
+
+
+@pytest.mark.parametrize("kind", ["gtp_grid", "gtp_fourier", "mtp"])
+def test_output_band_past_product(tpo, orc, kind):
+    # degrees past the product band are exactly zero (proj/src/gtp.cpp:237-258)
+    x, y = _inputs(33, 1, 1, 710)
+    out = _gpu(tpo, kind, x, y, 1, 1, 5)
+    ref = np.stack([_ref_single(orc, kind, x[b], y[b], 1, 1, 5) for b in range(33)])
+    assert _normwise(out, ref) <= TOL
+    if kind != "mtp":
+        assert np.all(out[:, 9:] == 0.0)
+
+
+def test_channels_shared_y(tpo, orc):
+    # channel-wise CGTP (config C4 shape, small batch): x [B][C][16], y [B][16]
+    L, B, C = 3, 24, 128
+    x, y = _inputs(B, L, L, 720, C=C, shared=True)
+    for kind in ("cgtp", "gtp_grid", "mtp", "gtp_fourier"):
+        out = _gpu(tpo, kind, x, y, L, L, 2 * L)
+        ref = orc.batch_mimo(kind, L, x.astype(np.float64), y.astype(np.float64), channels=C, y_shared=True)
+        assert _normwise(out, ref) <= TOL, kind
+
+
+def test_channels_unshared(tpo, orc):
+    L, B, C = 2, 10, 7
+    x, y = _inputs(B, L, L, 730, C=C, shared=False)
+    for kind in ("cgtp", "gtp_grid"):
+        out = _gpu(tpo, kind, x, y, L, L, 2 * L)
+        ref = orc.batch_mimo(kind, L, x.astype(np.float64), y.astype(np.float64), channels=C, y_shared=False)
+        assert _normwise(out, ref) <= TOL
+
+
+def test_mtp_carrier_override(tpo, orc):
+    x, y = _inputs(50, 2, 2, 740)
+    out = _gpu(tpo, "mtp", x, y, 2, 2, 4, lt=3)
+    ref = np.stack([_ref_single(orc, "mtp", x[b], y[b], 2, 2, 4, lt=3) for b in range(50)])
+    assert _normwise(out, ref) <= TOL
+    with pytest.raises(ValueError):
+        _gpu(tpo, "mtp", x, y, 2, 2, 4, lt=1)
+
+
+# ---------------------------------------------------------------- known answers (reference tests)
+def test_kats(tpo):
+    import torch
+
+    x = torch.tensor([[3.0]], device="cuda"); y = torch.tensor([[-2.0]], device="cuda")
+    # proj/tests/test_gtp.cpp:36-43
+    assert tpo.gtp_grid(x, y, 0, 0, 0).item() == pytest.approx(-6 / math.sqrt(4 * math.pi), rel=1e-6)
+    assert tpo.gtp_fourier(x, y, 0, 0, 0).item() == pytest.approx(-6 / math.sqrt(4 * math.pi), rel=1e-6)
+    # proj/tests/test_mtp.cpp:73-88
+    assert tpo.mtp(x, y, 0, 0, 0).item() == pytest.approx(-6.0, rel=1e-6)
+    assert tpo.mtp(x, y, 0, 0, 0, l_tilde=1).item() == pytest.approx(6 / math.sqrt(3), rel=1e-6)
+    # proj/tests/test_cgtp.cpp:81-104: (0,0,0) path is the plain product
+    assert tpo.cgtp(x, y, 0, 0).item() == pytest.approx(-6.0, rel=1e-6)
+
+
+def test_equivariance(tpo, orc):
+    # SO(3) equivariance of the GPU products (proj/src/verify.cpp:76-117 protocol)
+    rng = orc.Rng(20240901)
+    L = 3
+    t = orc.tower(L)
+    for kind in ("cgtp", "gtp_grid", "gtp_fourier", "mtp"):
+        worst, scale = 0.0, 0.0
+        for _ in range(5):
+            x, y = rng.tower(L), rng.tower(L)
+            R = rng.rotation()
+            rx, ry = orc.rotate(t, x, R), orc.rotate(t, y, R)
+            X = np.stack([x, rx]).astype(np.float32); Y = np.stack([y, ry]).astype(np.float32)
+            out = _gpu(tpo, kind, X, Y, L, L, 2 * L)
+            if kind == "cgtp":
+                out_ls = [l3 for l1 in t for l2 in t for l3 in range(abs(l1 - l2), l1 + l2 + 1)]
+            else:
+                out_ls = orc.tower(2 * L)
+            rhs = orc.rotate(out_ls, out[0], R)
+            worst = max(worst, np.abs(out[1] - rhs).max())
+            scale = max(scale, np.abs(out[0]).max())
+        assert worst / scale < 1e-5, (kind, worst / scale)
+
+
+def test_bad_arguments(tpo):
+    import torch
+
+    x = torch.zeros((4, 9), device="cuda"); y = torch.zeros((4, 9), device="cuda")
+    with pytest.raises(ValueError):
+        tpo.gtp_grid(x, y, 2, 2, -1)
+    with pytest.raises(ValueError):
+        tpo.gtp_grid(x, y, 1, 2, 2)  # x has 9 components, L1=1 means 4
+    with pytest.raises(ValueError):
+        tpo.cgtp(x.cpu(), y.cpu(), 2, 2)
+    with pytest.raises(ValueError):
+        tpo.weighted_gtp(x, y, np.ones(2), np.ones(3), np.ones(5), 2, 2, 4)
+
+
+def test_weighted_gtp(tpo, orc):
+    x, y = _inputs(20, 2, 2, 760)
+    rng = np.random.default_rng(1)
+    a, b, c = rng.standard_normal(3), rng.standard_normal(3), rng.standard_normal(5)
+    import torch
+
+    out = tpo.weighted_gtp(torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda(), a, b, c, 2, 2, 4).cpu().numpy()
+    ref = np.stack([orc.weighted_gtp(orc.tower(2), x[i].astype(np.float64), orc.tower(2),
+                                     y[i].astype(np.float64), a, b, c, 4) for i in range(20)])
+    assert _normwise(out, ref) <= TOL
+
+
+def test_native_library_loaded(tpo, orc):
+    ctx = tpo.context()
+    before = ctx.launches
+    _check_batch(tpo, orc, "gtp_grid", 1, 10, 1)
+    assert ctx.launches > before
+    with open("/proc/self/maps") as f:
+        assert "libtpo_b200.so" in f.read()
