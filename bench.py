@@ -218,23 +218,17 @@ def main():
         torch.cuda.synchronize()
         wall = time.perf_counter() - wall0
     launches = ctx.launches - launches0
+    from paper_2506_13523_b200.dist import gather_checksums, max_over_ranks
+
+    total_ms = max_over_ranks(total_ms, dev)  # device time, max over ranks
     if world > 1:
-        t = torch.tensor([total_ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
         dist.barrier()
     torch.cuda.synchronize()
     ms_per_step = total_ms / args.steps
     value = world * len(LS) * B / (ms_per_step / 1e3)
 
     # result gather after the timed region: per-shard checksums over NCCL
-    cks = torch.stack([outs[L].double().sum() for L in LS]).float()
-    if world > 1:
-        allc = [torch.empty_like(cks) for _ in range(world)]
-        dist.all_gather(allc, cks)
-        checks = [c.cpu().tolist() for c in allc]
-    else:
-        checks = [cks.cpu().tolist()]
+    checks = gather_checksums(torch.stack([outs[L].double().sum() for L in LS]), dev)
 
     peaks = load_peaks()
     tc_peak = peaks["bf16_tflops"] / 3.0  # 3xFP16 split on the fp16/bf16 tensor pipe
@@ -292,11 +286,7 @@ def main():
         t0 = time.perf_counter()
         for _ in range(n_e2e):
             e2e_step()
-        et = (time.perf_counter() - t0) / n_e2e
-        if world > 1:
-            t = torch.tensor([et], device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            et = float(t.item())
+        et = max_over_ranks((time.perf_counter() - t0) / n_e2e, dev)
         e2e = {"value": round(world * len(LS) * B / et, 1), "unit": UNIT,
                "h2d_bytes_per_step": int(sum(2 * B * (L + 1) ** 2 * 4 for L in LS)),
                "d2h_bytes_per_step": int(sum(B * (2 * L + 1) ** 2 * 4 for L in LS)),

@@ -105,6 +105,19 @@ int tpo_run_host_f32(tpo_ctx* ctx, int kind, int L1, int L2, int L3, int l_tilde
                      const float* x_host, const float* y_host, float* out_host, int64_t batch,
                      int64_t channels, int y_shared);
 
+/* Table introspection ------------------------------------------------------
+ * Real-basis CG table of (l1,l2)->l3 as the device kernels use it (mirrors
+ * tpo::cg_real, proj/include/tpo/wigner.hpp:59-64, and the pybind
+ * cg_table, proj/bindings/py_core.cpp:62-72).  With m1 == NULL returns the
+ * entry count; otherwise fills up to `cap` entries and returns the count.
+ * Negative status on error. */
+int tpo_cg_real(int l1, int l2, int l3, int* m1, int* m2, int* m3, double* value, int cap);
+/* Torus Fourier tables of band L (tpo::fourier_tables, proj/include/tpo/gtp.hpp:76):
+ * which = 0 encode (l <= L), 1 decode (l <= 2L).  counts[(lmax+1)^2] per (l,m)
+ * in l*l+m+l order, entries (u, v, re, im) concatenated.  Returns the total
+ * entry count (or a negative status). */
+int tpo_fourier_table(int L, int which, int* counts, int* u, int* v, double* re, double* im, int cap);
+
 /* Kernel selection for GTP-grid (for tests/bench): 0 auto, 1 force the fused
  * tcgen05 kernel (fails if the shape does not fit), 2 force the SIMT
  * separable kernel.  Returns the previous setting. */

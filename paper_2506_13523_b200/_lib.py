@@ -25,7 +25,7 @@ class TpoError(RuntimeError):
 
 
 _lib = None
-_lock = threading.Lock()
+_lock = threading.RLock()  # reentrant: context() -> Context() -> lib()
 
 
 def lib():
@@ -59,6 +59,8 @@ def lib():
             "tpo_run_f32": (i, [p, i, i, i, i, i, p, p, p, i64, i64, i, p]),
             "tpo_run_host_f32": (i, [p, i, i, i, i, i, p, p, p, i64, i64, i]),
             "tpo_set_gtp_grid_path": (i, [p, i]),
+            "tpo_cg_real": (i, [i, i, i, p, p, p, p, i]),
+            "tpo_fourier_table": (i, [i, i, p, p, p, p, p, i]),
             "tpo_last_gtp_grid_path": (i, [p]),
         }
         for name, (res, args) in sig.items():
@@ -73,7 +75,7 @@ EXPORTED = [
     "tpo_last_error", "tpo_version", "tpo_ctx_create", "tpo_ctx_destroy", "tpo_ctx_launches",
     "tpo_tower_dim", "tpo_out_dim", "tpo_mtp_l_tilde", "tpo_cgtp_mimo_f32", "tpo_gtp_grid_f32",
     "tpo_gtp_fourier_f32", "tpo_mtp_f32", "tpo_weighted_gtp_f32", "tpo_run_f32", "tpo_run_host_f32",
-    "tpo_set_gtp_grid_path", "tpo_last_gtp_grid_path",
+    "tpo_set_gtp_grid_path", "tpo_last_gtp_grid_path", "tpo_cg_real", "tpo_fourier_table",
 ]
 
 

@@ -7,6 +7,7 @@
 #include <vector>
 
 #include "host/context.hpp"
+#include "host/tables.hpp"
 
 using tpo_b200::Context;
 using tpo_b200::CudaFailure;
@@ -289,6 +290,48 @@ int tpo_run_host_f32(tpo_ctx* ctx, int kind, int L1, int L2, int L3, int l_tilde
     tpo_b200::cuda_check(cudaMemcpyAsync(out_host, dout_p, no * sizeof(float), cudaMemcpyDeviceToHost, s), "D2H");
     tpo_b200::cuda_check(cudaStreamSynchronize(s), "sync");
   });
+}
+
+int tpo_cg_real(int l1, int l2, int l3, int* m1, int* m2, int* m3, double* value, int cap) {
+  int n = 0;
+  const int st = guarded([&] {
+    if (l1 < 0 || l2 < 0 || l3 < 0) throw InvalidArgument("cg_real: negative degree");
+    if (l1 + l2 + l3 + 1 > 511) throw InvalidArgument("cg_real: degrees too large");
+    const auto& t = tpo_b200::real_cg(l1, l2, l3);
+    n = static_cast<int>(t.size());
+    if (!m1) return;
+    if (cap < n) throw InvalidArgument("cg_real: buffer too small");
+    for (int i = 0; i < n; ++i) {
+      m1[i] = t[i].m1;
+      m2[i] = t[i].m2;
+      m3[i] = t[i].m3;
+      value[i] = t[i].v;
+    }
+  });
+  return st ? -st : n;
+}
+
+int tpo_fourier_table(int L, int which, int* counts, int* u, int* v, double* re, double* im, int cap) {
+  int total = 0;
+  const int st = guarded([&] {
+    if (L < 0 || L > kMaxL) throw InvalidArgument("fourier_tables: L out of range");
+    const auto& t = tpo_b200::fourier_tables(L);
+    const auto& modes = which == 0 ? t.enc : t.dec;
+    for (size_t i = 0; i < modes.size(); ++i) {
+      if (counts) counts[i] = static_cast<int>(modes[i].size());
+      for (const auto& e : modes[i]) {
+        if (u) {
+          if (total >= cap) throw InvalidArgument("fourier_tables: buffer too small");
+          u[total] = e.u;
+          v[total] = e.v;
+          re[total] = e.w.real();
+          im[total] = e.w.imag();
+        }
+        ++total;
+      }
+    }
+  });
+  return st ? -st : total;
 }
 
 int tpo_set_gtp_grid_path(tpo_ctx* ctx, int path) {

@@ -52,3 +52,17 @@ def test_no_silent_cpu_path():
     x = torch.zeros((2, 9)); y = torch.zeros((2, 9))
     with pytest.raises(ValueError):
         tpo.gtp_grid(x, y, 2, 2, 4)  # CPU tensors are rejected, never computed on host
+
+
+def test_context_first_call_does_not_deadlock():
+    """context() before any other library call must not self-deadlock on the
+    loader lock (regression: non-reentrant lock in _lib.context -> lib())."""
+    import subprocess
+    import sys
+
+    code = ("import sys; sys.path.insert(0, %r)\n"
+            "import paper_2506_13523_b200 as t\n"
+            "try:\n    t.context(0)\nexcept Exception as e:\n    print(type(e).__name__)\n"
+            "print('done')" % str(ROOT))
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=120)
+    assert "done" in r.stdout, r.stderr

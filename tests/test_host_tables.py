@@ -1,0 +1,72 @@
+"""The product's own host table builders (paper_2506_13523_b200/csrc/host/
+tables.cpp, exposed through tpo_cg_real / tpo_fourier_table) agree with the
+oracle's independent restatement -- CPU only, no device needed."""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+
+def product_cg(l1, l2, l3):
+    import paper_2506_13523_b200 as tpo
+
+    lib = tpo.lib()
+    n = lib.tpo_cg_real(l1, l2, l3, None, None, None, None, 0)
+    assert n >= 0
+    a = np.empty(n, np.int32); b = np.empty(n, np.int32); c = np.empty(n, np.int32); v = np.empty(n)
+    p = lambda z: z.ctypes.data_as(C.c_void_p)  # noqa: E731
+    assert lib.tpo_cg_real(l1, l2, l3, p(a), p(b), p(c), p(v), n) == n
+    return [(int(i), int(j), int(k), float(x)) for i, j, k, x in zip(a, b, c, v)]
+
+
+def product_fourier(L, which):
+    import paper_2506_13523_b200 as tpo
+
+    lib = tpo.lib()
+    w = 0 if which == "encode" else 1
+    lmax = L if w == 0 else 2 * L
+    counts = np.empty((lmax + 1) ** 2, np.int32)
+    p = lambda z: z.ctypes.data_as(C.c_void_p)  # noqa: E731
+    n = lib.tpo_fourier_table(L, w, p(counts), None, None, None, None, 0)
+    u = np.empty(n, np.int32); v = np.empty(n, np.int32); re = np.empty(n); im = np.empty(n)
+    assert lib.tpo_fourier_table(L, w, p(counts), p(u), p(v), p(re), p(im), n) == n
+    out, k = {}, 0
+    for l in range(lmax + 1):
+        for m in range(-l, l + 1):
+            cnt = int(counts[l * l + m + l])
+            out[(l, m)] = {(int(u[k + i]), int(v[k + i])): complex(re[k + i], im[k + i]) for i in range(cnt)}
+            k += cnt
+    return out
+
+
+def test_real_cg_matches_oracle(orc):
+    worst = 0.0
+    for l1 in range(7):
+        for l2 in range(7):
+            for l3 in range(abs(l1 - l2), l1 + l2 + 1):
+                a = product_cg(l1, l2, l3)
+                b = orc.cg_real(l1, l2, l3)
+                assert [e[:3] for e in a] == [e[:3] for e in b], (l1, l2, l3)
+                worst = max(worst, max(abs(x[3] - y[3]) for x, y in zip(a, b)))
+    assert worst < 1e-14
+    assert product_cg(1, 1, 3) == []
+
+
+def test_real_cg_large_degree(orc):
+    for (l1, l2, l3) in [(16, 16, 32), (16, 16, 7), (12, 9, 10)]:
+        a, b = product_cg(l1, l2, l3), orc.cg_real(l1, l2, l3)
+        assert len(a) == len(b)
+        assert max(abs(x[3] - y[3]) for x, y in zip(a, b)) < 1e-12
+
+
+@pytest.mark.parametrize("L", [0, 1, 3, 6])
+def test_fourier_tables_match_oracle(orc, L):
+    for which in ("encode", "decode"):
+        a = product_fourier(L, which)
+        b = orc.fourier_tables(L, which)
+        for key, ents in b.items():
+            ref = {(u, v): w for u, v, w in ents}
+            got = a[key]
+            # entries near the 1e-13 cut may differ in presence; values must agree
+            for uv in set(ref) | set(got):
+                assert abs(got.get(uv, 0) - ref.get(uv, 0)) < 1e-11, (L, which, key, uv)
