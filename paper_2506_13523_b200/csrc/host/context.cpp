@@ -6,6 +6,8 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "../kernels/sm100.cuh"
@@ -134,6 +136,28 @@ const CgtpTables& Context::cgtp(int L1, int L2) {
 }
 
 // ------------------------------------------------------------------ GTP grid (tcgen05)
+namespace {
+int env_int(const char* name, int dflt) {
+  const char* v = std::getenv(name);
+  return (v && *v) ? std::atoi(v) : dflt;
+}
+// tcgen05.mma cycles for one M = 128, K = 16 instruction of width N, as
+// measured on B200 (tools/ubench/mma_ubench2.cu): single-thread issue floor
+// ~45 cycles, math N / 2 cycles, and operands read from shared memory at
+// ~128 B / cycle (A 4 KB + B 32 N bytes for an SS MMA; B only when A is in TMEM).
+constexpr int kMaxRingStages = 8;
+double mma_ss(int n) { return std::max({45.0, n / 2.0, (4096.0 + 32.0 * n) / 128.0}); }
+double mma_ts(int n) { return std::max({45.0, n / 2.0, 32.0 * n / 128.0}); }
+// GEMM 2 N-split of a group of zg outputs (parts of <= 256 rows, multiple of
+// 16).  Splitting is kept at 1: narrower MMAs leave too little slack over the
+// issue floor to hide the per-stage mbarrier wait (tools/ubench/mma_ubench3.cu).
+int parts_for(int zg) {
+  int np = 1;
+  while (zg / np > 256 || (zg % np) != 0 || ((zg / np) % 16) != 0) ++np;
+  return np;
+}
+}  // namespace
+
 const GridTcEntry& Context::grid_tc(int L1, int L2, int L3) {
   std::lock_guard<std::mutex> g(mu_);
   auto it = grid_tc_.find({L1, L2, L3});
@@ -148,55 +172,113 @@ const GridTcEntry& Context::grid_tc(int L1, int L2, int L3) {
   t.k2p = pad_to(t.din2, 16);
   t.dout_eff = (L3e + 1) * (L3e + 1);
   t.dout_total = (L3 + 1) * (L3 + 1);
-  t.dout_pad = pad_to(t.dout_eff, 16);
   t.same_s = (L1 == L2) ? 1 : 0;
   const S2Grid& gr = s2_grid(band);
   const int G = gr.n_theta * gr.n_phi;
   const int max_smem = gtp_grid_tc_max_smem();
-  auto smem_for = [&](int nc, uint32_t* offs) {
-    uint32_t o = 0;
-    const uint32_t xy = std::max<uint32_t>(512u * (t.k1p + t.k2p), 128u * 33u * 4u);
-    offs[0] = 0;
-    offs[1] = 512u * t.k1p;
-    o = pad_to(static_cast<int>(xy), 128);
-    offs[2] = o;
-    o += pad_to(4 * nc * t.k1p, 128);
-    offs[3] = o;
-    if (!t.same_s) o += pad_to(4 * nc * t.k2p, 128);
-    offs[4] = o;
-    o += pad_to(512 * nc, 128);
-    offs[5] = o;
-    o += pad_to(4 * t.dout_pad * nc, 128);
-    return static_cast<int>(o);
-  };
-  int nc = 0;
-  uint32_t offs[6] = {};
-  if (t.k1p <= 128 && t.k2p <= 128) {
-    for (int cand = 128; cand >= 16; cand -= 16)
-      if (t.dout_pad + 2 * cand <= 512 && smem_for(cand, offs) <= max_smem) {
-        nc = cand;
-        break;
-      }
-  }
-  if (nc == 0) {  // does not fit the fused tiling: SIMT separable kernel handles this shape
+  if (t.k1p > 128 || t.k2p > 128 || max_smem <= 0) {  // SIMT separable kernel handles these shapes
     ent.fits = false;
     return grid_tc_.emplace(std::array<int, 3>{L1, L2, L3}, ent).first->second;
   }
-  t.nchunks = (G + nc - 1) / nc;
-  nc = pad_to((G + t.nchunks - 1) / t.nchunks, 16);  // rebalance padding over chunks
-  t.nc = nc;
-  t.smem_bytes = smem_for(nc, offs);
-  t.off_x = offs[0];
-  t.off_y = offs[1];
-  t.off_s1 = offs[2];
-  t.off_s2 = offs[3];
-  t.off_p = offs[4];
-  t.off_a = offs[5];
-  int cols = 32;
-  while (cols < t.dout_pad + 2 * nc) cols *= 2;
-  t.tmem_cols = cols;
 
-  // dense operators on the product grid (proj/src/sphere.cpp:105-195)
+  // ---- tiling: choose (output groups, chunk width) minimising estimated MMA cycles per tile
+  //   TMEM: zg (Z) + 2 nc (F_x, F_y; P overwrites F_x) <= 512 columns
+  const int force_nc = env_int("TPO_GRID_NC", 0), force_groups = env_int("TPO_GRID_GROUPS", 0);
+  double best = 1e300;
+  int best_g = 0, best_nc = 0, best_chunks = 0, best_zg = 0;
+  for (int ng = 1; ng <= 8; ++ng) {
+    if (force_groups && ng != force_groups) continue;
+    const int zg = pad_to((t.dout_eff + ng - 1) / ng, 16);
+    if (zg > 256) continue;
+    for (int cand = 128; cand >= 16; cand -= 16) {
+      if (force_nc && cand != force_nc) continue;
+      if (zg + 2 * cand > 512) continue;
+      const int nch = (G + cand - 1) / cand;
+      const int nc = pad_to((G + nch - 1) / nch, 16);  // rebalance padding over chunks
+      const int np = parts_for(zg);
+      // + ~60 cycles per ring stage for the mbarrier wait when a stage's MMAs lack slack
+      const double g1 = 3.0 * ((t.k1p + t.k2p) / 16) * mma_ss(nc) +
+                        ((t.k1p + t.k2p) / 16) * std::max(0.0, 60.0 - 3.0 * (mma_ss(nc) - 45.0)) / (t.same_s ? 2 : 1);
+      const double g2 = 3.0 * (nc / 16) * np * mma_ts(zg / np);
+      const double cost = ng * (nch * (g1 + g2 + 400.0) + 1500.0);
+      if (cost < best) {
+        best = cost;
+        best_g = ng;
+        best_nc = nc;
+        best_chunks = nch;
+        best_zg = zg;
+      }
+    }
+  }
+  if (best_g == 0) {
+    ent.fits = false;
+    return grid_tc_.emplace(std::array<int, 3>{L1, L2, L3}, ent).first->second;
+  }
+  const int nc = best_nc;
+  t.nc = nc;
+  t.nchunks = best_chunks;
+  t.nslices = nc / 16;
+  t.ngroups = best_g;
+  t.zg = best_zg;
+  t.nparts = parts_for(t.zg);
+  t.zp = t.zg / t.nparts;
+  t.safe_war = env_int("TPO_GRID_SAFE_WAR", 1);
+  t.dbg = env_int("TPO_GRID_DBG", 0);
+
+  // ---- shared memory: X/Y operands, optional separate raw staging, B ring, epilogue staging
+  const uint32_t xy = 512u * (t.k1p + t.k2p);
+  const uint32_t raw = static_cast<uint32_t>(pad_to(512 * (t.din1 + t.din2), 1024));
+  const uint32_t epi = 8u * 32u * 17u * 4u;
+  const int force_inplace = env_int("TPO_GRID_INPLACE", -1), force_stages = env_int("TPO_GRID_STAGES", 0);
+  // two B-operand rings; prefer the separate raw staging buffer, then depth
+  t.s_stage_bytes = static_cast<uint32_t>(64 * nc);
+  t.a_stage_bytes = static_cast<uint32_t>(64 * t.zp);
+  auto fixed = [&](int ip) { return static_cast<int>(xy + (ip ? 0u : raw) + epi); };
+  int inplace = -1, s_st = 0, a_st = 0;
+  int best_score = -1;
+  for (int ip = 0; ip <= 1; ++ip) {
+    if (force_inplace >= 0 && ip != force_inplace) continue;
+    const int room = max_smem - fixed(ip);
+    for (int ss = 2; ss <= kMaxRingStages; ++ss)
+      for (int sa = 2; sa <= kMaxRingStages; ++sa) {
+        if (force_stages && (ss != force_stages || sa != force_stages)) continue;
+        if (static_cast<int>(ss * t.s_stage_bytes + sa * t.a_stage_bytes) > room) continue;
+        // shallowest ring first; the separate raw buffer (prefetch a whole tile ahead) breaks ties
+        const int score = std::min(std::min(ss, sa), 4) * 100 + (ip == 0 ? 50 : 0) + ss + sa;
+        if (score > best_score) {
+          best_score = score;
+          inplace = ip;
+          s_st = ss;
+          a_st = sa;
+        }
+      }
+  }
+  if (inplace < 0) {
+    ent.fits = false;
+    return grid_tc_.emplace(std::array<int, 3>{L1, L2, L3}, ent).first->second;
+  }
+  t.raw_inplace = inplace;
+  t.s_stages = s_st;
+  t.a_stages = a_st;
+  t.off_x = 0;
+  t.off_y = 256u * t.k1p * 2u;
+  uint32_t o = xy;
+  t.off_raw = inplace ? t.off_x : o;
+  if (!inplace) o += raw;
+  t.off_sring = o;
+  o += s_st * t.s_stage_bytes;
+  t.off_aring = o;
+  o += a_st * t.a_stage_bytes;
+  t.off_stage = o;
+  o += epi;
+  t.smem_bytes = static_cast<int>(o);
+  if (env_int("TPO_GRID_VERBOSE", 0))
+    std::fprintf(stderr,
+                 "[tpo] grid_tc L=(%d,%d,%d) G=%d nc=%d chunks=%d groups=%d zg=%d parts=%d s_stages=%d a_stages=%d "
+                 "inplace=%d smem=%d\n",
+                 L1, L2, L3, G, nc, t.nchunks, t.ngroups, t.zg, t.nparts, s_st, a_st, inplace, t.smem_bytes);
+
+  // ---- dense operators on the product grid (proj/src/sphere.cpp:105-195)
   const double phi_scale = 2.0 * M_PI / gr.n_phi;
   auto s_val = [&](int gidx, int k) -> double {  // S[g][(l,m)]
     const int j = gidx / gr.n_phi, kk = gidx % gr.n_phi;
@@ -206,66 +288,77 @@ const GridTcEntry& Context::grid_tc(int L1, int L2, int L3) {
   };
   double amax = 0.0;
   for (int gidx = 0; gidx < G; ++gidx)
-    for (int o = 0; o < t.dout_eff; ++o) {
+    for (int o2 = 0; o2 < t.dout_eff; ++o2) {
       const int j = gidx / gr.n_phi;
-      amax = std::max(amax, std::abs(gr.weights[j] * phi_scale * s_val(gidx, o)));
+      amax = std::max(amax, std::abs(gr.weights[j] * phi_scale * s_val(gidx, o2)));
     }
   t.a_shift = amax > 0 ? -(std::ilogb(amax) + 1) : 0;
   const double a_scale = std::ldexp(1.0, t.a_shift);
 
+  // S slices: [chunk][kstep][hi | lo][nc x 16 canonical]
   auto build_s = [&](int din, int kp, std::vector<uint16_t>& buf) {
-    const size_t half_elems = static_cast<size_t>(nc) * kp;  // per hi / lo block
-    buf.assign(static_cast<size_t>(t.nchunks) * 2 * half_elems, 0);
-    for (int c = 0; c < t.nchunks; ++c) {
-      uint16_t* hi = buf.data() + static_cast<size_t>(c) * 2 * half_elems;
-      uint16_t* lo = hi + half_elems;
-      for (int r = 0; r < nc; ++r) {
-        const int gidx = c * nc + r;
-        for (int k = 0; k < kp; ++k) {
-          const double v = (gidx < G && k < din) ? s_val(gidx, k) : 0.0;
-          uint16_t h, l;
-          split_half(v, h, l);
-          const uint32_t e = sm100::canon_off(r, k, nc) / 2;
-          hi[e] = h;
-          lo[e] = l;
+    const size_t half = static_cast<size_t>(nc) * 16;  // elements per hi / lo block
+    const int nks = kp / 16;
+    buf.assign(static_cast<size_t>(t.nchunks) * nks * 2 * half, 0);
+    for (int c = 0; c < t.nchunks; ++c)
+      for (int ks = 0; ks < nks; ++ks) {
+        uint16_t* hi = buf.data() + (static_cast<size_t>(c) * nks + ks) * 2 * half;
+        uint16_t* lo = hi + half;
+        for (int r = 0; r < nc; ++r) {
+          const int gidx = c * nc + r;
+          for (int kk = 0; kk < 16; ++kk) {
+            const int k = ks * 16 + kk;
+            const double v = (gidx < G && k < din) ? s_val(gidx, k) : 0.0;
+            uint16_t hv, lv;
+            split_half(v, hv, lv);
+            const uint32_t e = sm100::canon_off(r, kk, nc) / 2;
+            hi[e] = hv;
+            lo[e] = lv;
+          }
         }
       }
-    }
   };
   std::vector<uint16_t> s1, s2, a;
   build_s(t.din1, t.k1p, s1);
-  t.s1_chunk_bytes = static_cast<uint32_t>(4u * nc * t.k1p);
+  t.s1_slice_bytes = static_cast<uint32_t>(64 * nc);
   t.s1 = reinterpret_cast<const uint8_t*>(upload(s1));
   if (t.same_s) {
     t.s2 = t.s1;
-    t.s2_chunk_bytes = t.s1_chunk_bytes;
+    t.s2_slice_bytes = t.s1_slice_bytes;
   } else {
     build_s(t.din2, t.k2p, s2);
-    t.s2_chunk_bytes = static_cast<uint32_t>(4u * nc * t.k2p);
+    t.s2_slice_bytes = static_cast<uint32_t>(64 * nc);
     t.s2 = reinterpret_cast<const uint8_t*>(upload(s2));
   }
+  // A slices: [group][chunk][slice][part][hi | lo][zp x 16 canonical]
   {
-    const size_t half_elems = static_cast<size_t>(t.dout_pad) * nc;
-    a.assign(static_cast<size_t>(t.nchunks) * 2 * half_elems, 0);
-    for (int c = 0; c < t.nchunks; ++c) {
-      uint16_t* hi = a.data() + static_cast<size_t>(c) * 2 * half_elems;
-      uint16_t* lo = hi + half_elems;
-      for (int o = 0; o < t.dout_pad; ++o)
-        for (int r = 0; r < nc; ++r) {
-          const int gidx = c * nc + r;
-          double v = 0.0;
-          if (gidx < G && o < t.dout_eff) {
-            const int j = gidx / gr.n_phi;
-            v = gr.weights[j] * phi_scale * s_val(gidx, o) * a_scale;
+    const size_t half = static_cast<size_t>(t.zp) * 16;
+    a.assign(static_cast<size_t>(t.ngroups) * t.nchunks * t.nslices * t.nparts * 2 * half, 0);
+    for (int gp = 0; gp < t.ngroups; ++gp)
+      for (int c = 0; c < t.nchunks; ++c)
+        for (int sl = 0; sl < t.nslices; ++sl)
+          for (int pt = 0; pt < t.nparts; ++pt) {
+            const size_t blk = ((static_cast<size_t>(gp) * t.nchunks + c) * t.nslices + sl) * t.nparts + pt;
+            uint16_t* hi = a.data() + blk * 2 * half;
+            uint16_t* lo = hi + half;
+            for (int rr = 0; rr < t.zp; ++rr) {
+              const int o2 = gp * t.zg + pt * t.zp + rr;
+              for (int kk = 0; kk < 16; ++kk) {
+                const int gidx = c * nc + sl * 16 + kk;
+                double v = 0.0;
+                if (gidx < G && o2 < t.dout_eff && pt * t.zp + rr < t.zg) {
+                  const int j = gidx / gr.n_phi;
+                  v = gr.weights[j] * phi_scale * s_val(gidx, o2) * a_scale;
+                }
+                uint16_t hv, lv;
+                split_half(v, hv, lv);
+                const uint32_t e = sm100::canon_off(rr, kk, t.zp) / 2;
+                hi[e] = hv;
+                lo[e] = lv;
+              }
+            }
           }
-          uint16_t h, l;
-          split_half(v, h, l);
-          const uint32_t e = sm100::canon_off(o, r, t.dout_pad) / 2;
-          hi[e] = h;
-          lo[e] = l;
-        }
-    }
-    t.a_chunk_bytes = static_cast<uint32_t>(4u * t.dout_pad * nc);
+    t.a_slice_bytes = static_cast<uint32_t>(64 * t.zp);
     t.a = reinterpret_cast<const uint8_t*>(upload(a));
   }
   ent.fits = true;

@@ -2,30 +2,34 @@
 //
 // Reference path: tpo::detail::gtp_grid_select (proj/src/gtp.cpp:228-260) =
 // to_sphere (proj/src/sphere.cpp:105-134) x2, pointwise_mul (:145-151),
-// from_sphere_select (:155-195).  Per tile of 128 samples this kernel does
-//   F_x = X S1^T,  F_y = Y S2^T        (SH -> grid, GEMM 1, TMEM accumulators)
-//   P   = F_x (.) F_y                  (pointwise product, registers)
-//   Z  += P A^T                        (grid -> SH quadrature, GEMM 2, TMEM)
-// chunk by chunk over the grid points, so grid values never leave the SM.
-// S[g][(l,m)] = Lambda_{l|m|}(theta_j) cs_m(phi_k) and
-// A[(l,m)][g] = w_j (2 pi / n_phi) Lambda_{l|m|}(theta_j) cs_m(phi_k) are
-// built by host/context.cpp on the reference's product grid (band L1+L2).
+// from_sphere_select (:155-195).  Per 128-row tile and output group g:
+//   F_x = X S1^T,  F_y = Y S2^T     (SH -> grid, GEMM 1, TMEM accumulators)
+//   P   = F_x (.) F_y               (pointwise product, written back to TMEM)
+//   Z_g += P A_g^T                  (grid -> SH quadrature, GEMM 2, A from TMEM)
+// chunk by chunk (nc grid points) over the product grid, so grid values never
+// leave the SM.  S[g][(l,m)] = Lambda_{l|m|}(theta_j) cs_m(phi_k) and
+// A[(l,m)][g] = w_j (2 pi / n_phi) Lambda_{l|m|}(theta_j) cs_m(phi_k) are built
+// by host/context.cpp on the reference's product grid (band L1+L2).
 //
-// Precision: "3xFP16".  Every fp32 operand v is split v = hi + lo with hi, lo
-// fp16 (11 significant bits each) and products use hi*hi + hi*lo + lo*hi on
-// kind::f16 tcgen05.mma with fp32 accumulation (dropped lo*lo ~ 2^-22 rel).
-// fp16's exponent range is made safe by power-of-two normalisation: each
-// input row is scaled by 2^-e so that ||x||_2 in [0.5, 1) (|F| is then
-// bounded by (L+1)/sqrt(4 pi) by the addition theorem), the A table by
-// 2^a_shift, and the output is rescaled by 2^(ex + ey - a_shift) exactly.
+// Precision: "3xFP16".  Every fp32 operand v is split v = hi + lo (fp16 each)
+// and products use hi*hi + hi*lo + lo*hi with fp32 accumulation.  fp16's
+// range is made safe by exact power-of-two scaling: each input row is scaled
+// so that ||x||_2 in [0.5, 1) (|F| <= (L+1)/sqrt(4 pi) by the addition
+// theorem), the A table by 2^a_shift; the epilogue rescales exactly.
 //
-// Data movement: operands for one grid chunk are pre-tiled on the host in
-// the UMMA canonical K-major (SWIZZLE_NONE) layout and streamed into shared
-// memory with one 1D TMA bulk copy each (cp.async.bulk -> UBLKCP), tracked
-// by mbarrier transaction counts.  X/Y tiles stay resident for the whole
-// chunk loop.  One elected thread issues all tcgen05.mma; completion is
-// signalled through tcgen05.commit -> mbarrier.
+// Warp roles (one persistent CTA per SM, 10 warps):
+//   warp 0     TMA producer: B-operand slices (S / A tables, one K-step each)
+//              through an mbarrier ring; raw input tiles (1D bulk copies).
+//   warp 1     MMA issuer (one thread) + TMEM owner.
+//   warps 2-9  workers: input conversion (norm, split, canonical layout),
+//              pointwise product TMEM -> TMEM, epilogue TMEM -> HBM.
+// MMA shapes are M = 128 and N >= 96 wherever possible: the tcgen05 issue
+// floor measured on B200 is ~45 cycles per instruction (tools/ubench), so
+// narrow MMAs would be issue-bound.
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
 
 #include "kernels.hpp"
 #include "sm100.cuh"
@@ -35,70 +39,63 @@ using namespace sm100;
 
 namespace {
 
-constexpr int BM = 128;          // samples per tile == TMEM lanes == threads
-constexpr int kStageStride = 33; // epilogue staging row pitch (floats)
+constexpr int BM = 128;            // rows per tile == TMEM lanes
+constexpr int kWorkerWarps = 8;
+constexpr int kWorkers = kWorkerWarps * 32;
+constexpr int kThreads = 96 + kWorkers;  // + producer A warp (warp 10)
+constexpr int kKHalfMax = 64;      // input K (padded) <= 128, split over 2 threads per row
+constexpr int kStageStride = 17;   // epilogue staging row pitch (floats)
+constexpr int kMaxStages = 8;
+constexpr int kMaxSlices = 8;      // nc <= 128
 
-__device__ __forceinline__ float warp_sum(float v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
+// barrier slots: two B-operand rings (S table for GEMM 1, A table for GEMM 2),
+// each fed by its own producer warp -- a single thread issues at most one
+// bulk copy per ~250 cycles (tools/ubench/tma_ubench.cu)
+constexpr int B_SFULL = 0;
+constexpr int B_SEMPTY = B_SFULL + kMaxStages;
+constexpr int B_AFULL = B_SEMPTY + kMaxStages;
+constexpr int B_AEMPTY = B_AFULL + kMaxStages;
+constexpr int B_RAW_FULL = B_AEMPTY + kMaxStages;
+constexpr int B_RAW_FREE = B_RAW_FULL + 1;
+constexpr int B_XY_FREE = B_RAW_FREE + 1;
+constexpr int B_XY_READY = B_XY_FREE + 1;
+constexpr int B_F_FULL = B_XY_READY + 1;
+constexpr int B_P_READY = B_F_FULL + 1;
+constexpr int B_G2_DONE = B_P_READY + kMaxSlices;
+constexpr int B_Z_FULL = B_G2_DONE + 1;
+constexpr int B_Z_EMPTY = B_Z_FULL + 1;
+constexpr int kNumBars = B_Z_EMPTY + 1;
+
+struct Unit {
+  int64_t tile;
+  int g;
+};
+
+__device__ __forceinline__ Unit unit_of(int64_t u, int ngroups) {
+  return Unit{u / ngroups, static_cast<int>(u % ngroups)};
 }
 
-// Load a 128-row tile of one input, normalise each row by a power of two
-// (||row||_2 -> [0.5, 1)), split into fp16 hi/lo and store both in the
-// canonical K-major layout (R = 128, K = kp).  Warp w handles rows
-// [32w, 32w+32); lanes walk k so global loads are coalesced.
-__device__ __forceinline__ void load_split_tile(const float* __restrict__ src, int64_t row0,
-                                                const RowSpec& rs, bool is_y, int din, int kp,
-                                                uint8_t* hi, uint8_t* lo, int* e_out) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int rr = 0; rr < 32; ++rr) {
-    const int r = warp * 32 + rr;
-    const int64_t g = row0 + r;
-    const bool valid = g < rs.rows;
-    const int64_t srow = (is_y && rs.y_shared) ? g / rs.channels : g;
-    const float* p = src + (valid ? srow : 0) * din;
-    float v[4];
-    float ss = 0.f;
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int k = lane + 32 * q;
-      v[q] = (valid && k < din) ? __ldg(p + k) : 0.f;
-      ss = fmaf(v[q], v[q], ss);
-    }
-    ss = warp_sum(ss);
-    int e = 0;
-    if (ss > 0.f && ss < 3.0e38f) e = ilogbf(sqrtf(ss)) + 1;
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int k = lane + 32 * q;
-      if (k < kp) {
-        const float xs = scalbnf(v[q], -e);
-        const __half h = __float2half_rn(xs);
-        const __half l = __float2half_rn(xs - __half2float(h));
-        const uint32_t off = canon_off(r, k, BM);
-        *reinterpret_cast<__half*>(hi + off) = h;
-        *reinterpret_cast<__half*>(lo + off) = l;
-      }
-    }
-    if (lane == 0) e_out[r] = e;
-  }
+// CTA b owns the contiguous unit range [u_begin, u_end): consecutive units
+// are the output groups of one tile, which then reuses its resident X / Y
+__device__ __forceinline__ void unit_range(int64_t nunits, int64_t& u_begin, int64_t& u_end) {
+  u_begin = nunits * blockIdx.x / gridDim.x;
+  u_end = nunits * (blockIdx.x + 1) / gridDim.x;
 }
 
-// D(128 x N) (+)= A(128 x K) B(N x K)^T in 3xFP16: hi*hi + hi*lo + lo*hi.
-// Operands are canonical K-major with row-group stride 128 B and K-core
-// stride a_lbo / b_lbo.  Issued by one thread.
-__device__ __forceinline__ void gemm3x(uint32_t d, uint32_t a_hi, uint32_t a_lo, uint32_t a_lbo,
-                                       uint32_t b_hi, uint32_t b_lo, uint32_t b_lbo, int K,
-                                       uint32_t idesc, bool zero_first) {
-  for (int ks = 0; ks < K / 16; ++ks) {
-    const uint32_t ao = ks * 2 * a_lbo, bo = ks * 2 * b_lbo;
-    const uint64_t ah = make_sdesc(a_hi + ao, a_lbo, 128), al = make_sdesc(a_lo + ao, a_lbo, 128);
-    const uint64_t bh = make_sdesc(b_hi + bo, b_lbo, 128), bl = make_sdesc(b_lo + bo, b_lbo, 128);
-    mma_f16_ss(d, ah, bh, idesc, (zero_first && ks == 0) ? 0u : 1u);
-    mma_f16_ss(d, ah, bl, idesc, 1u);
-    mma_f16_ss(d, al, bh, idesc, 1u);
-  }
+// a tile whose x / y rows are one contiguous, 16-byte aligned block can be
+// fetched with two bulk copies; anything else (tail tile, shared y, odd base
+// pointer) is gathered by the workers
+__device__ __forceinline__ bool tile_tma_ok(const RowSpec& rs, int64_t tile) {
+  return !rs.y_shared && (tile + 1) * BM <= rs.rows && ((reinterpret_cast<uintptr_t>(rs.x) & 15) == 0) &&
+         ((reinterpret_cast<uintptr_t>(rs.y) & 15) == 0);
+}
+
+// 2^k for |k| <= 126, exact (exponent bits)
+__device__ __forceinline__ float pow2i(int k) { return __int_as_float((127 + k) << 23); }
+// v * 2^k, exact for |k| <= 252 unless the result itself is subnormal
+__device__ __forceinline__ float mul_pow2(float v, int k) {
+  const int k1 = k >> 1;
+  return (v * pow2i(k1)) * pow2i(k - k1);
 }
 
 __device__ __forceinline__ uint32_t pack_half2(float a, float b) {
@@ -106,189 +103,506 @@ __device__ __forceinline__ uint32_t pack_half2(float a, float b) {
   return *reinterpret_cast<const uint32_t*>(&h);
 }
 
-__global__ void __launch_bounds__(BM, 1)
-    gtp_grid_tc_kernel(const __grid_constant__ GridTcTables t, const __grid_constant__ RowSpec rs) {
-  extern __shared__ __align__(128) uint8_t smem[];
-  __shared__ __align__(8) uint64_t bars[4];
-  __shared__ uint32_t tmem_sh;
-  __shared__ int ex_sh[BM], ey_sh[BM];
-  uint64_t* bar_s = &bars[0];   // S chunk landed (TMA)
-  uint64_t* bar_a = &bars[1];   // A chunk landed (TMA)
-  uint64_t* bar_g1 = &bars[2];  // GEMM 1 of the chunk retired
-  uint64_t* bar_g2 = &bars[3];  // GEMM 2 of the chunk retired
-
-  const int tid = threadIdx.x, warp = tid >> 5;
-  if (tid == 0) {
+// Convert one input of the tile: raw fp32 rows [128][din] in shared memory ->
+// fp16 hi / lo in the canonical K-major layout (R = 128, K = kp), each row
+// scaled by 2^-e with ||row||_2 * 2^-e in [0.5, 1).  Thread (r, h) owns half
+// h of row r.  Two phases separated by a worker barrier, so the raw rows may
+// alias the destination (in-place mode).
+__device__ __noinline__ void convert_input(const float* raw, int din, int kp, uint8_t* dst_hi, uint8_t* dst_lo,
+                                              float* part, int* e_out, int r, int h, bool wait_free,
+                                              uint64_t* xy_free, uint32_t xy_free_par) {
+  const int kh = kp >> 1;  // multiple of 8
+  const int k0 = h * kh;
+  const float* src = raw + r * din + k0;
+  const int nv = min(kh, din - k0);  // valid raw values of this half (may be <= 0)
+  float v[kKHalfMax];
+  float ss = 0.f;
 #pragma unroll
-    for (int i = 0; i < 4; ++i) mbar_init(&bars[i], 1);
+  for (int j0 = 0; j0 < kKHalfMax; j0 += 8) {
+    if (j0 < kh) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        v[j0 + q] = (j0 + q < nv) ? src[j0 + q] : 0.f;
+        ss = fmaf(v[j0 + q], v[j0 + q], ss);
+      }
+    }
+  }
+  part[h * BM + r] = ss;
+  named_bar_sync(1, kWorkers);
+  if (wait_free) mbar_wait(xy_free, xy_free_par);  // the previous unit's GEMM 1 has retired
+  const float tot = part[r] + part[BM + r];
+  int e = 0;
+  if (tot > 0.f && tot < 3.0e38f) e = max(-120, min(120, ilogbf(tot) / 2 + 1));
+  // |x| * 2^-e <= 2: fp16 hi/lo stay normal for the row's dominant entries
+  const float sc = pow2i(-e);
+#pragma unroll
+  for (int j0 = 0; j0 < kKHalfMax; j0 += 8) {
+    if (j0 < kh) {
+      uint32_t hw[4], lw[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float a0 = v[j0 + 2 * q] * sc, a1 = v[j0 + 2 * q + 1] * sc;
+        const __half2 hh = __floats2half2_rn(a0, a1);
+        const float2 hf = __half22float2(hh);
+        hw[q] = *reinterpret_cast<const uint32_t*>(&hh);
+        lw[q] = pack_half2(a0 - hf.x, a1 - hf.y);
+      }
+      const uint32_t off = canon_off(r, k0 + j0, BM);
+      *reinterpret_cast<uint4*>(dst_hi + off) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+      *reinterpret_cast<uint4*>(dst_lo + off) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+    }
+  }
+  if (h == 0) e_out[r] = e;
+}
+
+// Optional per-role cycle accounting (PROF = true; debugging aid, env
+// TPO_GRID_PROF=1): slot layout per CTA in `g_prof` (unsigned long long):
+//   MMA thread : 0 total, 1 wait xy_ready, 2 wait S ring, 3 wait p_ready, 4 wait z_empty, 5 wait g2_done,
+//                6 wait A ring
+//   worker w2  : 8 total, 9 wait f_full, 10 product, 11 convert, 12 wait z_full, 13 epilogue
+constexpr int kProfSlots = 16;
+__device__ unsigned long long* g_prof = nullptr;
+
+template <bool PROF>
+__global__ void __launch_bounds__(kThreads, 1)
+    gtp_grid_tc_kernel(const __grid_constant__ GridTcTables t, const __grid_constant__ RowSpec rs) {
+  unsigned long long pc[kProfSlots];
+#pragma unroll
+  for (int k = 0; k < kProfSlots; ++k) pc[k] = 0;
+  auto now = []() -> unsigned long long { return PROF ? clock64() : 0ull; };
+  const unsigned long long t_start = now();
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ __align__(8) uint64_t bars[kNumBars];
+  __shared__ uint32_t tmem_sh;
+  __shared__ int ex_sh[2][BM], ey_sh[2][BM];
+  __shared__ float part_sh[2 * BM];
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
+    for (int i = 0; i < kNumBars; ++i) {
+      uint32_t cnt = 1;
+      if (i == B_RAW_FREE || i == B_XY_READY || i == B_Z_EMPTY) cnt = kWorkers;
+      if (i >= B_P_READY && i < B_P_READY + kMaxSlices) cnt = BM;
+      mbar_init(&bars[i], cnt);
+    }
     fence_mbar_init();
   }
-  if (warp == 0) {
-    tmem_alloc(&tmem_sh, t.tmem_cols);
+  if (warp == 1) {
+    tmem_alloc(&tmem_sh, 512);
     tmem_relinquish();
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = tmem_sh;
-  const uint32_t lane_base = tmem + (static_cast<uint32_t>(warp * 32) << 16);
-  const int fx0 = t.dout_pad, fy0 = t.dout_pad + t.nc;
 
+  const int64_t ntiles = (rs.rows + BM - 1) / BM;
+  const int64_t nunits = ntiles * t.ngroups;
+  int64_t u_begin, u_end;
+  unit_range(nunits, u_begin, u_end);
   uint8_t* xh = smem + t.off_x;
   uint8_t* xl = xh + BM * t.k1p * 2;
   uint8_t* yh = smem + t.off_y;
   uint8_t* yl = yh + BM * t.k2p * 2;
-  uint8_t* s1 = smem + t.off_s1;
-  uint8_t* s2 = t.same_s ? s1 : smem + t.off_s2;
-  uint8_t* pb = smem + t.off_p;
-  uint8_t* ab = smem + t.off_a;
-  const uint32_t p_half = BM * t.nc * 2;
-  const uint32_t s1_half = t.nc * t.k1p * 2, s2_half = t.nc * t.k2p * 2;
-  const uint32_t a_half = t.dout_pad * t.nc * 2;
-  const uint32_t lbo_m = (BM / 8) * 128;          // X, Y, P (R = 128)
-  const uint32_t lbo_s = (t.nc / 8) * 128;        // S chunk (R = nc)
-  const uint32_t lbo_a = (t.dout_pad / 8) * 128;  // A chunk (R = dout_pad)
-  const uint32_t id1 = idesc_f16(BM, t.nc);
+  float* raw_x = reinterpret_cast<float*>(smem + t.off_raw);
+  float* raw_y = t.raw_inplace ? reinterpret_cast<float*>(smem + t.off_y) : raw_x + BM * t.din1;
+  uint8_t* sring = smem + t.off_sring;
+  uint8_t* aring = smem + t.off_aring;
+  const uint32_t zc = static_cast<uint32_t>(t.zg);   // TMEM: Z [0, zg), F_x [zc, zc+nc), F_y [zc+nc, zc+2nc)
+  const uint32_t fx = zc, fy = zc + t.nc;
 
-  uint32_t ph_s = 0, ph_a = 0, ph_g1 = 0, ph_g2 = 0;
-  const int64_t ntiles = (rs.rows + BM - 1) / BM;
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const int64_t row0 = tile * BM;
-    if (tid == 0) {  // chunk 0 operands; every MMA of the previous tile has retired
-      mbar_arrive_expect_tx(bar_s, t.s1_chunk_bytes + (t.same_s ? 0u : t.s2_chunk_bytes));
-      bulk_g2s(s1, t.s1, t.s1_chunk_bytes, bar_s);
-      if (!t.same_s) bulk_g2s(s2, t.s2, t.s2_chunk_bytes, bar_s);
-      mbar_arrive_expect_tx(bar_a, t.a_chunk_bytes);
-      bulk_g2s(ab, t.a, t.a_chunk_bytes, bar_a);
+  if (warp == 0) {
+    // ===================================================== TMA producer
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t ph = 0;
+      auto push = [&](const uint8_t* src, uint32_t bytes) {
+        mbar_wait(&bars[B_SEMPTY + stage], ph ^ 1);
+        mbar_arrive_expect_tx(&bars[B_SFULL + stage], bytes);
+        bulk_g2s(sring + stage * t.s_stage_bytes, src, bytes, &bars[B_SFULL + stage]);
+        if (++stage == t.s_stages) {
+          stage = 0;
+          ph ^= 1;
+        }
+      };
+      // raw tile number v of this CTA: the destination must be free, i.e. tile
+      // v-1's last GEMM 1 retired (in-place: raw lands in the X/Y operand
+      // buffers) or the workers finished reading raw tile v-1 (separate buffer)
+      auto issue_raw = [&](int64_t tile, int64_t v) {
+        if (v > 0) mbar_wait(&bars[t.raw_inplace ? B_XY_FREE : B_RAW_FREE], static_cast<uint32_t>((v - 1) & 1));
+        const uint32_t bx = BM * t.din1 * 4, by = BM * t.din2 * 4;
+        mbar_arrive_expect_tx(&bars[B_RAW_FULL], bx + by);
+        bulk_g2s(raw_x, rs.x + tile * BM * t.din1, bx, &bars[B_RAW_FULL]);
+        bulk_g2s(raw_y, rs.y + tile * BM * t.din2, by, &bars[B_RAW_FULL]);
+      };
+      int64_t v = 0;  // tile sequence number
+      if (u_begin < u_end) {
+        const Unit u0 = unit_of(u_begin, t.ngroups);
+        if (tile_tma_ok(rs, u0.tile)) issue_raw(u0.tile, 0);
+      }
+      for (int64_t u = u_begin; u < u_end; ++u) {
+        const Unit cu = unit_of(u, t.ngroups);
+        const bool first_of_tile = (u == u_begin) || unit_of(u - 1, t.ngroups).tile != cu.tile;
+        const bool last_of_tile = (u + 1 == u_end) || unit_of(u + 1, t.ngroups).tile != cu.tile;
+        // the next tile of this CTA starts right after this tile's units
+        const int64_t next_u = u + (t.ngroups - cu.g);
+        const bool has_next = next_u < u_end;
+        for (int c = 0; c < t.nchunks; ++c) {
+          for (int ks = 0; ks < t.k1p / 16; ++ks)
+            push(t.s1 + static_cast<size_t>(c * (t.k1p / 16) + ks) * t.s1_slice_bytes, t.s1_slice_bytes);
+          if (!t.same_s)
+            for (int ks = 0; ks < t.k2p / 16; ++ks)
+              push(t.s2 + static_cast<size_t>(c * (t.k2p / 16) + ks) * t.s2_slice_bytes, t.s2_slice_bytes);
+          const bool raw_point = t.raw_inplace ? (last_of_tile && c == t.nchunks - 1) : (first_of_tile && c == 0);
+          if (raw_point && has_next) {
+            const Unit nu = unit_of(next_u, t.ngroups);
+            if (tile_tma_ok(rs, nu.tile)) issue_raw(nu.tile, v + 1);
+          }
+        }
+        if (last_of_tile) ++v;
+      }
     }
-    load_split_tile(rs.x, row0, rs, false, t.din1, t.k1p, xh, xl, ex_sh);
-    load_split_tile(rs.y, row0, rs, true, t.din2, t.k2p, yh, yl, ey_sh);
-    fence_proxy_async_smem();
-    __syncthreads();
-
-    for (int c = 0; c < t.nchunks; ++c) {
-      if (tid == 0) {
-        mbar_wait(bar_s, ph_s);
+  } else if (warp == 10) {
+    // ===================================================== TMA producer, A table (GEMM 2)
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t ph = 0;
+      for (int64_t u = u_begin; u < u_end; ++u) {
+        const Unit cu = unit_of(u, t.ngroups);
+        const size_t abase = static_cast<size_t>(cu.g) * t.nchunks * t.nslices * t.nparts;
+        const int n = t.nchunks * t.nslices * t.nparts;
+        for (int k = 0; k < n; ++k) {
+          mbar_wait(&bars[B_AEMPTY + stage], ph ^ 1);
+          mbar_arrive_expect_tx(&bars[B_AFULL + stage], t.a_slice_bytes);
+          bulk_g2s(aring + stage * t.a_stage_bytes, t.a + (abase + k) * t.a_slice_bytes, t.a_slice_bytes,
+                   &bars[B_AFULL + stage]);
+          if (++stage == t.a_stages) {
+            stage = 0;
+            ph ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ===================================================== MMA issuer
+    if (lane == 0) {
+      int s_stage = 0, a_stage = 0;
+      uint32_t s_ph = 0, a_ph = 0;
+      // next slice of a ring: wait until it landed, return its shared-memory address
+      auto take_s = [&](uint32_t& slot) -> uint32_t {
+        slot = B_SEMPTY + s_stage;
+        const auto t0 = now();
+        mbar_wait(&bars[B_SFULL + s_stage], s_ph);
+        pc[2] += now() - t0;
         tc_fence_after();
-        gemm3x(tmem + fx0, smem_u32(xh), smem_u32(xl), lbo_m, smem_u32(s1), smem_u32(s1) + s1_half, lbo_s,
-               t.k1p, id1, true);
-        gemm3x(tmem + fy0, smem_u32(yh), smem_u32(yl), lbo_m, smem_u32(s2), smem_u32(s2) + s2_half, lbo_s,
-               t.k2p, id1, true);
-        tc_commit(bar_g1);
-      }
-      ph_s ^= 1;
-      if (c > 0) {
-        if (tid == 0) {  // GEMM 2 of chunk c-1 retired: A buffer free -> prefetch A[c]
-          mbar_wait(bar_g2, ph_g2);
-          mbar_arrive_expect_tx(bar_a, t.a_chunk_bytes);
-          bulk_g2s(ab, t.a + static_cast<size_t>(c) * t.a_chunk_bytes, t.a_chunk_bytes, bar_a);
+        const uint32_t a = smem_u32(sring + s_stage * t.s_stage_bytes);
+        if (++s_stage == t.s_stages) {
+          s_stage = 0;
+          s_ph ^= 1;
         }
-        ph_g2 ^= 1;
-      }
-      mbar_wait(bar_g1, ph_g1);
-      ph_g1 ^= 1;
-      tc_fence_after();
-      if (tid == 0 && c + 1 < t.nchunks) {  // S buffer free -> prefetch S[c+1]
-        mbar_arrive_expect_tx(bar_s, t.s1_chunk_bytes + (t.same_s ? 0u : t.s2_chunk_bytes));
-        bulk_g2s(s1, t.s1 + static_cast<size_t>(c + 1) * t.s1_chunk_bytes, t.s1_chunk_bytes, bar_s);
-        if (!t.same_s)
-          bulk_g2s(s2, t.s2 + static_cast<size_t>(c + 1) * t.s2_chunk_bytes, t.s2_chunk_bytes, bar_s);
-      }
-      // pointwise product on the grid chunk, split to fp16 hi/lo -> P (A operand of GEMM 2)
-      for (int j0 = 0; j0 < t.nc; j0 += 16) {
-        uint32_t fx[16], fy[16];
-        tmem_ld16(lane_base + fx0 + j0, fx);
-        tmem_ld16(lane_base + fy0 + j0, fy);
-        tmem_wait_ld();
-        uint32_t hw[8], lw[8];
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          const float a0 = __uint_as_float(fx[2 * q]) * __uint_as_float(fy[2 * q]);
-          const float a1 = __uint_as_float(fx[2 * q + 1]) * __uint_as_float(fy[2 * q + 1]);
-          const __half2 h = __floats2half2_rn(a0, a1);
-          const float2 hf = __half22float2(h);
-          hw[q] = *reinterpret_cast<const uint32_t*>(&h);
-          lw[q] = pack_half2(a0 - hf.x, a1 - hf.y);
+        return a;
+      };
+      auto take_a = [&](uint32_t& slot) -> uint32_t {
+        slot = B_AEMPTY + a_stage;
+        const auto t0 = now();
+        mbar_wait(&bars[B_AFULL + a_stage], a_ph);
+        pc[6] += now() - t0;
+        tc_fence_after();
+        const uint32_t a = smem_u32(aring + a_stage * t.a_stage_bytes);
+        if (++a_stage == t.a_stages) {
+          a_stage = 0;
+          a_ph ^= 1;
         }
-        const uint32_t o0 = canon_off(tid, j0, BM), o1 = canon_off(tid, j0 + 8, BM);
-        *reinterpret_cast<uint4*>(pb + o0) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
-        *reinterpret_cast<uint4*>(pb + o1) = make_uint4(hw[4], hw[5], hw[6], hw[7]);
-        *reinterpret_cast<uint4*>(pb + p_half + o0) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
-        *reinterpret_cast<uint4*>(pb + p_half + o1) = make_uint4(lw[4], lw[5], lw[6], lw[7]);
+        return a;
+      };
+      const uint32_t id1 = idesc_f16(BM, t.nc), id2 = idesc_f16(BM, t.zp);
+      const uint32_t lbo_x = (BM / 8) * 128;
+      const uint32_t lbo_s = (t.nc / 8) * 128, lbo_a = (t.zp / 8) * 128;
+      const uint32_t s_half = t.nc * 32, a_half = t.zp * 32;  // lo block offset inside a slice
+      const uint64_t dx_hi = make_sdesc(smem_u32(xh), lbo_x, 128), dx_lo = make_sdesc(smem_u32(xl), lbo_x, 128);
+      const uint64_t dy_hi = make_sdesc(smem_u32(yh), lbo_x, 128), dy_lo = make_sdesc(smem_u32(yl), lbo_x, 128);
+      const uint64_t kstep_x = (2 * lbo_x) >> 4;  // descriptor advance per K-step of X/Y
+      int64_t j = 0;  // chunk counter
+      int64_t i = 0;  // unit counter
+      int64_t v = 0;  // tile sequence number
+      for (int64_t u = u_begin; u < u_end; ++u, ++i) {
+        const Unit cu = unit_of(u, t.ngroups);
+        const bool first_of_tile = (u == u_begin) || unit_of(u - 1, t.ngroups).tile != cu.tile;
+        const bool last_of_tile = (u + 1 == u_end) || unit_of(u + 1, t.ngroups).tile != cu.tile;
+        if (first_of_tile) {
+          const auto t0 = now();
+          mbar_wait(&bars[B_XY_READY], static_cast<uint32_t>(v & 1));
+          pc[1] += now() - t0;
+          tc_fence_after();
+        }
+        for (int c = 0; c < t.nchunks; ++c, ++j) {
+          if (j > 0 && t.safe_war) {  // P of the previous chunk (in F_x) consumed
+            const auto t0 = now();
+            mbar_wait(&bars[B_G2_DONE], static_cast<uint32_t>((j - 1) & 1));
+            pc[5] += now() - t0;
+            tc_fence_after();
+          }
+          // ---- GEMM 1: F_x = X S1^T, F_y = Y S2^T (3xFP16)
+          const int ks1 = t.k1p / 16;
+          for (int ks = 0; ks < ks1; ++ks) {
+            uint32_t slot;
+            const uint32_t sb = take_s(slot);
+            const uint64_t bh = make_sdesc(sb, lbo_s, 128), bl = make_sdesc(sb + s_half, lbo_s, 128);
+            const uint64_t ah = dx_hi + ks * kstep_x, al = dx_lo + ks * kstep_x;
+            const uint32_t acc = ks > 0 ? 1u : 0u;
+            mma_f16_ss(tmem + fx, ah, bh, id1, acc);
+            mma_f16_ss(tmem + fx, ah, bl, id1, 1u);
+            mma_f16_ss(tmem + fx, al, bh, id1, 1u);
+            if (t.same_s) {
+              const uint64_t yh_ = dy_hi + ks * kstep_x, yl_ = dy_lo + ks * kstep_x;
+              mma_f16_ss(tmem + fy, yh_, bh, id1, acc);
+              mma_f16_ss(tmem + fy, yh_, bl, id1, 1u);
+              mma_f16_ss(tmem + fy, yl_, bh, id1, 1u);
+            }
+            tc_commit(&bars[slot]);
+          }
+          if (!t.same_s) {
+            for (int ks = 0; ks < t.k2p / 16; ++ks) {
+              uint32_t slot;
+              const uint32_t sb = take_s(slot);
+              const uint32_t s2_half = t.nc * 32;
+              const uint64_t bh = make_sdesc(sb, lbo_s, 128), bl = make_sdesc(sb + s2_half, lbo_s, 128);
+              const uint64_t ah = dy_hi + ks * kstep_x, al = dy_lo + ks * kstep_x;
+              const uint32_t acc = ks > 0 ? 1u : 0u;
+              mma_f16_ss(tmem + fy, ah, bh, id1, acc);
+              mma_f16_ss(tmem + fy, ah, bl, id1, 1u);
+              mma_f16_ss(tmem + fy, al, bh, id1, 1u);
+              tc_commit(&bars[slot]);
+            }
+          }
+          tc_commit(&bars[B_F_FULL]);
+          if (c == t.nchunks - 1 && last_of_tile) tc_commit(&bars[B_XY_FREE]);
+          // ---- GEMM 2: Z += P A^T, P (hi/lo fp16) read from TMEM in place of F_x
+          if (c == 0 && i > 0) {  // previous unit's epilogue has drained Z
+            const auto t0 = now();
+            mbar_wait(&bars[B_Z_EMPTY], static_cast<uint32_t>((i - 1) & 1));
+            pc[4] += now() - t0;
+            tc_fence_after();
+          }
+          for (int s = 0; s < t.nslices; ++s) {
+            { const auto t0 = now(); mbar_wait(&bars[B_P_READY + s], static_cast<uint32_t>(j & 1)); pc[3] += now() - t0; }
+            const uint32_t p_hi = tmem + fx + 16 * s, p_lo = p_hi + 8;
+            for (int pt = 0; pt < t.nparts; ++pt) {
+              uint32_t slot;
+              const uint32_t sb = take_a(slot);
+              const uint64_t bh = make_sdesc(sb, lbo_a, 128), bl = make_sdesc(sb + a_half, lbo_a, 128);
+              const uint32_t zd = tmem + pt * t.zp;
+              mma_f16_ts(zd, p_hi, bh, id2, (c == 0 && s == 0) ? 0u : 1u);
+              mma_f16_ts(zd, p_hi, bl, id2, 1u);
+              mma_f16_ts(zd, p_lo, bh, id2, 1u);
+              tc_commit(&bars[slot]);
+            }
+          }
+          tc_commit(&bars[B_G2_DONE]);
+        }
+        tc_commit(&bars[B_Z_FULL]);
+        if (last_of_tile) ++v;
       }
-      tc_fence_before();
+      pc[0] = now() - t_start;
+      if (PROF) for (int k = 0; k < 8; ++k) g_prof[blockIdx.x * kProfSlots + k] = pc[k];
+    }
+  } else {
+    // ===================================================== workers
+    const int q = warp & 3;                // TMEM lane quarter of this warp
+    const int h = (warp - 2) >> 2;         // worker half: 0 (warps 2-5) or 1 (warps 6-9)
+    const int r = q * 32 + lane;           // tile row == TMEM lane
+    const int wt = tid - 64;               // 0..255
+    const uint32_t lane_base = tmem + (static_cast<uint32_t>(q * 32) << 16);
+    float* stage = reinterpret_cast<float*>(smem + t.off_stage) + (warp - 2) * 32 * kStageStride;
+    uint32_t n_raw = 0;
+    int64_t j = 0;
+
+    auto convert = [&](int64_t u, int64_t iu) {
+      const Unit cu = unit_of(u, t.ngroups);
+      const int buf = static_cast<int>(iu & 1);
+      const bool tma = tile_tma_ok(rs, cu.tile);
+      named_bar_sync(1, kWorkers);  // part_sh / raw of the previous conversion fully consumed
+      if (tma) {
+        mbar_wait(&bars[B_RAW_FULL], n_raw & 1);
+        ++n_raw;
+      } else {
+        // gather path: the raw region must be free (in-place: previous GEMM 1 retired)
+        if (t.raw_inplace && iu > 0) mbar_wait(&bars[B_XY_FREE], static_cast<uint32_t>((iu - 1) & 1));
+        const int64_t row0 = cu.tile * BM;
+        for (int idx = wt; idx < BM * t.din1; idx += kWorkers) {
+          const int rr = idx / t.din1;
+          raw_x[idx] = (row0 + rr < rs.rows) ? __ldg(rs.x + row0 * t.din1 + idx) : 0.f;
+        }
+        for (int idx = wt; idx < BM * t.din2; idx += kWorkers) {
+          const int rr = idx / t.din2, kk = idx - rr * t.din2;
+          const int64_t g = row0 + rr;
+          const int64_t yr = rs.y_shared ? g / rs.channels : g;
+          raw_y[idx] = (g < rs.rows) ? __ldg(rs.y + yr * t.din2 + kk) : 0.f;
+        }
+        named_bar_sync(1, kWorkers);
+      }
+      const bool wait_free = iu > 0;
+      const uint32_t par = static_cast<uint32_t>((iu - 1) & 1);
+      if (t.dbg & 4) {
+        if (wait_free) mbar_wait(&bars[B_XY_FREE], par);
+        if (!t.raw_inplace) mbar_arrive(&bars[B_RAW_FREE]);
+      } else if (t.raw_inplace) {
+        convert_input(raw_x, t.din1, t.k1p, xh, xl, part_sh, ex_sh[buf], r, h, wait_free, &bars[B_XY_FREE], par);
+        named_bar_sync(1, kWorkers);
+        convert_input(raw_y, t.din2, t.k2p, yh, yl, part_sh, ey_sh[buf], r, h, false, &bars[B_XY_FREE], par);
+      } else {
+        // both inputs are read before the raw buffer is handed back to the producer
+        convert_input(raw_x, t.din1, t.k1p, xh, xl, part_sh, ex_sh[buf], r, h, wait_free, &bars[B_XY_FREE], par);
+        named_bar_sync(1, kWorkers);
+        convert_input(raw_y, t.din2, t.k2p, yh, yl, part_sh, ey_sh[buf], r, h, false, &bars[B_XY_FREE], par);
+        mbar_arrive(&bars[B_RAW_FREE]);
+      }
       fence_proxy_async_smem();
-      __syncthreads();
-      if (tid == 0) {
-        mbar_wait(bar_a, ph_a);
-        tc_fence_after();
-        for (int n0 = 0; n0 < t.dout_pad; n0 += 256) {
-          const int nn = min(256, t.dout_pad - n0);
-          const uint32_t bo = (n0 / 8) * 128;
-          gemm3x(tmem + n0, smem_u32(pb), smem_u32(pb) + p_half, lbo_m, smem_u32(ab) + bo,
-                 smem_u32(ab) + a_half + bo, lbo_a, t.nc, idesc_f16(BM, nn), c == 0);
-        }
-        tc_commit(bar_g2);
-      }
-      ph_a ^= 1;
-    }
+      mbar_arrive(&bars[B_XY_READY]);
+    };
 
-    // ---- epilogue: TMEM -> registers -> rescale -> smem stage -> coalesced stores
-    mbar_wait(bar_g2, ph_g2);
-    ph_g2 ^= 1;
-    tc_fence_after();
-    float* stage = reinterpret_cast<float*>(smem + t.off_x);
-    const int e_row = ex_sh[tid] + ey_sh[tid] - t.a_shift;
-    for (int c0 = 0; c0 < t.dout_total; c0 += 32) {
-      uint32_t r0[16], r1[16];
+    int64_t i = 0;  // unit counter
+    int64_t v = 0;  // tile sequence number
+    { const auto t0 = now(); if (u_begin < u_end) convert(u_begin, 0); pc[11] += now() - t0; }
+    for (int64_t u = u_begin; u < u_end; ++u, ++i) {
+      const Unit cu = unit_of(u, t.ngroups);
+      const bool last_of_tile = (u + 1 == u_end) || unit_of(u + 1, t.ngroups).tile != cu.tile;
+      const int buf = static_cast<int>(v & 1);  // ex/ey of this unit's tile
+      // ---- pointwise product, chunk by chunk; P overwrites F_x slice by slice
+      for (int c = 0; c < t.nchunks; ++c, ++j) {
+        { const auto t0 = now(); mbar_wait(&bars[B_F_FULL], static_cast<uint32_t>(j & 1)); pc[9] += now() - t0; }
+        tc_fence_after();
+        const auto tp0 = now();
+        for (int s = h; s < t.nslices; s += 2) {
+          if (t.dbg & 1) {
+            mbar_arrive(&bars[B_P_READY + s]);
+            continue;
+          }
+          uint32_t vx[16], vy[16];
+          tmem_ld16(lane_base + fx + 16 * s, vx);
+          tmem_ld16(lane_base + fy + 16 * s, vy);
+          tmem_wait_ld();
+          uint32_t hw[8], lw[8];
 #pragma unroll
-      for (int q = 0; q < 16; ++q) r0[q] = r1[q] = 0u;
-      if (c0 < t.dout_pad) tmem_ld16(lane_base + c0, r0);
-      if (c0 + 16 < t.dout_pad) tmem_ld16(lane_base + c0 + 16, r1);
-      tmem_wait_ld();
-#pragma unroll
-      for (int q = 0; q < 16; ++q) {
-        stage[tid * kStageStride + q] = (c0 + q < t.dout_eff) ? scalbnf(__uint_as_float(r0[q]), e_row) : 0.f;
-        stage[tid * kStageStride + 16 + q] =
-            (c0 + 16 + q < t.dout_eff) ? scalbnf(__uint_as_float(r1[q]), e_row) : 0.f;
+          for (int qq = 0; qq < 8; ++qq) {
+            const float a0 = __uint_as_float(vx[2 * qq]) * __uint_as_float(vy[2 * qq]);
+            const float a1 = __uint_as_float(vx[2 * qq + 1]) * __uint_as_float(vy[2 * qq + 1]);
+            const __half2 hh = __floats2half2_rn(a0, a1);
+            const float2 hf = __half22float2(hh);
+            hw[qq] = *reinterpret_cast<const uint32_t*>(&hh);
+            lw[qq] = pack_half2(a0 - hf.x, a1 - hf.y);
+          }
+          tmem_st8(lane_base + fx + 16 * s, hw);
+          tmem_st8(lane_base + fx + 16 * s + 8, lw);
+          tmem_wait_st();
+          tc_fence_before();
+          mbar_arrive(&bars[B_P_READY + s]);
+        }
+        pc[10] += now() - tp0;
       }
-      __syncthreads();
-      for (int i = tid; i < BM * 32; i += BM) {
-        const int r = i >> 5, cc = i & 31;
-        const int64_t g = row0 + r;
-        const int col = c0 + cc;
-        if (g < rs.rows && col < t.dout_total) rs.out[g * t.dout_total + col] = stage[r * kStageStride + cc];
+      // ---- next unit's inputs (overlaps this unit's last GEMM 2)
+      if (last_of_tile && u + 1 < u_end) {
+        const auto t0 = now();
+        convert(u + 1, v + 1);
+        pc[11] += now() - t0;
+      }
+      // ---- epilogue: Z -> registers -> rescale -> staging -> coalesced row-segment stores
+      { const auto t0 = now(); mbar_wait(&bars[B_Z_FULL], static_cast<uint32_t>(i & 1)); pc[12] += now() - t0; }
+      const auto te0 = now();
+      tc_fence_after();
+      const int e_row = ex_sh[buf][r] + ey_sh[buf][r] - t.a_shift;
+      const int64_t row0 = cu.tile * BM + q * 32;
+      const int col0 = cu.g * t.zg;
+      const int col_end = min(col0 + t.zg, t.dout_eff);
+      const int nblk = t.zg / 16;
+      const int half_lane = lane >> 4, cl = lane & 15;
+      for (int cb = h; cb < ((t.dbg & 2) ? 0 : nblk); cb += 2) {
+        uint32_t v0[16];
+        tmem_ld16(lane_base + cb * 16, v0);
+        tmem_wait_ld();
+#pragma unroll
+        for (int qq = 0; qq < 16; ++qq) stage[lane * kStageStride + qq] = mul_pow2(__uint_as_float(v0[qq]), e_row);
+        __syncwarp();
+        // two rows per store instruction: lanes 0-15 row rr, lanes 16-31 row rr + 1
+        const int col = col0 + cb * 16 + cl;
+        if (col < col_end) {
+          float* op = rs.out + (row0 + half_lane) * t.dout_total + col;
+          const int64_t rows_left = rs.rows - row0 - half_lane;
+#pragma unroll 4
+          for (int rr = 0; rr < 32; rr += 2) {
+            if (rr < rows_left) op[static_cast<int64_t>(rr) * t.dout_total] = stage[(rr + half_lane) * kStageStride + cl];
+          }
+        }
+        __syncwarp();
       }
       tc_fence_before();
-      __syncthreads();
+      mbar_arrive(&bars[B_Z_EMPTY]);
+      pc[13] += now() - te0;
+      // degrees past the product band are exactly zero (proj/src/gtp.cpp:237-258)
+      if (cu.g == t.ngroups - 1 && t.dout_total > t.dout_eff && h == 0) {
+        for (int rr = 0; rr < 32; ++rr) {
+          const int64_t g = row0 + rr;
+          if (g >= rs.rows) break;
+          for (int col = t.dout_eff + lane; col < t.dout_total; col += 32) rs.out[g * t.dout_total + col] = 0.f;
+        }
+      }
+      if (last_of_tile) ++v;
     }
+    pc[8] = now() - t_start;
+    if (PROF && warp == 2 && lane == 0)
+      for (int k = 8; k < kProfSlots; ++k) g_prof[blockIdx.x * kProfSlots + k] = pc[k];
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  if (warp == 0) tmem_dealloc(tmem, t.tmem_cols);
+  if (warp == 1) tmem_dealloc(tmem, 512);
 }
 
 }  // namespace
 
 int gtp_grid_tc_max_smem() {
-  // 227 KB opt-in minus the kernel's static shared memory
-  return 232448 - static_cast<int>(4 * 8 + 4 + 2 * BM * 4) - 64;
+  cudaFuncAttributes a{};
+  if (cudaFuncGetAttributes(&a, gtp_grid_tc_kernel<false>) != cudaSuccess) return 0;
+  int dev = 0, optin = 0;
+  cudaGetDevice(&dev);
+  if (cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess) return 0;
+  return optin - static_cast<int>(a.sharedSizeBytes) - 1024;  // slack for the 1 KB dynamic alignment
 }
 
 cudaError_t launch_gtp_grid_tc(const GridTcTables& t, const RowSpec& rs, int num_sms, cudaStream_t s) {
   if (rs.rows <= 0) return cudaSuccess;
-  cudaError_t e = cudaFuncSetAttribute(gtp_grid_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       t.smem_bytes);
+  static const bool prof = [] {
+    const char* v = std::getenv("TPO_GRID_PROF");
+    return v && *v == '1';
+  }();
+  auto kern = prof ? gtp_grid_tc_kernel<true> : gtp_grid_tc_kernel<false>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, t.smem_bytes);
   if (e != cudaSuccess) return e;
-  int occ = 1;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gtp_grid_tc_kernel, BM, t.smem_bytes);
-  if (e != cudaSuccess) return e;
-  occ = std::max(1, std::min(occ, 512 / t.tmem_cols));  // TMEM columns per SM
-  const int64_t ntiles = (rs.rows + BM - 1) / BM;
-  const int grid = static_cast<int>(std::min<int64_t>(ntiles, static_cast<int64_t>(num_sms) * occ));
-  gtp_grid_tc_kernel<<<grid, BM, t.smem_bytes, s>>>(t, rs);
-  return cudaGetLastError();
+  const int64_t units = ((rs.rows + BM - 1) / BM) * t.ngroups;
+  const int grid = static_cast<int>(std::min<int64_t>(units, num_sms));
+  unsigned long long* buf = nullptr;
+  if (prof) {
+    cudaMalloc(&buf, sizeof(unsigned long long) * kProfSlots * grid);
+    cudaMemset(buf, 0, sizeof(unsigned long long) * kProfSlots * grid);
+    cudaMemcpyToSymbol(g_prof, &buf, sizeof(buf));
+  }
+  kern<<<grid, kThreads, t.smem_bytes, s>>>(t, rs);
+  e = cudaGetLastError();
+  if (prof && e == cudaSuccess) {
+    std::vector<unsigned long long> h(kProfSlots * grid);
+    cudaStreamSynchronize(s);
+    cudaMemcpy(h.data(), buf, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+    double avg[kProfSlots] = {};
+    for (int b = 0; b < grid; ++b)
+      for (int k = 0; k < kProfSlots; ++k) avg[k] += static_cast<double>(h[b * kProfSlots + k]) / grid;
+    std::fprintf(stderr,
+                 "[tpo-prof] units=%lld grid=%d MMA: total %.0f xy_ready %.0f s_ring %.0f p_ready %.0f z_empty %.0f "
+                 "g2_done %.0f a_ring %.0f | worker: total %.0f f_full %.0f product %.0f convert %.0f z_full %.0f epilogue %.0f\n",
+                 static_cast<long long>(units), grid, avg[0], avg[1], avg[2], avg[3], avg[4], avg[5], avg[6], avg[8], avg[9],
+                 avg[10], avg[11], avg[12], avg[13]);
+    cudaFree(buf);
+  }
+  return e;
 }
 
 }  // namespace tpo_b200

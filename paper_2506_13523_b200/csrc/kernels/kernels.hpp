@@ -34,26 +34,34 @@ struct CgtpTables {
 cudaError_t launch_cgtp(const CgtpTables& t, const RowSpec& rs, cudaStream_t s);
 
 // ---------------------------------------------------------------- GTP grid, tcgen05
-// Operands pre-split into fp16 hi/lo and pre-tiled in the UMMA canonical
-// K-major layout, one contiguous block per grid chunk:
-//   s[c]  : [2 (hi,lo)][nc rows (grid pts)][kp] canonical, R = nc
-//   a[c]  : [2 (hi,lo)][dout_pad rows (outputs)][nc] canonical, R = dout_pad
+// Dense operators of the reference's product grid, pre-split into fp16 hi/lo
+// and pre-tiled on the host in the UMMA canonical K-major layout, one
+// contiguous block per MMA K-step ("slice") so that every ring stage of the
+// kernel is a single 1D TMA bulk copy:
+//   s1[c][ks] : [hi | lo] x [nc rows (grid points of chunk c)][16 (K = (l,m) 16ks..)]
+//   a[g][c][s][p]: [hi | lo] x [zp rows (outputs p*zp.. of group g)][16 (K = grid points 16s..)]
+// Work unit = (128-row tile, output group g); the grid is swept in chunks of
+// nc points (N of GEMM 1, K of GEMM 2).
 struct GridTcTables {
   int din1, din2, k1p, k2p;  // input dims, K padded to 16
-  int nc, nchunks;           // grid points per chunk, chunks
+  int nc, nchunks, nslices;  // grid points per chunk (multiple of 16), chunks, nc / 16
+  int ngroups, zg;           // output groups, outputs per group (padded to 16, <= 256)
+  int nparts, zp;            // GEMM 2 N-split: zg = nparts * zp, zp <= 128 (keeps ring stages small)
   int dout_eff;              // outputs computed (degrees <= min(L3, band))
   int dout_total;            // (L3+1)^2 written (zeros past the band)
-  int dout_pad;              // dout_eff padded to 16
   int a_shift;               // device A = A * 2^a_shift
-  int tmem_cols;             // power of two >= dout_pad + 2*nc
-  int smem_bytes;
   int same_s;                // s2 == s1 (L1 == L2)
+  int s_stages, a_stages;    // B-operand rings (S table -> GEMM 1, A table -> GEMM 2), one producer warp each
+  uint32_t s_stage_bytes, a_stage_bytes;
+  int raw_inplace;           // raw input tiles land in the X/Y operand buffers
+  int safe_war;              // wait for GEMM 2 of chunk c before GEMM 1 of chunk c+1
+  int dbg;                   // timing experiments only (results invalid): 1 no product, 2 no epilogue, 4 no convert
+  int smem_bytes;
+  uint32_t off_x, off_y, off_raw, off_sring, off_aring, off_stage;  // dynamic shared-memory carve-up
   const uint8_t* s1;
   const uint8_t* s2;
   const uint8_t* a;
-  uint32_t s1_chunk_bytes, s2_chunk_bytes, a_chunk_bytes;
-  // shared-memory carve-up (byte offsets)
-  uint32_t off_x, off_y, off_s1, off_s2, off_p, off_a;
+  uint32_t s1_slice_bytes, s2_slice_bytes, a_slice_bytes;
 };
 cudaError_t launch_gtp_grid_tc(const GridTcTables& t, const RowSpec& rs, int num_sms, cudaStream_t s);
 int gtp_grid_tc_max_smem();

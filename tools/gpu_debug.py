@@ -52,7 +52,7 @@ if __name__ == "__main__":
     which = sys.argv[1] if len(sys.argv) > 1 else "all"
     if which in ("all", "grid"):
         for L in range(0, 11):
-            run("gtp_grid", L, path="tc", timeout=90)
+            run("gtp_grid", L, path="tc", timeout=45)
     if which in ("all", "simt"):
         for L in (1, 3, 6, 11, 16):
             run("gtp_grid", L, B=200, path="simt")
