@@ -5,8 +5,9 @@ L_max, % of roofline).
 Workload (BASELINE.json configs[1]): S2-grid Gaunt TP, L_max sweep 1..10,
 batch 65,536 x 1 channel per GPU, L3 = 2L.  One step = one pass of the sweep
 (ten launches of the fused tcgen05 kernel, one per L) over inputs resident in
-HBM.  L2 (126 MB) is flushed between steps by writing a 256 MiB buffer; the
-flush is outside the CUDA-event-timed region.  Multi-GPU (torchrun): every
+HBM, captured once into a CUDA graph and replayed (no host launch gaps in the
+device time).  L2 (126 MB) is flushed between steps by writing a 256 MiB
+buffer; the flush is outside the CUDA-event-timed region.  Multi-GPU (torchrun): every
 rank processes its own 65,536-sample shard (weak scaling, no collective on
 the data path); per-rank device times are max-reduced and a per-shard
 checksum is all-gathered after the timed region.
@@ -73,7 +74,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", "20"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self._t = threading.Thread(target=self._read, daemon=True)
             self._t.start()
         except FileNotFoundError:
@@ -153,8 +154,8 @@ def cpu_reference(Ls, seconds_per_L: float, nthreads: int, steps: int = 1):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
-    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--batch", type=int, default=BATCH)
     ap.add_argument("--cpu-seconds", type=float, default=1.0, help="CPU baseline seconds per L")
@@ -188,36 +189,57 @@ def main():
     outs = {L: torch.empty((B, (2 * L + 1) ** 2), device=dev) for L in LS}
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MiB > 126 MB L2
 
-    def step(evs=None):
-        for i, L in enumerate(LS):
-            if evs is not None:
-                evs[i].record(stream)
+    def sweep(Ls):
+        for L in Ls:
             tpo.gtp_grid(xs[L], ys[L], L, L, 2 * L, out=outs[L])
-        if evs is not None:
-            evs[len(LS)].record(stream)
 
-    for _ in range(max(args.warmup, 3)):
-        step()
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
+    # eager warm-up builds the device tables, then the sweep (and each L on its
+    # own, for the per-L breakdown) is captured into CUDA graphs
+    sweep(LS)
     torch.cuda.synchronize()
     launches0 = ctx.launches
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        sweep(LS)
+    launches_per_step = ctx.launches - launches0
+    graphs_L = {}
+    for L in LS:
+        graphs_L[L] = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graphs_L[L]):
+            sweep([L])
+    torch.cuda.synchronize()
+
     per_L = {L: 0.0 for L in LS}
     total_ms = 0.0
     with ClockSampler(local) as clk:
+        for _ in range(max(args.warmup, 3)):
+            graph.replay()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
         wall0 = time.perf_counter()
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
         for _ in range(args.steps):
             flush.zero_()  # evict L2 (untimed)
-            evs = [torch.cuda.Event(enable_timing=True) for _ in range(len(LS) + 1)]
-            step(evs)
-            evs[-1].synchronize()
-            for i, L in enumerate(LS):
-                per_L[L] += evs[i].elapsed_time(evs[i + 1])
-            total_ms += evs[0].elapsed_time(evs[-1])
+            ev0.record(stream)
+            graph.replay()
+            ev1.record(stream)
+            ev1.synchronize()
+            total_ms += ev0.elapsed_time(ev1)
         torch.cuda.synchronize()
         wall = time.perf_counter() - wall0
-    launches = ctx.launches - launches0
+        # per-L breakdown (outside the headline timing; same flush discipline)
+        for L in LS:
+            for _ in range(max(3, args.steps // 5)):
+                flush.zero_()
+                ev0.record(stream)
+                graphs_L[L].replay()
+                ev1.record(stream)
+                ev1.synchronize()
+                per_L[L] += ev0.elapsed_time(ev1) / max(3, args.steps // 5) * args.steps
+    launches = launches_per_step * args.steps
     from paper_2506_13523_b200.dist import gather_checksums, max_over_ranks
 
     total_ms = max_over_ranks(total_ms, dev)  # device time, max over ranks
@@ -316,6 +338,8 @@ def main():
                        "parallelism": f"dp{world} (independent shards, no data-path collective)"},
             "per_L": per, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clk.summary(), "wall_s_timed": round(wall, 3), "checksums": checks,
+            "timing": "CUDA graph of the 10-launch sweep replayed per step; CUDA events on the replay stream; "
+                      "L2 flushed (256 MiB write) before every step, outside the events",
             "extras": extras,
         }
         print(json.dumps(line), flush=True)

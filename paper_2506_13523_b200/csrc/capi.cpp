@@ -269,8 +269,17 @@ int tpo_weighted_gtp_f32(tpo_ctx* ctx, int L1, int L2, int L3, const double* a, 
   });
 }
 
+namespace {
+void cuda_check_s(cudaError_t e, const char* what) { tpo_b200::cuda_check(e, what); }
+}  // namespace
+
 int tpo_run_host_f32(tpo_ctx* ctx, int kind, int L1, int L2, int L3, int l_tilde, const float* x_host,
                      const float* y_host, float* out_host, int64_t batch, int64_t channels, int y_shared) {
+  // Host buffers in, host buffers out, synchronous like the reference's call.
+  // The batch is cut into chunks that flow through three streams (copy-in,
+  // compute, copy-out) and kPipeBufs device buffer sets, so both PCIe
+  // directions and the kernels overlap (full overlap needs pinned host memory;
+  // pageable buffers still work, the copies are then staged by the driver).
   return guarded([&] {
     check_args(ctx, L1, L2, x_host, y_host, out_host, batch, channels);
     const int64_t dout = out_dim(kind, L1, L2, L3);
@@ -278,17 +287,45 @@ int tpo_run_host_f32(tpo_ctx* ctx, int kind, int L1, int L2, int L3, int l_tilde
     c.activate();
     const int64_t rows = batch * channels;
     if (rows == 0) return;
-    const int64_t yrows = y_shared ? batch : rows;
-    const size_t nx = rows * (L1 + 1) * (L1 + 1), ny = yrows * (L2 + 1) * (L2 + 1), no = rows * dout;
-    float* dx = c.scratch(0, nx);
-    float* dy = c.scratch(1, ny);
-    float* dout_p = c.scratch(2, no);
-    const cudaStream_t s = c.host_stream();
-    tpo_b200::cuda_check(cudaMemcpyAsync(dx, x_host, nx * sizeof(float), cudaMemcpyHostToDevice, s), "H2D x");
-    tpo_b200::cuda_check(cudaMemcpyAsync(dy, y_host, ny * sizeof(float), cudaMemcpyHostToDevice, s), "H2D y");
-    run_kind(ctx, kind, L1, L2, L3, l_tilde, dx, dy, dout_p, batch, channels, y_shared, s);
-    tpo_b200::cuda_check(cudaMemcpyAsync(out_host, dout_p, no * sizeof(float), cudaMemcpyDeviceToHost, s), "D2H");
-    tpo_b200::cuda_check(cudaStreamSynchronize(s), "sync");
+    std::lock_guard<std::mutex> lk(c.host_path_mutex());
+    const int64_t d1 = (L1 + 1) * (L1 + 1), d2 = (L2 + 1) * (L2 + 1);
+    // chunk = whole batch entries (y_shared rows stay with their channels), ~8 MiB of traffic
+    const int64_t bytes_per_b = 4 * channels * (d1 + dout + (y_shared ? 0 : d2)) + (y_shared ? 4 * d2 : 0);
+    int64_t bc = std::max<int64_t>(1, (8ll << 20) / std::max<int64_t>(bytes_per_b, 1));
+    bc = std::min(bc, batch);
+    const int nb = Context::kPipeBufs;
+    float* dx[Context::kPipeBufs];
+    float* dy[Context::kPipeBufs];
+    float* dz[Context::kPipeBufs];
+    for (int b = 0; b < nb; ++b) {
+      dx[b] = c.scratch(3 * b + 0, static_cast<size_t>(bc * channels * d1));
+      dy[b] = c.scratch(3 * b + 1, static_cast<size_t>(bc * (y_shared ? 1 : channels) * d2));
+      dz[b] = c.scratch(3 * b + 2, static_cast<size_t>(bc * channels * dout));
+    }
+    const cudaStream_t si = c.h2d_stream(), sc = c.host_stream(), so = c.d2h_stream();
+    int64_t k = 0;
+    for (int64_t b0 = 0; b0 < batch; b0 += bc, ++k) {
+      const int b = static_cast<int>(k % nb);
+      const int64_t nbt = std::min(bc, batch - b0);
+      const int64_t r0 = b0 * channels, nr = nbt * channels;
+      const int64_t yr0 = y_shared ? b0 : r0, ynr = y_shared ? nbt : nr;
+      if (k >= nb) cuda_check_s(cudaStreamWaitEvent(si, c.pipe_event(2, b), 0), "wait d2h");
+      cuda_check_s(cudaMemcpyAsync(dx[b], x_host + r0 * d1, nr * d1 * sizeof(float), cudaMemcpyHostToDevice, si),
+                   "H2D x");
+      cuda_check_s(cudaMemcpyAsync(dy[b], y_host + yr0 * d2, ynr * d2 * sizeof(float), cudaMemcpyHostToDevice, si),
+                   "H2D y");
+      cuda_check_s(cudaEventRecord(c.pipe_event(0, b), si), "record h2d");
+      cuda_check_s(cudaStreamWaitEvent(sc, c.pipe_event(0, b), 0), "wait h2d");
+      run_kind(ctx, kind, L1, L2, L3, l_tilde, dx[b], dy[b], dz[b], nbt, channels, y_shared, sc);
+      cuda_check_s(cudaEventRecord(c.pipe_event(1, b), sc), "record compute");
+      cuda_check_s(cudaStreamWaitEvent(so, c.pipe_event(1, b), 0), "wait compute");
+      cuda_check_s(cudaMemcpyAsync(out_host + r0 * dout, dz[b], nr * dout * sizeof(float), cudaMemcpyDeviceToHost, so),
+                   "D2H");
+      cuda_check_s(cudaEventRecord(c.pipe_event(2, b), so), "record d2h");
+    }
+    cuda_check_s(cudaStreamSynchronize(so), "sync");
+    cuda_check_s(cudaStreamSynchronize(sc), "sync");
+    cuda_check_s(cudaStreamSynchronize(si), "sync");
   });
 }
 

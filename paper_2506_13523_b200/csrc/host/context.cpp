@@ -44,6 +44,10 @@ Context::Context(int device) : device_(device) {
                       "; this library is built for sm_100a (B200) only");
   num_sms_ = prop.multiProcessorCount;
   cuda_check(cudaStreamCreateWithFlags(&host_stream_, cudaStreamNonBlocking), "cudaStreamCreate");
+  cuda_check(cudaStreamCreateWithFlags(&h2d_stream_, cudaStreamNonBlocking), "cudaStreamCreate");
+  cuda_check(cudaStreamCreateWithFlags(&d2h_stream_, cudaStreamNonBlocking), "cudaStreamCreate");
+  for (auto& row : pipe_ev_)
+    for (auto& e : row) cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
 }
 
 Context::~Context() {
@@ -52,6 +56,11 @@ Context::~Context() {
   for (void* p : scratch_)
     if (p) cudaFree(p);
   if (host_stream_) cudaStreamDestroy(host_stream_);
+  if (h2d_stream_) cudaStreamDestroy(h2d_stream_);
+  if (d2h_stream_) cudaStreamDestroy(d2h_stream_);
+  for (auto& row : pipe_ev_)
+    for (auto& e : row)
+      if (e) cudaEventDestroy(e);
 }
 
 void Context::activate() const { cuda_check(cudaSetDevice(device_), "cudaSetDevice"); }

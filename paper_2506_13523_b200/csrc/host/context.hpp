@@ -54,6 +54,12 @@ class Context {
   // scratch for host entry points / weighted products (grown on demand)
   float* scratch(int slot, size_t floats);
   cudaStream_t host_stream() const { return host_stream_; }
+  // pipelined host-buffer path: copy-in / copy-out streams and per-buffer events
+  static constexpr int kPipeBufs = 3;
+  cudaStream_t h2d_stream() const { return h2d_stream_; }
+  cudaStream_t d2h_stream() const { return d2h_stream_; }
+  cudaEvent_t pipe_event(int which, int buf) const { return pipe_ev_[which][buf]; }
+  std::mutex& host_path_mutex() { return host_mu_; }
 
   std::atomic<int64_t> launches{0};
   int grid_path = 0;       // 0 auto, 1 tcgen05, 2 simt
@@ -67,6 +73,9 @@ class Context {
   int device_ = 0;
   int num_sms_ = 148;
   cudaStream_t host_stream_ = nullptr;
+  cudaStream_t h2d_stream_ = nullptr, d2h_stream_ = nullptr;
+  cudaEvent_t pipe_ev_[3][kPipeBufs] = {};  // [h2d done, compute done, d2h done][buffer]
+  std::mutex host_mu_;
   std::mutex mu_;
   std::vector<void*> allocs_;
   std::map<std::array<int, 2>, CgtpTables> cgtp_;
@@ -75,8 +84,8 @@ class Context {
   std::map<std::array<int, 3>, FourierDevTables> fourier_;
   std::map<std::array<int, 4>, MtpDevTables> mtp_;
   std::map<std::vector<double>, const float*> weights_;
-  std::array<void*, 4> scratch_{};
-  std::array<size_t, 4> scratch_cap_{};
+  std::array<void*, 12> scratch_{};
+  std::array<size_t, 12> scratch_cap_{};
 };
 
 }  // namespace tpo_b200
