@@ -83,21 +83,7 @@ int min_lt(int L1, int L2, int L3) { return (std::max({L1, L2, L3}) + 1) / 2; }
 
 void run_cgtp(tpo_ctx* ctx, int L1, int L2, const RowSpec& rs, cudaStream_t s) {
   const auto& t = ctx->impl.cgtp(L1, L2);
-  // keep each launch under 2^31 blocks (rows/16 * chunks)
-  const int64_t max_rows = std::max<int64_t>(16, (2147483647LL / std::max(t.nchunks, 1)) / 16 * 16);
-  for (int64_t r0 = 0; r0 < rs.rows; r0 += max_rows) {
-    RowSpec sub = rs;
-    sub.rows = std::min(max_rows, rs.rows - r0);
-    sub.x = rs.x + r0 * t.din1;
-    sub.out = rs.out + r0 * t.dout;
-    if (rs.y_shared) {
-      if (r0 % rs.channels) throw InvalidArgument("cgtp: batch too large for one call");
-      sub.y = rs.y + (r0 / rs.channels) * t.din2;
-    } else {
-      sub.y = rs.y + r0 * t.din2;
-    }
-    launched(ctx, tpo_b200::launch_cgtp(t, sub, s), "cgtp kernel");
-  }
+  launched(ctx, tpo_b200::launch_cgtp(t, rs, ctx->impl.num_sms(), s), "cgtp kernel");
 }
 
 void run_grid(tpo_ctx* ctx, int L1, int L2, int L3, const RowSpec& rs, cudaStream_t s) {
@@ -116,6 +102,23 @@ void run_grid(tpo_ctx* ctx, int L1, int L2, int L3, const RowSpec& rs, cudaStrea
            "gtp_grid simt kernel");
 }
 
+// Fourier GTP: torus-grid dense operators on the tcgen05 kernel when the shape
+// fits (Din <= 128), else the SIMT direct-convolution kernel
+void run_fourier(tpo_ctx* ctx, int L1, int L2, int L3, const RowSpec& rs, cudaStream_t s) {
+  Context& c = ctx->impl;
+  if (c.grid_path != 2) {
+    const auto& e = c.fourier_tc(L1, L2, L3);
+    if (e.fits) {
+      c.last_grid_path = 1;
+      launched(ctx, tpo_b200::launch_gtp_grid_tc(e.t, rs, c.num_sms(), s), "gtp_fourier tcgen05 kernel");
+      return;
+    }
+    if (c.grid_path == 1) throw InvalidArgument("gtp_fourier: shape does not fit the tcgen05 tiling");
+  }
+  c.last_grid_path = 2;
+  launched(ctx, tpo_b200::launch_gtp_fourier(c.fourier(L1, L2, L3), rs, c.num_sms(), s), "gtp_fourier kernel");
+}
+
 void run_kind(tpo_ctx* ctx, int kind, int L1, int L2, int L3, int lt, const float* x, const float* y,
               float* out, int64_t batch, int64_t channels, int y_shared, cudaStream_t s) {
   check_args(ctx, L1, L2, x, y, out, batch, channels);
@@ -131,9 +134,7 @@ void run_kind(tpo_ctx* ctx, int kind, int L1, int L2, int L3, int lt, const floa
       return;
     case TPO_KIND_GTP_FOURIER:
       check_L3(L3, "gtp_fourier");
-      if (rs.rows > 0)
-        launched(ctx, tpo_b200::launch_gtp_fourier(ctx->impl.fourier(L1, L2, L3), rs, ctx->impl.num_sms(), s),
-                 "gtp_fourier kernel");
+      if (rs.rows > 0) run_fourier(ctx, L1, L2, L3, rs, s);
       return;
     case TPO_KIND_MTP: {
       check_L3(L3, "mtp");

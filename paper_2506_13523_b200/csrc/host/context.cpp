@@ -8,6 +8,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <complex>
 #include <cstring>
 
 #include "../kernels/sm100.cuh"
@@ -111,25 +112,26 @@ const CgtpTables& Context::cgtp(int L1, int L2) {
       }
   const int dout = static_cast<int>(per_out.size());
   const int nchunks = (dout + kCgtpChunk - 1) / kCgtpChunk;
-  std::vector<int> off(nchunks), nt(nchunks);
+  const int nwarps = nchunks * kCgtpChunk / 32;
+  std::vector<int> off(nwarps), nt(nwarps);
   std::vector<uint2> terms;
-  for (int q = 0; q < nchunks; ++q) {
+  for (int w = 0; w < nwarps; ++w) {
     int tmax = 0;
-    for (int i = 0; i < kCgtpChunk; ++i) {
-      const int o = q * kCgtpChunk + i;
+    for (int i = 0; i < 32; ++i) {
+      const int o = w * 32 + i;
       if (o < dout) tmax = std::max<int>(tmax, static_cast<int>(per_out[o].size()));
     }
-    off[q] = static_cast<int>(terms.size());
-    nt[q] = tmax;
-    terms.resize(terms.size() + static_cast<size_t>(tmax) * kCgtpChunk, make_uint2(0u, 0u));
-    for (int i = 0; i < kCgtpChunk; ++i) {
-      const int o = q * kCgtpChunk + i;
+    off[w] = static_cast<int>(terms.size());
+    nt[w] = tmax;
+    terms.resize(terms.size() + static_cast<size_t>(tmax) * 32, make_uint2(0u, 0u));  // padding: coef 0
+    for (int i = 0; i < 32; ++i) {
+      const int o = w * 32 + i;
       if (o >= dout) continue;
-      for (size_t t = 0; t < per_out[o].size(); ++t) {
-        float c = per_out[o][t].second;
+      for (size_t k = 0; k < per_out[o].size(); ++k) {
+        const float c = per_out[o][k].second;
         uint32_t cb;
         std::memcpy(&cb, &c, 4);
-        terms[off[q] + t * kCgtpChunk + i] = make_uint2(per_out[o][t].first, cb);
+        terms[off[w] + k * 32 + i] = make_uint2(per_out[o][k].first, cb);
       }
     }
   }
@@ -139,8 +141,8 @@ const CgtpTables& Context::cgtp(int L1, int L2) {
   t.dout = dout;
   t.nchunks = nchunks;
   t.terms = upload(terms);
-  t.chunk_off = upload(off);
-  t.chunk_nt = upload(nt);
+  t.warp_off = upload(off);
+  t.warp_nt = upload(nt);
   return cgtp_.emplace(std::array<int, 2>{L1, L2}, t).first->second;
 }
 
@@ -167,29 +169,33 @@ int parts_for(int zg) {
 }
 }  // namespace
 
-const GridTcEntry& Context::grid_tc(int L1, int L2, int L3) {
-  std::lock_guard<std::mutex> g(mu_);
-  auto it = grid_tc_.find({L1, L2, L3});
-  if (it != grid_tc_.end()) return it->second;
+// Dense operators of a "pointwise product" TPO on a point set of G points:
+// out = A ((S1 x) .* (S2 y)).  Both the S2-grid GTP (Gauss-Legendre x uniform
+// phi product grid) and the Fourier GTP (uniform torus grid, convolution
+// theorem) have this form and run through the same tcgen05 kernel.
+struct DenseOps {
+  int G = 0, din1 = 0, din2 = 0, dout_eff = 0, dout_total = 0;
+  bool same_s = false;
+  std::vector<double> s1, s2;  // [G][din]
+  std::vector<double> a;       // [dout_eff][G]
+};
+
+GridTcEntry Context::build_dense_tc(const DenseOps& ops, const char* label) {
   GridTcEntry ent;
   GridTcTables& t = ent.t;
-  const int band = L1 + L2;
-  const int L3e = std::min(L3, band);
-  t.din1 = (L1 + 1) * (L1 + 1);
-  t.din2 = (L2 + 1) * (L2 + 1);
+  const int G = ops.G;
+  t.din1 = ops.din1;
+  t.din2 = ops.din2;
   t.k1p = pad_to(t.din1, 16);
   t.k2p = pad_to(t.din2, 16);
-  t.dout_eff = (L3e + 1) * (L3e + 1);
-  t.dout_total = (L3 + 1) * (L3 + 1);
-  t.same_s = (L1 == L2) ? 1 : 0;
-  const S2Grid& gr = s2_grid(band);
-  const int G = gr.n_theta * gr.n_phi;
+  t.dout_eff = ops.dout_eff;
+  t.dout_total = ops.dout_total;
+  t.same_s = ops.same_s ? 1 : 0;
   const int max_smem = gtp_grid_tc_max_smem();
-  if (t.k1p > 128 || t.k2p > 128 || max_smem <= 0) {  // SIMT separable kernel handles these shapes
+  if (t.k1p > 128 || t.k2p > 128 || max_smem <= 0) {  // SIMT kernels handle these shapes
     ent.fits = false;
-    return grid_tc_.emplace(std::array<int, 3>{L1, L2, L3}, ent).first->second;
+    return ent;
   }
-
   // ---- tiling: choose (output groups, chunk width) minimising estimated MMA cycles per tile
   //   TMEM: zg (Z) + 2 nc (F_x, F_y; P overwrites F_x) <= 512 columns
   const int force_nc = env_int("TPO_GRID_NC", 0), force_groups = env_int("TPO_GRID_GROUPS", 0);
@@ -221,7 +227,7 @@ const GridTcEntry& Context::grid_tc(int L1, int L2, int L3) {
   }
   if (best_g == 0) {
     ent.fits = false;
-    return grid_tc_.emplace(std::array<int, 3>{L1, L2, L3}, ent).first->second;
+    return ent;
   }
   const int nc = best_nc;
   t.nc = nc;
@@ -264,7 +270,7 @@ const GridTcEntry& Context::grid_tc(int L1, int L2, int L3) {
   }
   if (inplace < 0) {
     ent.fits = false;
-    return grid_tc_.emplace(std::array<int, 3>{L1, L2, L3}, ent).first->second;
+    return ent;
   }
   t.raw_inplace = inplace;
   t.s_stages = s_st;
@@ -283,29 +289,19 @@ const GridTcEntry& Context::grid_tc(int L1, int L2, int L3) {
   t.smem_bytes = static_cast<int>(o);
   if (env_int("TPO_GRID_VERBOSE", 0))
     std::fprintf(stderr,
-                 "[tpo] grid_tc L=(%d,%d,%d) G=%d nc=%d chunks=%d groups=%d zg=%d parts=%d s_stages=%d a_stages=%d "
-                 "inplace=%d smem=%d\n",
-                 L1, L2, L3, G, nc, t.nchunks, t.ngroups, t.zg, t.nparts, s_st, a_st, inplace, t.smem_bytes);
+                 "[tpo] %s tcgen05 G=%d din=(%d,%d) dout=%d nc=%d chunks=%d groups=%d zg=%d parts=%d s_stages=%d "
+                 "a_stages=%d inplace=%d smem=%d\n",
+                 label, G, t.din1, t.din2, t.dout_eff, nc, t.nchunks, t.ngroups, t.zg, t.nparts, s_st, a_st, inplace,
+                 t.smem_bytes);
 
-  // ---- dense operators on the product grid (proj/src/sphere.cpp:105-195)
-  const double phi_scale = 2.0 * M_PI / gr.n_phi;
-  auto s_val = [&](int gidx, int k) -> double {  // S[g][(l,m)]
-    const int j = gidx / gr.n_phi, kk = gidx % gr.n_phi;
-    const int l = static_cast<int>(std::sqrt(static_cast<double>(k)) + 1e-9);
-    const int m = k - l * l - l;
-    return gr.lambda(l, std::abs(m), j) * gr.csm(m, kk);
-  };
+  // ---- operators -> fp16 hi / lo slices in the UMMA canonical layout
   double amax = 0.0;
-  for (int gidx = 0; gidx < G; ++gidx)
-    for (int o2 = 0; o2 < t.dout_eff; ++o2) {
-      const int j = gidx / gr.n_phi;
-      amax = std::max(amax, std::abs(gr.weights[j] * phi_scale * s_val(gidx, o2)));
-    }
+  for (double v : ops.a) amax = std::max(amax, std::abs(v));
   t.a_shift = amax > 0 ? -(std::ilogb(amax) + 1) : 0;
   const double a_scale = std::ldexp(1.0, t.a_shift);
 
   // S slices: [chunk][kstep][hi | lo][nc x 16 canonical]
-  auto build_s = [&](int din, int kp, std::vector<uint16_t>& buf) {
+  auto build_s = [&](const std::vector<double>& S, int din, int kp, std::vector<uint16_t>& buf) {
     const size_t half = static_cast<size_t>(nc) * 16;  // elements per hi / lo block
     const int nks = kp / 16;
     buf.assign(static_cast<size_t>(t.nchunks) * nks * 2 * half, 0);
@@ -317,7 +313,7 @@ const GridTcEntry& Context::grid_tc(int L1, int L2, int L3) {
           const int gidx = c * nc + r;
           for (int kk = 0; kk < 16; ++kk) {
             const int k = ks * 16 + kk;
-            const double v = (gidx < G && k < din) ? s_val(gidx, k) : 0.0;
+            const double v = (gidx < G && k < din) ? S[static_cast<size_t>(gidx) * din + k] : 0.0;
             uint16_t hv, lv;
             split_half(v, hv, lv);
             const uint32_t e = sm100::canon_off(r, kk, nc) / 2;
@@ -328,14 +324,14 @@ const GridTcEntry& Context::grid_tc(int L1, int L2, int L3) {
       }
   };
   std::vector<uint16_t> s1, s2, a;
-  build_s(t.din1, t.k1p, s1);
+  build_s(ops.s1, t.din1, t.k1p, s1);
   t.s1_slice_bytes = static_cast<uint32_t>(64 * nc);
   t.s1 = reinterpret_cast<const uint8_t*>(upload(s1));
   if (t.same_s) {
     t.s2 = t.s1;
     t.s2_slice_bytes = t.s1_slice_bytes;
   } else {
-    build_s(t.din2, t.k2p, s2);
+    build_s(ops.s2, t.din2, t.k2p, s2);
     t.s2_slice_bytes = static_cast<uint32_t>(64 * nc);
     t.s2 = reinterpret_cast<const uint8_t*>(upload(s2));
   }
@@ -355,10 +351,8 @@ const GridTcEntry& Context::grid_tc(int L1, int L2, int L3) {
               for (int kk = 0; kk < 16; ++kk) {
                 const int gidx = c * nc + sl * 16 + kk;
                 double v = 0.0;
-                if (gidx < G && o2 < t.dout_eff && pt * t.zp + rr < t.zg) {
-                  const int j = gidx / gr.n_phi;
-                  v = gr.weights[j] * phi_scale * s_val(gidx, o2) * a_scale;
-                }
+                if (gidx < G && o2 < t.dout_eff && pt * t.zp + rr < t.zg)
+                  v = ops.a[static_cast<size_t>(o2) * G + gidx] * a_scale;
                 uint16_t hv, lv;
                 split_half(v, hv, lv);
                 const uint32_t e = sm100::canon_off(rr, kk, t.zp) / 2;
@@ -371,7 +365,92 @@ const GridTcEntry& Context::grid_tc(int L1, int L2, int L3) {
     t.a = reinterpret_cast<const uint8_t*>(upload(a));
   }
   ent.fits = true;
-  return grid_tc_.emplace(std::array<int, 3>{L1, L2, L3}, ent).first->second;
+  return ent;
+}
+
+const GridTcEntry& Context::grid_tc(int L1, int L2, int L3) {
+  std::lock_guard<std::mutex> g(mu_);
+  auto it = grid_tc_.find({L1, L2, L3});
+  if (it != grid_tc_.end()) return it->second;
+  // dense operators on the reference's product grid (proj/src/sphere.cpp:105-195, gtp.cpp:228-260)
+  const int band = L1 + L2;
+  const int L3e = std::min(L3, band);
+  const S2Grid& gr = s2_grid(band);
+  DenseOps ops;
+  ops.G = gr.n_theta * gr.n_phi;
+  ops.din1 = (L1 + 1) * (L1 + 1);
+  ops.din2 = (L2 + 1) * (L2 + 1);
+  ops.dout_eff = (L3e + 1) * (L3e + 1);
+  ops.dout_total = (L3 + 1) * (L3 + 1);
+  ops.same_s = L1 == L2;
+  const double phi_scale = 2.0 * M_PI / gr.n_phi;
+  auto s_val = [&](int gidx, int k) -> double {  // Lambda_{l|m|}(theta_j) cs_m(phi_k)
+    const int j = gidx / gr.n_phi, kk = gidx % gr.n_phi;
+    const int l = static_cast<int>(std::sqrt(static_cast<double>(k)) + 1e-9);
+    const int m = k - l * l - l;
+    return gr.lambda(l, std::abs(m), j) * gr.csm(m, kk);
+  };
+  ops.s1.resize(static_cast<size_t>(ops.G) * ops.din1);
+  for (int gi = 0; gi < ops.G; ++gi)
+    for (int k = 0; k < ops.din1; ++k) ops.s1[static_cast<size_t>(gi) * ops.din1 + k] = s_val(gi, k);
+  if (!ops.same_s) {
+    ops.s2.resize(static_cast<size_t>(ops.G) * ops.din2);
+    for (int gi = 0; gi < ops.G; ++gi)
+      for (int k = 0; k < ops.din2; ++k) ops.s2[static_cast<size_t>(gi) * ops.din2 + k] = s_val(gi, k);
+  }
+  ops.a.resize(static_cast<size_t>(ops.dout_eff) * ops.G);
+  for (int o = 0; o < ops.dout_eff; ++o)  // quadrature weight w_j * 2 pi / n_phi
+    for (int gi = 0; gi < ops.G; ++gi)
+      ops.a[static_cast<size_t>(o) * ops.G + gi] = gr.weights[gi / gr.n_phi] * phi_scale * s_val(gi, o);
+  return grid_tc_.emplace(std::array<int, 3>{L1, L2, L3}, build_dense_tc(ops, "gtp_grid")).first->second;
+}
+
+// Fourier GTP on the tensor cores.  The reference convolves the two torus
+// spectra directly (proj/src/gtp.cpp:290-301).  The product spectrum has band
+// 2L per axis, so on a uniform N x N torus grid with N = 4L + 1 the
+// convolution theorem is exact: cz = DFT_N(IDFT_N(cx) .* IDFT_N(cy)) / N^2.
+// Folding encode into the inverse DFT and decode into the forward DFT gives
+// two real dense operators (the torus functions of real inputs are real):
+//   S[(a,b)][k] = Re sum_{(u,v,w) in enc_k} w w_N^(u a + v b),   w_N = exp(2 pi i / N)
+//   A[o][(a,b)] = Re sum_{(U,V,w) in dec_o} w w_N^-(U a + V b) / N^2
+const GridTcEntry& Context::fourier_tc(int L1, int L2, int L3) {
+  std::lock_guard<std::mutex> g(mu_);
+  auto it = fourier_tc_.find({L1, L2, L3});
+  if (it != fourier_tc_.end()) return it->second;
+  const int L = std::max(L1, L2);
+  const FourierTables& ft = fourier_tables(L);
+  const int N = 4 * L + 1;
+  const int Lz = 2 * L;
+  const int L3e = std::min(L3, Lz);
+  DenseOps ops;
+  ops.G = N * N;
+  ops.din1 = (L1 + 1) * (L1 + 1);
+  ops.din2 = (L2 + 1) * (L2 + 1);
+  ops.dout_eff = (L3e + 1) * (L3e + 1);
+  ops.dout_total = (L3 + 1) * (L3 + 1);
+  ops.same_s = L1 == L2;
+  std::vector<std::complex<double>> wn(N);
+  for (int k = 0; k < N; ++k) wn[k] = std::polar(1.0, 2.0 * M_PI * k / N);
+  auto modn = [N](long v) { return static_cast<int>(((v % N) + N) % N); };
+  auto build_s = [&](int din, std::vector<double>& S) {
+    S.assign(static_cast<size_t>(ops.G) * din, 0.0);
+    for (int k = 0; k < din; ++k)
+      for (const FourierMode& e : ft.enc[k])
+        for (int a = 0; a < N; ++a)
+          for (int b = 0; b < N; ++b)
+            S[static_cast<size_t>(a * N + b) * din + k] += (e.w * wn[modn(static_cast<long>(e.u) * a + static_cast<long>(e.v) * b)]).real();
+  };
+  build_s(ops.din1, ops.s1);
+  if (!ops.same_s) build_s(ops.din2, ops.s2);
+  ops.a.assign(static_cast<size_t>(ops.dout_eff) * ops.G, 0.0);
+  const double inv = 1.0 / (static_cast<double>(N) * N);
+  for (int o = 0; o < ops.dout_eff; ++o)
+    for (const FourierMode& e : ft.dec[o])
+      for (int a = 0; a < N; ++a)
+        for (int b = 0; b < N; ++b)
+          ops.a[static_cast<size_t>(o) * ops.G + a * N + b] +=
+              (e.w * wn[modn(-(static_cast<long>(e.u) * a + static_cast<long>(e.v) * b))]).real() * inv;
+  return fourier_tc_.emplace(std::array<int, 3>{L1, L2, L3}, build_dense_tc(ops, "gtp_fourier")).first->second;
 }
 
 // ------------------------------------------------------------------ GTP grid (SIMT separable)

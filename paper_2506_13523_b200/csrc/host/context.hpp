@@ -46,6 +46,7 @@ class Context {
 
   const CgtpTables& cgtp(int L1, int L2);
   const GridTcEntry& grid_tc(int L1, int L2, int L3);
+  const GridTcEntry& fourier_tc(int L1, int L2, int L3);  // Fourier GTP as torus-grid dense operators
   const GridSimtTables& grid_simt(int L1, int L2, int L3);
   const FourierDevTables& fourier(int L1, int L2, int L3);
   const MtpDevTables& mtp(int L1, int L2, int L3, int lt);
@@ -62,7 +63,7 @@ class Context {
   std::mutex& host_path_mutex() { return host_mu_; }
 
   std::atomic<int64_t> launches{0};
-  int grid_path = 0;       // 0 auto, 1 tcgen05, 2 simt
+  int grid_path = 0;       // 0 auto, 1 tcgen05, 2 simt (also selects the Fourier GTP path)
   int last_grid_path = 0;
 
  private:
@@ -80,6 +81,8 @@ class Context {
   std::vector<void*> allocs_;
   std::map<std::array<int, 2>, CgtpTables> cgtp_;
   std::map<std::array<int, 3>, GridTcEntry> grid_tc_;
+  std::map<std::array<int, 3>, GridTcEntry> fourier_tc_;
+  GridTcEntry build_dense_tc(const struct DenseOps& ops, const char* label);
   std::map<std::array<int, 3>, GridSimtTables> grid_simt_;
   std::map<std::array<int, 3>, FourierDevTables> fourier_;
   std::map<std::array<int, 4>, MtpDevTables> mtp_;

@@ -21,17 +21,18 @@ struct RowSpec {
 };
 
 // ---------------------------------------------------------------- CGTP
-// For output chunk q (kCgtpChunk consecutive outputs), terms are stored
-// term-major: term t of output (q*kCgtpChunk + i) at
-// terms[chunk_off[q] + t*kCgtpChunk + i], packed {i1 | i2 << 16, coef bits}.
-constexpr int kCgtpChunk = 128;
+// Output coefficient o is owned by thread o % kCgtpChunk of output pass
+// o / kCgtpChunk.  Terms {i1 | i2 << 16, coef bits} are stored term-major per
+// warp (32 outputs), padded to that warp's longest list:
+//   term t of output o: terms[warp_off[o / 32] + t * 32 + o % 32], t < warp_nt[o / 32].
+constexpr int kCgtpChunk = 256;
 struct CgtpTables {
   int din1, din2, dout, nchunks;
   const uint2* terms;
-  const int* chunk_off;  // [nchunks]
-  const int* chunk_nt;   // [nchunks] padded term count
+  const int* warp_off;  // [nchunks * kCgtpChunk / 32]
+  const int* warp_nt;   // [nchunks * kCgtpChunk / 32]
 };
-cudaError_t launch_cgtp(const CgtpTables& t, const RowSpec& rs, cudaStream_t s);
+cudaError_t launch_cgtp(const CgtpTables& t, const RowSpec& rs, int num_sms, cudaStream_t s);
 
 // ---------------------------------------------------------------- GTP grid, tcgen05
 // Dense operators of the reference's product grid, pre-split into fp16 hi/lo

@@ -4,10 +4,14 @@
 // embed both inputs into (2lt+1)^2 carrier matrices through the real CG
 // tables (proj/src/mtp.cpp:20-58), classical cubic matmul Z = X Y
 // (:119-133, sub-cubic forbidden by the cost model), extract every output
-// degree by the adjoint CG contraction (:60-97).  The embed / extract maps
-// are flattened on the host into per-cell and per-output gather lists over
-// the CG nonzeros; a block keeps `rows_per_block` products resident in
-// shared memory and runs the three phases with all threads.
+// degree by the adjoint CG contraction (:60-97).
+//
+// A block owns a tile of R products with all intermediates in shared memory
+// (odd row pitches, so column-wise reads are bank-conflict free).  The embed
+// and extract maps are CSR gather lists over the CG nonzeros (host/context.cpp);
+// each list entry is fetched once per tile and applied to all R products from
+// registers.  The R x dt matmul row tasks keep one output row of Z in
+// registers and stream X / Y from shared memory.
 #include <algorithm>
 
 #include "kernels.hpp"
@@ -16,79 +20,134 @@ namespace tpo_b200 {
 namespace {
 
 constexpr int kThreads = 256;
+constexpr int kMaxDt = 33;  // lt <= 16
 
+template <int R>
 __global__ void __launch_bounds__(kThreads)
-    mtp_kernel(const __grid_constant__ MtpDevTables t, const __grid_constant__ RowSpec rs, int R) {
+    mtp_kernel(const __grid_constant__ MtpDevTables t, const __grid_constant__ RowSpec rs) {
   extern __shared__ float sm[];
-  const int dt2 = t.dt * t.dt;
-  float* xs = sm;                 // [R][din1]
-  float* ys = xs + R * t.din1;    // [R][din2]
-  float* X = ys + R * t.din2;     // [R][dt2]
-  float* Y = X + R * dt2;         // [R][dt2]
-  float* Z = Y + R * dt2;         // [R][dt2]
+  const int dt = t.dt, dt2 = dt * dt;
+  const int px = t.din1 | 1, py = t.din2 | 1, pc = dt2 | 1;
+  float* xs = sm;             // [R][px]
+  float* ys = xs + R * px;    // [R][py]
+  float* X = ys + R * py;     // [R][pc]
+  float* Y = X + R * pc;      // [R][pc]
+  float* Z = Y + R * pc;      // [R][pc]
+  const int tid = threadIdx.x;
   const int64_t ntiles = (rs.rows + R - 1) / R;
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int64_t row0 = tile * R;
-    const int nr = static_cast<int>(std::min<int64_t>(R, rs.rows - row0));
-    // rows are contiguous in global memory: linear, coalesced loads
-    for (int i = threadIdx.x; i < nr * t.din1; i += kThreads) xs[i] = __ldg(rs.x + row0 * t.din1 + i);
-    for (int i = threadIdx.x; i < nr * t.din2; i += kThreads) {
+    const int64_t left = rs.rows - row0;
+    const int nr = left < R ? static_cast<int>(left) : R;
+    __syncthreads();
+    for (int i = tid; i < R * t.din1; i += kThreads) {
+      const int r = i / t.din1, k = i - r * t.din1;
+      xs[r * px + k] = r < nr ? __ldg(rs.x + row0 * t.din1 + i) : 0.f;
+    }
+    for (int i = tid; i < R * t.din2; i += kThreads) {
       const int r = i / t.din2, k = i - r * t.din2;
       const int64_t g = row0 + r;
-      ys[i] = __ldg(rs.y + (rs.y_shared ? g / rs.channels : g) * t.din2 + k);
+      const int64_t yr = rs.y_shared ? g / rs.channels : g;
+      ys[r * py + k] = r < nr ? __ldg(rs.y + yr * t.din2 + k) : 0.f;
     }
     __syncthreads();
-    for (int i = threadIdx.x; i < nr * dt2; i += kThreads) {  // embed (sparse CG gather)
-      const int r = i / dt2, cell = i - r * dt2;
-      float ax = 0.f, ay = 0.f;
-      for (int e = __ldg(t.emb1_off + cell), e1 = __ldg(t.emb1_off + cell + 1); e < e1; ++e)
-        ax = fmaf(__ldg(t.emb1_c + e), xs[r * t.din1 + __ldg(t.emb1_idx + e)], ax);
-      for (int e = __ldg(t.emb2_off + cell), e1 = __ldg(t.emb2_off + cell + 1); e < e1; ++e)
-        ay = fmaf(__ldg(t.emb2_c + e), ys[r * t.din2 + __ldg(t.emb2_idx + e)], ay);
-      X[i] = ax;
-      Y[i] = ay;
+    // ---- embed (proj/src/mtp.cpp:20-58): X[cell] = sum_e c_e x[idx_e]
+    for (int cell = tid; cell < 2 * dt2; cell += kThreads) {
+      const bool second = cell >= dt2;
+      const int cl = second ? cell - dt2 : cell;
+      const int* off = second ? t.emb2_off : t.emb1_off;
+      const int* idx = second ? t.emb2_idx : t.emb1_idx;
+      const float* cf = second ? t.emb2_c : t.emb1_c;
+      const float* src = second ? ys : xs;
+      const int pitch = second ? py : px;
+      float acc[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) acc[r] = 0.f;
+      for (int e = __ldg(off + cl), e1 = __ldg(off + cl + 1); e < e1; ++e) {
+        const float c = __ldg(cf + e);
+        const int k = __ldg(idx + e);
+#pragma unroll
+        for (int r = 0; r < R; ++r) acc[r] = fmaf(c, src[r * pitch + k], acc[r]);
+      }
+      float* dst = (second ? Y : X) + cl;
+#pragma unroll
+      for (int r = 0; r < R; ++r) dst[r * pc] = acc[r];
     }
     __syncthreads();
-    for (int i = threadIdx.x; i < nr * dt2; i += kThreads) {  // Z = X Y, classical cubic
-      const int r = i / dt2, cell = i - r * dt2;
-      const int a = cell / t.dt, b = cell - a * t.dt;
-      const float* xr = X + r * dt2 + a * t.dt;
-      const float* yc = Y + r * dt2 + b;
-      float acc = 0.f;
-      for (int k = 0; k < t.dt; ++k) acc = fmaf(xr[k], yc[k * t.dt], acc);
-      Z[i] = acc;
+    // ---- Z = X Y, classical cubic (proj/src/mtp.cpp:119-133): task = (row r, Z row i)
+    for (int task = tid; task < R * dt; task += kThreads) {
+      const int r = task / dt, i = task - r * dt;
+      const float* xr = X + r * pc + i * dt;
+      const float* yb = Y + r * pc;
+      float acc[kMaxDt];
+#pragma unroll
+      for (int j = 0; j < kMaxDt; ++j) acc[j] = 0.f;
+      for (int k = 0; k < dt; ++k) {
+        const float a = xr[k];
+        const float* yk = yb + k * dt;
+        // 8-wide blocks guarded as a whole: no issue slots spent past dt
+#pragma unroll
+        for (int j0 = 0; j0 < kMaxDt; j0 += 8) {
+          if (j0 < dt) {
+#pragma unroll
+            for (int jj = 0; jj < 8; ++jj)
+              if (j0 + jj < kMaxDt && j0 + jj < dt) acc[j0 + jj] = fmaf(a, yk[j0 + jj], acc[j0 + jj]);
+          }
+        }
+      }
+      float* zr = Z + r * pc + i * dt;
+#pragma unroll
+      for (int j = 0; j < kMaxDt; ++j)
+        if (j < dt) zr[j] = acc[j];
     }
     __syncthreads();
-    for (int i = threadIdx.x; i < nr * t.dout_total; i += kThreads) {  // extract
-      const int r = i / t.dout_total, o = i - r * t.dout_total;
-      float acc = 0.f;
-      if (o < t.dout_eff)
-        for (int e = __ldg(t.ext_off + o), e1 = __ldg(t.ext_off + o + 1); e < e1; ++e)
-          acc = fmaf(__ldg(t.ext_c + e), Z[r * dt2 + __ldg(t.ext_idx + e)], acc);
-      rs.out[row0 * t.dout_total + i] = acc;
+    // ---- extract (proj/src/mtp.cpp:60-97): out[o] = sum_e c_e Z[cell_e]; zero past the carrier band
+    for (int o = tid; o < t.dout_total; o += kThreads) {
+      float acc[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) acc[r] = 0.f;
+      if (o < t.dout_eff) {
+        for (int e = __ldg(t.ext_off + o), e1 = __ldg(t.ext_off + o + 1); e < e1; ++e) {
+          const float c = __ldg(t.ext_c + e);
+          const int cell = __ldg(t.ext_idx + e);
+#pragma unroll
+          for (int r = 0; r < R; ++r) acc[r] = fmaf(c, Z[r * pc + cell], acc[r]);
+        }
+      }
+      float* op = rs.out + row0 * t.dout_total + o;
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+        if (r < nr) op[static_cast<int64_t>(r) * t.dout_total] = acc[r];
     }
-    __syncthreads();
   }
+}
+
+template <int R>
+cudaError_t launch_r(const MtpDevTables& t, const RowSpec& rs, int num_sms, cudaStream_t s) {
+  const int dt2 = t.dt * t.dt;
+  const size_t smem = sizeof(float) * R * ((t.din1 | 1) + (t.din2 | 1) + 3 * (dt2 | 1));
+  cudaError_t e = cudaFuncSetAttribute(mtp_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  int occ = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, mtp_kernel<R>, kThreads, smem);
+  const int64_t ntiles = (rs.rows + R - 1) / R;
+  const int grid = static_cast<int>(std::min<int64_t>(ntiles, static_cast<int64_t>(num_sms) * std::max(occ, 1)));
+  mtp_kernel<R><<<grid, kThreads, smem, s>>>(t, rs);
+  return cudaGetLastError();
 }
 
 }  // namespace
 
 cudaError_t launch_mtp(const MtpDevTables& t, const RowSpec& rs, int num_sms, cudaStream_t s) {
   if (rs.rows <= 0) return cudaSuccess;
-  const int per_row = t.din1 + t.din2 + 3 * t.dt * t.dt;
-  int R = std::max(1, std::min(32, (40 * 1024 / 4) / per_row));
-  const size_t smem = sizeof(float) * static_cast<size_t>(R) * per_row;
-  if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(mtp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem));
-    if (e != cudaSuccess) return e;
-  }
-  int occ = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, mtp_kernel, kThreads, smem);
-  const int64_t ntiles = (rs.rows + R - 1) / R;
-  const int grid = static_cast<int>(std::min<int64_t>(ntiles, static_cast<int64_t>(num_sms) * std::max(occ, 1)));
-  mtp_kernel<<<grid, kThreads, smem, s>>>(t, rs, R);
-  return cudaGetLastError();
+  if (t.dt > kMaxDt) return cudaErrorInvalidValue;
+  // rows per tile: as many as keep >= 2 blocks per SM within 227 KB
+  const int per_row = ((t.din1 | 1) + (t.din2 | 1) + 3 * ((t.dt * t.dt) | 1)) * 4;
+  if (per_row * 32 <= 110 * 1024) return launch_r<32>(t, rs, num_sms, s);
+  if (per_row * 16 <= 110 * 1024) return launch_r<16>(t, rs, num_sms, s);
+  if (per_row * 8 <= 220 * 1024) return launch_r<8>(t, rs, num_sms, s);
+  return launch_r<4>(t, rs, num_sms, s);
 }
 
 }  // namespace tpo_b200

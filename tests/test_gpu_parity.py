@@ -101,14 +101,43 @@ def test_cgtp(tpo, orc, L):
     _check_batch(tpo, orc, "cgtp", L, 257, 300 + L)
 
 
+@pytest.mark.parametrize("C", [32, 96])
+def test_cgtp_edge_tiles(tpo, orc, C):
+    # shared-y fast path (channels a multiple of the 32-row tile), ragged batch tail
+    L, B = 3, 5
+    x, y = _inputs(B, L, L, 330 + C, C=C, shared=True)
+    out = _gpu(tpo, "cgtp", x, y, L, L, 0)
+    ref = orc.batch_mimo("cgtp", L, x.astype(np.float64), y.astype(np.float64), channels=C, y_shared=True)
+    assert _normwise(out, ref) <= TOL
+
+
 @pytest.mark.parametrize("L", [12, 16])
 def test_cgtp_large(tpo, orc, L):
     _check_batch(tpo, orc, "cgtp", L, 8, 310 + L)
 
 
-@pytest.mark.parametrize("L", [0, 1, 2, 4, 6, 8, 10, 16])
-def test_gtp_fourier(tpo, orc, L):
-    _check_batch(tpo, orc, "gtp_fourier", L, 129 if L <= 8 else 16, 400 + L)
+@pytest.mark.parametrize("L", list(range(0, 11)))
+def test_gtp_fourier_tcgen05(tpo, orc, L):
+    # torus-grid dense operators (convolution theorem) on the fused tcgen05 kernel
+    ctx = tpo.context()
+    ctx.set_grid_path("tc")
+    try:
+        _check_batch(tpo, orc, "gtp_fourier", L, 1000 if L <= 8 else 300, 400 + L)
+        assert ctx.last_grid_path == "tcgen05"
+    finally:
+        ctx.set_grid_path("auto")
+
+
+@pytest.mark.parametrize("L", [0, 1, 2, 4, 6, 11, 16])
+def test_gtp_fourier_simt(tpo, orc, L):
+    # direct spectral convolution on the Hermitian half plane (SIMT)
+    ctx = tpo.context()
+    ctx.set_grid_path("simt")
+    try:
+        _check_batch(tpo, orc, "gtp_fourier", L, 129 if L <= 8 else 16, 420 + L)
+        assert ctx.last_grid_path == "simt"
+    finally:
+        ctx.set_grid_path("auto")
 
 
 @pytest.mark.parametrize("L", [0, 1, 2, 3, 6, 10, 16])
