@@ -14,6 +14,8 @@ from pathlib import Path
 
 _HERE = Path(__file__).resolve().parent
 LIB_PATH = _HERE / "libtpo_b200.so"
+if os.environ.get("TPO_LIB_PATH"):  # A/B timing of an alternative in-tree build (tools/ab_timing.sh)
+    LIB_PATH = Path(os.environ["TPO_LIB_PATH"]).resolve()
 
 TPO_OK, TPO_EINVAL, TPO_ERANGE, TPO_ERUNTIME, TPO_ECUDA = 0, 1, 2, 3, 4
 KIND_CGTP, KIND_GTP_GRID, KIND_GTP_FOURIER, KIND_MTP = 0, 1, 2, 3
