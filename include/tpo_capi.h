@@ -99,8 +99,10 @@ int tpo_weighted_gtp_f32(tpo_ctx* ctx, int L1, int L2, int L3, const double* a,
 int tpo_run_f32(tpo_ctx* ctx, int kind, int L1, int L2, int L3, int l_tilde, const float* x,
                 const float* y, float* out, int64_t batch, int64_t channels, int y_shared,
                 void* stream);
-/* Same with HOST buffers: H2D copy, launch, D2H copy, synchronize.  Scratch
- * device buffers are owned by the context and reused across calls. */
+/* Same with HOST buffers, synchronous like the reference's call: the batch is
+ * cut into ~8 MiB chunks that flow through copy-in, compute and copy-out
+ * streams over three device buffer sets owned by the context, so both PCIe
+ * directions overlap the kernels (pinned host memory gives full overlap). */
 int tpo_run_host_f32(tpo_ctx* ctx, int kind, int L1, int L2, int L3, int l_tilde,
                      const float* x_host, const float* y_host, float* out_host, int64_t batch,
                      int64_t channels, int y_shared);
@@ -118,11 +120,13 @@ int tpo_cg_real(int l1, int l2, int l3, int* m1, int* m2, int* m3, double* value
  * entry count (or a negative status). */
 int tpo_fourier_table(int L, int which, int* counts, int* u, int* v, double* re, double* im, int cap);
 
-/* Kernel selection for GTP-grid (for tests/bench): 0 auto, 1 force the fused
- * tcgen05 kernel (fails if the shape does not fit), 2 force the SIMT
- * separable kernel.  Returns the previous setting. */
+/* Kernel selection for the two Gaunt products (for tests/bench): 0 auto,
+ * 1 force the fused tcgen05 kernel (fails if the shape does not fit: inputs
+ * of more than 128 coefficients, i.e. L > 10), 2 force the SIMT kernels
+ * (separable grid GTP; direct half-plane spectral convolution for the
+ * Fourier GTP).  Returns the previous setting. */
 int tpo_set_gtp_grid_path(tpo_ctx* ctx, int path);
-/* Which GTP-grid kernel the last tpo_gtp_grid_f32 call used (1 tc, 2 simt). */
+/* Which kernel the last GTP-grid / GTP-Fourier call used (1 tc, 2 simt). */
 int tpo_last_gtp_grid_path(const tpo_ctx* ctx);
 
 #ifdef __cplusplus
