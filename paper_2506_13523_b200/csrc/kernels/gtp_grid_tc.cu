@@ -285,7 +285,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp == 1) {
     // ===================================================== MMA issuer
-    if (lane == 0) {
+    // The whole (converged) warp runs the loop and waits; one elected lane
+    // issues each tcgen05 instruction.  Keeping the warp converged lets the
+    // descriptors live in uniform registers without a divergent waterfall per
+    // MMA, which lowers the per-instruction issue cost of the single issuer.
+    const bool leader_lane = elect_one_sync();
+    {
       int s_stage = 0, a_stage = 0;
       uint32_t s_ph = 0, a_ph = 0;
       // next slice of a ring: wait until it landed, return its shared-memory address
@@ -350,16 +355,16 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint64_t bh = make_sdesc(sb, lbo_s, 128), bl = make_sdesc(sb + s_half, lbo_s, 128);
             const uint64_t ah = dx_hi + ks * kstep_x, al = dx_lo + ks * kstep_x;
             const uint32_t acc = ks > 0 ? 1u : 0u;
-            mma_f16_ss(tmem + fx, ah, bh, id1, acc);
-            mma_f16_ss(tmem + fx, ah, bl, id1, 1u);
-            mma_f16_ss(tmem + fx, al, bh, id1, 1u);
+            if (leader_lane) mma_f16_ss(tmem + fx, ah, bh, id1, acc);
+            if (leader_lane) mma_f16_ss(tmem + fx, ah, bl, id1, 1u);
+            if (leader_lane) mma_f16_ss(tmem + fx, al, bh, id1, 1u);
             if (t.same_s) {
               const uint64_t yh_ = dy_hi + ks * kstep_x, yl_ = dy_lo + ks * kstep_x;
-              mma_f16_ss(tmem + fy, yh_, bh, id1, acc);
-              mma_f16_ss(tmem + fy, yh_, bl, id1, 1u);
-              mma_f16_ss(tmem + fy, yl_, bh, id1, 1u);
+              if (leader_lane) mma_f16_ss(tmem + fy, yh_, bh, id1, acc);
+              if (leader_lane) mma_f16_ss(tmem + fy, yh_, bl, id1, 1u);
+              if (leader_lane) mma_f16_ss(tmem + fy, yl_, bh, id1, 1u);
             }
-            tc_commit(&bars[slot]);
+            if (leader_lane) tc_commit(&bars[slot]);
           }
           if (!t.same_s) {
             for (int ks = 0; ks < t.k2p / 16; ++ks) {
@@ -369,14 +374,14 @@ __global__ void __launch_bounds__(kThreads, 1)
               const uint64_t bh = make_sdesc(sb, lbo_s, 128), bl = make_sdesc(sb + s2_half, lbo_s, 128);
               const uint64_t ah = dy_hi + ks * kstep_x, al = dy_lo + ks * kstep_x;
               const uint32_t acc = ks > 0 ? 1u : 0u;
-              mma_f16_ss(tmem + fy, ah, bh, id1, acc);
-              mma_f16_ss(tmem + fy, ah, bl, id1, 1u);
-              mma_f16_ss(tmem + fy, al, bh, id1, 1u);
-              tc_commit(&bars[slot]);
+              if (leader_lane) mma_f16_ss(tmem + fy, ah, bh, id1, acc);
+              if (leader_lane) mma_f16_ss(tmem + fy, ah, bl, id1, 1u);
+              if (leader_lane) mma_f16_ss(tmem + fy, al, bh, id1, 1u);
+              if (leader_lane) tc_commit(&bars[slot]);
             }
           }
-          tc_commit(&bars[B_F_FULL]);
-          if (c == t.nchunks - 1 && last_of_tile) tc_commit(&bars[B_XY_FREE]);
+          if (leader_lane) tc_commit(&bars[B_F_FULL]);
+          if (c == t.nchunks - 1 && last_of_tile) if (leader_lane) tc_commit(&bars[B_XY_FREE]);
           // ---- GEMM 2: Z += P A^T, P (hi/lo fp16) read from TMEM in place of F_x
           if (c == 0 && i > 0) {  // previous unit's epilogue has drained Z
             const auto t0 = now();
@@ -392,19 +397,19 @@ __global__ void __launch_bounds__(kThreads, 1)
               const uint32_t sb = take_a(slot);
               const uint64_t bh = make_sdesc(sb, lbo_a, 128), bl = make_sdesc(sb + a_half, lbo_a, 128);
               const uint32_t zd = tmem + pt * t.zp;
-              mma_f16_ts(zd, p_hi, bh, id2, (c == 0 && s == 0) ? 0u : 1u);
-              mma_f16_ts(zd, p_hi, bl, id2, 1u);
-              mma_f16_ts(zd, p_lo, bh, id2, 1u);
-              tc_commit(&bars[slot]);
+              if (leader_lane) mma_f16_ts(zd, p_hi, bh, id2, (c == 0 && s == 0) ? 0u : 1u);
+              if (leader_lane) mma_f16_ts(zd, p_hi, bl, id2, 1u);
+              if (leader_lane) mma_f16_ts(zd, p_lo, bh, id2, 1u);
+              if (leader_lane) tc_commit(&bars[slot]);
             }
           }
-          tc_commit(&bars[B_G2_DONE]);
+          if (leader_lane) tc_commit(&bars[B_G2_DONE]);
         }
-        tc_commit(&bars[B_Z_FULL]);
+        if (leader_lane) tc_commit(&bars[B_Z_FULL]);
         if (last_of_tile) ++v;
       }
       pc[0] = now() - t_start;
-      if (PROF) for (int k = 0; k < 8; ++k) g_prof[blockIdx.x * kProfSlots + k] = pc[k];
+      if (PROF && lane == 0) for (int k = 0; k < 8; ++k) g_prof[blockIdx.x * kProfSlots + k] = pc[k];
     }
   } else {
     // ===================================================== workers
