@@ -213,13 +213,15 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp == 0) {
     // ===================================================== TMA producer
-    if (lane == 0) {
+    // converged warp, elected lane issues (as for the MMA issuer)
+    const bool pl = elect_one_sync();
+    {
       int stage = 0;
       uint32_t ph = 0;
       auto push = [&](const uint8_t* src, uint32_t bytes) {
         mbar_wait(&bars[B_SEMPTY + stage], ph ^ 1);
-        mbar_arrive_expect_tx(&bars[B_SFULL + stage], bytes);
-        bulk_g2s(sring + stage * t.s_stage_bytes, src, bytes, &bars[B_SFULL + stage]);
+        if (pl) mbar_arrive_expect_tx(&bars[B_SFULL + stage], bytes);
+        if (pl) bulk_g2s(sring + stage * t.s_stage_bytes, src, bytes, &bars[B_SFULL + stage]);
         if (++stage == t.s_stages) {
           stage = 0;
           ph ^= 1;
@@ -231,9 +233,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       auto issue_raw = [&](int64_t tile, int64_t v) {
         if (v > 0) mbar_wait(&bars[t.raw_inplace ? B_XY_FREE : B_RAW_FREE], static_cast<uint32_t>((v - 1) & 1));
         const uint32_t bx = BM * t.din1 * 4, by = BM * t.din2 * 4;
-        mbar_arrive_expect_tx(&bars[B_RAW_FULL], bx + by);
-        bulk_g2s(raw_x, rs.x + tile * BM * t.din1, bx, &bars[B_RAW_FULL]);
-        bulk_g2s(raw_y, rs.y + tile * BM * t.din2, by, &bars[B_RAW_FULL]);
+        if (pl) mbar_arrive_expect_tx(&bars[B_RAW_FULL], bx + by);
+        if (pl) bulk_g2s(raw_x, rs.x + tile * BM * t.din1, bx, &bars[B_RAW_FULL]);
+        if (pl) bulk_g2s(raw_y, rs.y + tile * BM * t.din2, by, &bars[B_RAW_FULL]);
       };
       int64_t v = 0;  // tile sequence number
       if (u_begin < u_end) {
@@ -264,7 +266,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp == 10) {
     // ===================================================== TMA producer, A table (GEMM 2)
-    if (lane == 0) {
+    const bool pl = elect_one_sync();
+    {
       int stage = 0;
       uint32_t ph = 0;
       for (int64_t u = u_begin; u < u_end; ++u) {
@@ -273,8 +276,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int n = t.nchunks * t.nslices * t.nparts;
         for (int k = 0; k < n; ++k) {
           mbar_wait(&bars[B_AEMPTY + stage], ph ^ 1);
-          mbar_arrive_expect_tx(&bars[B_AFULL + stage], t.a_slice_bytes);
-          bulk_g2s(aring + stage * t.a_stage_bytes, t.a + (abase + k) * t.a_slice_bytes, t.a_slice_bytes,
+          if (pl) mbar_arrive_expect_tx(&bars[B_AFULL + stage], t.a_slice_bytes);
+          if (pl) bulk_g2s(aring + stage * t.a_stage_bytes, t.a + (abase + k) * t.a_slice_bytes, t.a_slice_bytes,
                    &bars[B_AFULL + stage]);
           if (++stage == t.a_stages) {
             stage = 0;
