@@ -159,6 +159,10 @@ int env_int(const char* name, int dflt) {
 constexpr int kMaxRingStages = 8;
 double mma_ss(int n) { return std::max({45.0, n / 2.0, (4096.0 + 32.0 * n) / 128.0}); }
 double mma_ts(int n) { return std::max({45.0, n / 2.0, 32.0 * n / 128.0}); }
+// the same per SM for a CTA pair (M = 256, one instruction for both SMs, each
+// SM reads its own A and half of B)
+double mma_ss_pair(int n) { return std::max({22.5, n / 2.0, (4096.0 + 16.0 * n) / 128.0}); }
+double mma_ts_pair(int n) { return std::max({22.5, n / 2.0, 16.0 * n / 128.0}); }
 // GEMM 2 N-split of a group of zg outputs (parts of <= 256 rows, multiple of
 // 16).  Splitting is kept at 1: narrower MMAs leave too little slack over the
 // issue floor to hide the per-stage mbarrier wait (tools/ubench/mma_ubench3.cu).
@@ -199,6 +203,10 @@ GridTcEntry Context::build_dense_tc(const DenseOps& ops, const char* label) {
   // ---- tiling: choose (output groups, chunk width) minimising estimated MMA cycles per tile
   //   TMEM: zg (Z) + 2 nc (F_x, F_y; P overwrites F_x) <= 512 columns
   const int force_nc = env_int("TPO_GRID_NC", 0), force_groups = env_int("TPO_GRID_GROUPS", 0);
+  // CTA pairs are correct but slower inside this kernel (profiles/r01/ubench_summary.md): opt-in
+  t.pair = env_int("TPO_GRID_PAIR", 0) ? 1 : 0;
+  auto mss = [&](int n) { return t.pair ? mma_ss_pair(n) : mma_ss(n); };
+  auto mts = [&](int n) { return t.pair ? mma_ts_pair(n) : mma_ts(n); };
   double best = 1e300;
   int best_g = 0, best_nc = 0, best_chunks = 0, best_zg = 0;
   for (int ng = 1; ng <= 8; ++ng) {
@@ -212,9 +220,9 @@ GridTcEntry Context::build_dense_tc(const DenseOps& ops, const char* label) {
       const int nc = pad_to((G + nch - 1) / nch, 16);  // rebalance padding over chunks
       const int np = parts_for(zg);
       // + ~60 cycles per ring stage for the mbarrier wait when a stage's MMAs lack slack
-      const double g1 = 3.0 * ((t.k1p + t.k2p) / 16) * mma_ss(nc) +
-                        ((t.k1p + t.k2p) / 16) * std::max(0.0, 60.0 - 3.0 * (mma_ss(nc) - 45.0)) / (t.same_s ? 2 : 1);
-      const double g2 = 3.0 * (nc / 16) * np * mma_ts(zg / np);
+      const double g1 = 3.0 * ((t.k1p + t.k2p) / 16) * mss(nc) +
+                        ((t.k1p + t.k2p) / 16) * std::max(0.0, 60.0 - 3.0 * (mss(nc) - 45.0)) / (t.same_s ? 2 : 1);
+      const double g2 = 3.0 * (nc / 16) * np * mts(zg / np);
       const double cost = ng * (nch * (g1 + g2 + 400.0) + 1500.0);
       if (cost < best) {
         best = cost;
@@ -246,8 +254,9 @@ GridTcEntry Context::build_dense_tc(const DenseOps& ops, const char* label) {
   const uint32_t epi = 8u * 32u * 17u * 4u;
   const int force_inplace = env_int("TPO_GRID_INPLACE", -1), force_stages = env_int("TPO_GRID_STAGES", 0);
   // two B-operand rings; prefer the separate raw staging buffer, then depth
-  t.s_stage_bytes = static_cast<uint32_t>(64 * nc);
-  t.a_stage_bytes = static_cast<uint32_t>(64 * t.zp);
+  const int kp = t.pair ? 2 : 1;  // each CTA of a pair streams one row half of every slice
+  t.s_stage_bytes = static_cast<uint32_t>(64 * nc / kp);
+  t.a_stage_bytes = static_cast<uint32_t>(64 * t.zp / kp);
   auto fixed = [&](int ip) { return static_cast<int>(xy + (ip ? 0u : raw) + epi); };
   int inplace = -1, s_st = 0, a_st = 0;
   int best_score = -1;
@@ -290,9 +299,9 @@ GridTcEntry Context::build_dense_tc(const DenseOps& ops, const char* label) {
   if (env_int("TPO_GRID_VERBOSE", 0))
     std::fprintf(stderr,
                  "[tpo] %s tcgen05 G=%d din=(%d,%d) dout=%d nc=%d chunks=%d groups=%d zg=%d parts=%d s_stages=%d "
-                 "a_stages=%d inplace=%d smem=%d\n",
+                 "a_stages=%d inplace=%d pair=%d smem=%d\n",
                  label, G, t.din1, t.din2, t.dout_eff, nc, t.nchunks, t.ngroups, t.zg, t.nparts, s_st, a_st, inplace,
-                 t.smem_bytes);
+                 t.pair, t.smem_bytes);
 
   // ---- operators -> fp16 hi / lo slices in the UMMA canonical layout
   double amax = 0.0;
@@ -301,27 +310,30 @@ GridTcEntry Context::build_dense_tc(const DenseOps& ops, const char* label) {
   const double a_scale = std::ldexp(1.0, t.a_shift);
 
   // S slices: [chunk][kstep][hi | lo][nc x 16 canonical]
-  auto build_s = [&](const std::vector<double>& S, int din, int kp, std::vector<uint16_t>& buf) {
-    const size_t half = static_cast<size_t>(nc) * 16;  // elements per hi / lo block
-    const int nks = kp / 16;
-    buf.assign(static_cast<size_t>(t.nchunks) * nks * 2 * half, 0);
+  // one slice = kp row halves, each [hi | lo][(nc / kp) x 16] canonical
+  auto build_s = [&](const std::vector<double>& S, int din, int kpad, std::vector<uint16_t>& buf) {
+    const int rh = nc / kp;                            // rows per half
+    const size_t half = static_cast<size_t>(rh) * 16;  // elements per hi / lo block
+    const int nks = kpad / 16;
+    buf.assign(static_cast<size_t>(t.nchunks) * nks * 2 * nc * 16, 0);
     for (int c = 0; c < t.nchunks; ++c)
-      for (int ks = 0; ks < nks; ++ks) {
-        uint16_t* hi = buf.data() + (static_cast<size_t>(c) * nks + ks) * 2 * half;
-        uint16_t* lo = hi + half;
-        for (int r = 0; r < nc; ++r) {
-          const int gidx = c * nc + r;
-          for (int kk = 0; kk < 16; ++kk) {
-            const int k = ks * 16 + kk;
-            const double v = (gidx < G && k < din) ? S[static_cast<size_t>(gidx) * din + k] : 0.0;
-            uint16_t hv, lv;
-            split_half(v, hv, lv);
-            const uint32_t e = sm100::canon_off(r, kk, nc) / 2;
-            hi[e] = hv;
-            lo[e] = lv;
+      for (int ks = 0; ks < nks; ++ks)
+        for (int hh = 0; hh < kp; ++hh) {
+          uint16_t* hi = buf.data() + (static_cast<size_t>(c) * nks + ks) * 2 * nc * 16 + hh * 2 * half;
+          uint16_t* lo = hi + half;
+          for (int r = 0; r < rh; ++r) {
+            const int gidx = c * nc + hh * rh + r;
+            for (int kk = 0; kk < 16; ++kk) {
+              const int k = ks * 16 + kk;
+              const double v = (gidx < G && k < din) ? S[static_cast<size_t>(gidx) * din + k] : 0.0;
+              uint16_t hv, lv;
+              split_half(v, hv, lv);
+              const uint32_t e = sm100::canon_off(r, kk, rh) / 2;
+              hi[e] = hv;
+              lo[e] = lv;
+            }
           }
         }
-      }
   };
   std::vector<uint16_t> s1, s2, a;
   build_s(ops.s1, t.din1, t.k1p, s1);
@@ -337,30 +349,32 @@ GridTcEntry Context::build_dense_tc(const DenseOps& ops, const char* label) {
   }
   // A slices: [group][chunk][slice][part][hi | lo][zp x 16 canonical]
   {
-    const size_t half = static_cast<size_t>(t.zp) * 16;
-    a.assign(static_cast<size_t>(t.ngroups) * t.nchunks * t.nslices * t.nparts * 2 * half, 0);
+    const int rh = t.zp / kp;
+    const size_t half = static_cast<size_t>(rh) * 16;
+    a.assign(static_cast<size_t>(t.ngroups) * t.nchunks * t.nslices * t.nparts * 2 * t.zp * 16, 0);
     for (int gp = 0; gp < t.ngroups; ++gp)
       for (int c = 0; c < t.nchunks; ++c)
         for (int sl = 0; sl < t.nslices; ++sl)
-          for (int pt = 0; pt < t.nparts; ++pt) {
-            const size_t blk = ((static_cast<size_t>(gp) * t.nchunks + c) * t.nslices + sl) * t.nparts + pt;
-            uint16_t* hi = a.data() + blk * 2 * half;
-            uint16_t* lo = hi + half;
-            for (int rr = 0; rr < t.zp; ++rr) {
-              const int o2 = gp * t.zg + pt * t.zp + rr;
-              for (int kk = 0; kk < 16; ++kk) {
-                const int gidx = c * nc + sl * 16 + kk;
-                double v = 0.0;
-                if (gidx < G && o2 < t.dout_eff && pt * t.zp + rr < t.zg)
-                  v = ops.a[static_cast<size_t>(o2) * G + gidx] * a_scale;
-                uint16_t hv, lv;
-                split_half(v, hv, lv);
-                const uint32_t e = sm100::canon_off(rr, kk, t.zp) / 2;
-                hi[e] = hv;
-                lo[e] = lv;
+          for (int pt = 0; pt < t.nparts; ++pt)
+            for (int hh = 0; hh < kp; ++hh) {
+              const size_t blk = ((static_cast<size_t>(gp) * t.nchunks + c) * t.nslices + sl) * t.nparts + pt;
+              uint16_t* hi = a.data() + blk * 2 * t.zp * 16 + hh * 2 * half;
+              uint16_t* lo = hi + half;
+              for (int rr = 0; rr < rh; ++rr) {
+                const int row = pt * t.zp + hh * rh + rr;  // output row within the group
+                const int o2 = gp * t.zg + row;
+                for (int kk = 0; kk < 16; ++kk) {
+                  const int gidx = c * nc + sl * 16 + kk;
+                  double v = 0.0;
+                  if (gidx < G && o2 < t.dout_eff && row < t.zg) v = ops.a[static_cast<size_t>(o2) * G + gidx] * a_scale;
+                  uint16_t hv, lv;
+                  split_half(v, hv, lv);
+                  const uint32_t e = sm100::canon_off(rr, kk, rh) / 2;
+                  hi[e] = hv;
+                  lo[e] = lv;
+                }
               }
             }
-          }
     t.a_slice_bytes = static_cast<uint32_t>(64 * t.zp);
     t.a = reinterpret_cast<const uint8_t*>(upload(a));
   }

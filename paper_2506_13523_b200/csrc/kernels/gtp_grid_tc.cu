@@ -75,11 +75,32 @@ __device__ __forceinline__ Unit unit_of(int64_t u, int ngroups) {
   return Unit{u / ngroups, static_cast<int>(u % ngroups)};
 }
 
-// CTA b owns the contiguous unit range [u_begin, u_end): consecutive units
-// are the output groups of one tile, which then reuses its resident X / Y
-__device__ __forceinline__ void unit_range(int64_t nunits, int64_t& u_begin, int64_t& u_end) {
-  u_begin = nunits * blockIdx.x / gridDim.x;
-  u_end = nunits * (blockIdx.x + 1) / gridDim.x;
+// worker idx of cnt owns the contiguous unit range [u_begin, u_end):
+// consecutive units are the output groups of one tile, which then reuses its
+// resident X / Y
+__device__ __forceinline__ void unit_range(int64_t nunits, int64_t idx, int64_t cnt, int64_t& u_begin,
+                                           int64_t& u_end) {
+  u_begin = nunits * idx / cnt;
+  u_end = nunits * (idx + 1) / cnt;
+}
+
+// arrive `count` on a barrier of the MMA-issuing CTA (the pair leader, rank 0).
+// kTmemOnly: the dependency is TMEM traffic already completed and fenced
+// (tcgen05.wait + fence::before_thread_sync), so the remote arrive can be
+// relaxed and does not wait for this thread's outstanding global stores.
+template <bool PAIR, bool kTmemOnly = false>
+__device__ __forceinline__ void arrive_leader(uint64_t* bar, uint32_t count, uint32_t rank) {
+  if (PAIR && rank != 0) {
+    if (kTmemOnly) mbar_arrive_cluster_relaxed(mapa_shared(smem_u32(bar), 0), count);
+    else mbar_arrive_cluster(mapa_shared(smem_u32(bar), 0), count);
+  } else {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+  }
+}
+template <bool PAIR>
+__device__ __forceinline__ void wait_leader(uint64_t* bar, uint32_t parity) {
+  if (PAIR) mbar_wait_cluster(bar, parity);
+  else mbar_wait(bar, parity);
 }
 
 // a tile whose x / y rows are one contiguous, 16-byte aligned block can be
@@ -163,7 +184,14 @@ __device__ __noinline__ void convert_input(const float* raw, int din, int kp, ui
 constexpr int kProfSlots = 16;
 __device__ unsigned long long* g_prof = nullptr;
 
-template <bool PROF>
+// PAIR: CTA pairs (cluster of 2) run tcgen05.mma.cta_group::2 with M = 256:
+// each CTA owns 128 rows (its own X / Y, TMEM lanes, epilogue) and streams
+// only its half of every B operand (S / A slice halves), halving the shared
+// memory read traffic of GEMM 1, the ring TMA writes per SM and -- most
+// important -- the number of MMA instructions per unit of work.  Rank 0
+// issues every MMA; its commits multicast to both CTAs; the rank-1 MMA warp
+// forwards "my half landed" to rank 0's ring slots; workers signal rank 0.
+template <bool PROF, bool PAIR>
 __global__ void __launch_bounds__(kThreads, 1)
     gtp_grid_tc_kernel(const __grid_constant__ GridTcTables t, const __grid_constant__ RowSpec rs) {
   unsigned long long pc[kProfSlots];
@@ -178,28 +206,43 @@ __global__ void __launch_bounds__(kThreads, 1)
   __shared__ float part_sh[2 * BM];
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t rank = PAIR ? cluster_ctarank() : 0u;
+  const bool leader = rank == 0;
+  constexpr int kPair = PAIR ? 2 : 1;
   if (tid == 0) {
     for (int i = 0; i < kNumBars; ++i) {
       uint32_t cnt = 1;
-      if (i == B_RAW_FREE || i == B_XY_READY || i == B_Z_EMPTY) cnt = kWorkers;
-      if (i >= B_P_READY && i < B_P_READY + kMaxSlices) cnt = BM;
+      if (i == B_RAW_FREE) cnt = kWorkers;
+      if (i == B_XY_READY || i == B_Z_EMPTY) cnt = kWorkers * kPair;
+      if (i >= B_P_READY && i < B_P_READY + kMaxSlices) cnt = BM * kPair;
+      // the leader's ring slots complete with its own bulk copy + the peer's forward
+      if (PAIR && leader && ((i >= B_SFULL && i < B_SFULL + kMaxStages) || (i >= B_AFULL && i < B_AFULL + kMaxStages)))
+        cnt = 2;
       mbar_init(&bars[i], cnt);
     }
     fence_mbar_init();
   }
   if (warp == 1) {
-    tmem_alloc(&tmem_sh, 512);
-    tmem_relinquish();
+    if (PAIR) {
+      tmem_alloc_pair(&tmem_sh, 512);
+      tmem_relinquish_pair();
+    } else {
+      tmem_alloc(&tmem_sh, 512);
+      tmem_relinquish();
+    }
   }
   tc_fence_before();
-  __syncthreads();
+  if (PAIR) cluster_sync_all();
+  else __syncthreads();
   tc_fence_after();
   const uint32_t tmem = tmem_sh;
 
-  const int64_t ntiles = (rs.rows + BM - 1) / BM;
+  // a unit tile is kPair x 128 rows; this CTA owns the 128 rows of tile ut * kPair + rank
+  const int64_t ntiles = (rs.rows + BM * kPair - 1) / (BM * kPair);
   const int64_t nunits = ntiles * t.ngroups;
   int64_t u_begin, u_end;
-  unit_range(nunits, u_begin, u_end);
+  unit_range(nunits, blockIdx.x / kPair, gridDim.x / kPair, u_begin, u_end);
+  auto my_tile = [&](int64_t ut) { return ut * kPair + rank; };
   uint8_t* xh = smem + t.off_x;
   uint8_t* xl = xh + BM * t.k1p * 2;
   uint8_t* yh = smem + t.off_y;
@@ -220,8 +263,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t ph = 0;
       auto push = [&](const uint8_t* src, uint32_t bytes) {
         mbar_wait(&bars[B_SEMPTY + stage], ph ^ 1);
-        if (pl) mbar_arrive_expect_tx(&bars[B_SFULL + stage], bytes);
-        if (pl) bulk_g2s(sring + stage * t.s_stage_bytes, src, bytes, &bars[B_SFULL + stage]);
+        if (pl) mbar_arrive_expect_tx(&bars[B_SFULL + stage], t.s_stage_bytes);
+        if (pl)
+          bulk_g2s(sring + stage * t.s_stage_bytes, src + (PAIR ? rank * t.s_stage_bytes : 0u), t.s_stage_bytes,
+                   &bars[B_SFULL + stage]);
         if (++stage == t.s_stages) {
           stage = 0;
           ph ^= 1;
@@ -240,7 +285,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       int64_t v = 0;  // tile sequence number
       if (u_begin < u_end) {
         const Unit u0 = unit_of(u_begin, t.ngroups);
-        if (tile_tma_ok(rs, u0.tile)) issue_raw(u0.tile, 0);
+        if (tile_tma_ok(rs, my_tile(u0.tile))) issue_raw(my_tile(u0.tile), 0);
       }
       for (int64_t u = u_begin; u < u_end; ++u) {
         const Unit cu = unit_of(u, t.ngroups);
@@ -258,7 +303,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const bool raw_point = t.raw_inplace ? (last_of_tile && c == t.nchunks - 1) : (first_of_tile && c == 0);
           if (raw_point && has_next) {
             const Unit nu = unit_of(next_u, t.ngroups);
-            if (tile_tma_ok(rs, nu.tile)) issue_raw(nu.tile, v + 1);
+            if (tile_tma_ok(rs, my_tile(nu.tile))) issue_raw(my_tile(nu.tile), v + 1);
           }
         }
         if (last_of_tile) ++v;
@@ -276,9 +321,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int n = t.nchunks * t.nslices * t.nparts;
         for (int k = 0; k < n; ++k) {
           mbar_wait(&bars[B_AEMPTY + stage], ph ^ 1);
-          if (pl) mbar_arrive_expect_tx(&bars[B_AFULL + stage], t.a_slice_bytes);
-          if (pl) bulk_g2s(aring + stage * t.a_stage_bytes, t.a + (abase + k) * t.a_slice_bytes, t.a_slice_bytes,
-                   &bars[B_AFULL + stage]);
+          if (pl) mbar_arrive_expect_tx(&bars[B_AFULL + stage], t.a_stage_bytes);
+          if (pl)
+            bulk_g2s(aring + stage * t.a_stage_bytes,
+                     t.a + (abase + k) * t.a_slice_bytes + (PAIR ? rank * t.a_stage_bytes : 0u), t.a_stage_bytes,
+                     &bars[B_AFULL + stage]);
           if (++stage == t.a_stages) {
             stage = 0;
             ph ^= 1;
@@ -293,14 +340,39 @@ __global__ void __launch_bounds__(kThreads, 1)
     // descriptors live in uniform registers without a divergent waterfall per
     // MMA, which lowers the per-instruction issue cost of the single issuer.
     const bool leader_lane = elect_one_sync();
-    {
+    if (PAIR && !leader) {
+      // rank 1: forward "my half of this ring slot landed" to the leader's slot,
+      // in the order the leader consumes the rings (chunk: S slices, A slices)
+      int s_stage = 0, a_stage = 0;
+      uint32_t s_ph = 0, a_ph = 0;
+      const int s_per_chunk = t.k1p / 16 + (t.same_s ? 0 : t.k2p / 16);
+      for (int64_t u = u_begin; u < u_end; ++u)
+        for (int c = 0; c < t.nchunks; ++c) {
+          for (int k = 0; k < s_per_chunk; ++k) {
+            mbar_wait(&bars[B_SFULL + s_stage], s_ph);
+            if (leader_lane) arrive_leader<PAIR>(&bars[B_SFULL + s_stage], 1, rank);
+            if (++s_stage == t.s_stages) {
+              s_stage = 0;
+              s_ph ^= 1;
+            }
+          }
+          for (int k = 0; k < t.nslices * t.nparts; ++k) {
+            mbar_wait(&bars[B_AFULL + a_stage], a_ph);
+            if (leader_lane) arrive_leader<PAIR>(&bars[B_AFULL + a_stage], 1, rank);
+            if (++a_stage == t.a_stages) {
+              a_stage = 0;
+              a_ph ^= 1;
+            }
+          }
+        }
+    } else {
       int s_stage = 0, a_stage = 0;
       uint32_t s_ph = 0, a_ph = 0;
       // next slice of a ring: wait until it landed, return its shared-memory address
       auto take_s = [&](uint32_t& slot) -> uint32_t {
         slot = B_SEMPTY + s_stage;
         const auto t0 = now();
-        mbar_wait(&bars[B_SFULL + s_stage], s_ph);
+        wait_leader<PAIR>(&bars[B_SFULL + s_stage], s_ph);
         pc[2] += now() - t0;
         tc_fence_after();
         const uint32_t a = smem_u32(sring + s_stage * t.s_stage_bytes);
@@ -313,7 +385,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       auto take_a = [&](uint32_t& slot) -> uint32_t {
         slot = B_AEMPTY + a_stage;
         const auto t0 = now();
-        mbar_wait(&bars[B_AFULL + a_stage], a_ph);
+        wait_leader<PAIR>(&bars[B_AFULL + a_stage], a_ph);
         pc[6] += now() - t0;
         tc_fence_after();
         const uint32_t a = smem_u32(aring + a_stage * t.a_stage_bytes);
@@ -323,10 +395,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         return a;
       };
-      const uint32_t id1 = idesc_f16(BM, t.nc), id2 = idesc_f16(BM, t.zp);
+      // pair: M = 256 and each CTA's B tile is its row half (nc / 2 or zp / 2 rows)
+      const uint32_t id1 = idesc_f16(BM * kPair, t.nc), id2 = idesc_f16(BM * kPair, t.zp);
       const uint32_t lbo_x = (BM / 8) * 128;
-      const uint32_t lbo_s = (t.nc / 8) * 128, lbo_a = (t.zp / 8) * 128;
-      const uint32_t s_half = t.nc * 32, a_half = t.zp * 32;  // lo block offset inside a slice
+      const uint32_t bn_s = t.nc / kPair, bn_a = t.zp / kPair;
+      const uint32_t lbo_s = (bn_s / 8) * 128, lbo_a = (bn_a / 8) * 128;
+      const uint32_t s_half = bn_s * 32, a_half = bn_a * 32;  // lo block offset inside a stage
       const uint64_t dx_hi = make_sdesc(smem_u32(xh), lbo_x, 128), dx_lo = make_sdesc(smem_u32(xl), lbo_x, 128);
       const uint64_t dy_hi = make_sdesc(smem_u32(yh), lbo_x, 128), dy_lo = make_sdesc(smem_u32(yl), lbo_x, 128);
       const uint64_t kstep_x = (2 * lbo_x) >> 4;  // descriptor advance per K-step of X/Y
@@ -339,7 +413,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const bool last_of_tile = (u + 1 == u_end) || unit_of(u + 1, t.ngroups).tile != cu.tile;
         if (first_of_tile) {
           const auto t0 = now();
-          mbar_wait(&bars[B_XY_READY], static_cast<uint32_t>(v & 1));
+          wait_leader<PAIR>(&bars[B_XY_READY], static_cast<uint32_t>(v & 1));
           pc[1] += now() - t0;
           tc_fence_after();
         }
@@ -358,57 +432,61 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint64_t bh = make_sdesc(sb, lbo_s, 128), bl = make_sdesc(sb + s_half, lbo_s, 128);
             const uint64_t ah = dx_hi + ks * kstep_x, al = dx_lo + ks * kstep_x;
             const uint32_t acc = ks > 0 ? 1u : 0u;
-            if (leader_lane) mma_f16_ss(tmem + fx, ah, bh, id1, acc);
-            if (leader_lane) mma_f16_ss(tmem + fx, ah, bl, id1, 1u);
-            if (leader_lane) mma_f16_ss(tmem + fx, al, bh, id1, 1u);
+            if (leader_lane) (PAIR ? mma_f16_ss_pair : mma_f16_ss)(tmem + fx, ah, bh, id1, acc);
+            if (leader_lane) (PAIR ? mma_f16_ss_pair : mma_f16_ss)(tmem + fx, ah, bl, id1, 1u);
+            if (leader_lane) (PAIR ? mma_f16_ss_pair : mma_f16_ss)(tmem + fx, al, bh, id1, 1u);
             if (t.same_s) {
               const uint64_t yh_ = dy_hi + ks * kstep_x, yl_ = dy_lo + ks * kstep_x;
-              if (leader_lane) mma_f16_ss(tmem + fy, yh_, bh, id1, acc);
-              if (leader_lane) mma_f16_ss(tmem + fy, yh_, bl, id1, 1u);
-              if (leader_lane) mma_f16_ss(tmem + fy, yl_, bh, id1, 1u);
+              if (leader_lane) (PAIR ? mma_f16_ss_pair : mma_f16_ss)(tmem + fy, yh_, bh, id1, acc);
+              if (leader_lane) (PAIR ? mma_f16_ss_pair : mma_f16_ss)(tmem + fy, yh_, bl, id1, 1u);
+              if (leader_lane) (PAIR ? mma_f16_ss_pair : mma_f16_ss)(tmem + fy, yl_, bh, id1, 1u);
             }
-            if (leader_lane) tc_commit(&bars[slot]);
+            if (leader_lane) (PAIR ? tc_commit_pair : tc_commit)(&bars[slot]);
           }
           if (!t.same_s) {
             for (int ks = 0; ks < t.k2p / 16; ++ks) {
               uint32_t slot;
               const uint32_t sb = take_s(slot);
-              const uint32_t s2_half = t.nc * 32;
+              const uint32_t s2_half = s_half;
               const uint64_t bh = make_sdesc(sb, lbo_s, 128), bl = make_sdesc(sb + s2_half, lbo_s, 128);
               const uint64_t ah = dy_hi + ks * kstep_x, al = dy_lo + ks * kstep_x;
               const uint32_t acc = ks > 0 ? 1u : 0u;
-              if (leader_lane) mma_f16_ss(tmem + fy, ah, bh, id1, acc);
-              if (leader_lane) mma_f16_ss(tmem + fy, ah, bl, id1, 1u);
-              if (leader_lane) mma_f16_ss(tmem + fy, al, bh, id1, 1u);
-              if (leader_lane) tc_commit(&bars[slot]);
+              if (leader_lane) (PAIR ? mma_f16_ss_pair : mma_f16_ss)(tmem + fy, ah, bh, id1, acc);
+              if (leader_lane) (PAIR ? mma_f16_ss_pair : mma_f16_ss)(tmem + fy, ah, bl, id1, 1u);
+              if (leader_lane) (PAIR ? mma_f16_ss_pair : mma_f16_ss)(tmem + fy, al, bh, id1, 1u);
+              if (leader_lane) (PAIR ? tc_commit_pair : tc_commit)(&bars[slot]);
             }
           }
-          if (leader_lane) tc_commit(&bars[B_F_FULL]);
-          if (c == t.nchunks - 1 && last_of_tile) if (leader_lane) tc_commit(&bars[B_XY_FREE]);
+          if (leader_lane) (PAIR ? tc_commit_pair : tc_commit)(&bars[B_F_FULL]);
+          if (c == t.nchunks - 1 && last_of_tile) if (leader_lane) (PAIR ? tc_commit_pair : tc_commit)(&bars[B_XY_FREE]);
           // ---- GEMM 2: Z += P A^T, P (hi/lo fp16) read from TMEM in place of F_x
           if (c == 0 && i > 0) {  // previous unit's epilogue has drained Z
             const auto t0 = now();
-            mbar_wait(&bars[B_Z_EMPTY], static_cast<uint32_t>((i - 1) & 1));
+            wait_leader<PAIR>(&bars[B_Z_EMPTY], static_cast<uint32_t>((i - 1) & 1));
             pc[4] += now() - t0;
             tc_fence_after();
           }
           for (int s = 0; s < t.nslices; ++s) {
-            { const auto t0 = now(); mbar_wait(&bars[B_P_READY + s], static_cast<uint32_t>(j & 1)); pc[3] += now() - t0; }
+            {
+              const auto t0 = now();
+              wait_leader<PAIR>(&bars[B_P_READY + s], static_cast<uint32_t>(j & 1));
+              pc[3] += now() - t0;
+            }
             const uint32_t p_hi = tmem + fx + 16 * s, p_lo = p_hi + 8;
             for (int pt = 0; pt < t.nparts; ++pt) {
               uint32_t slot;
               const uint32_t sb = take_a(slot);
               const uint64_t bh = make_sdesc(sb, lbo_a, 128), bl = make_sdesc(sb + a_half, lbo_a, 128);
               const uint32_t zd = tmem + pt * t.zp;
-              if (leader_lane) mma_f16_ts(zd, p_hi, bh, id2, (c == 0 && s == 0) ? 0u : 1u);
-              if (leader_lane) mma_f16_ts(zd, p_hi, bl, id2, 1u);
-              if (leader_lane) mma_f16_ts(zd, p_lo, bh, id2, 1u);
-              if (leader_lane) tc_commit(&bars[slot]);
+              if (leader_lane) (PAIR ? mma_f16_ts_pair : mma_f16_ts)(zd, p_hi, bh, id2, (c == 0 && s == 0) ? 0u : 1u);
+              if (leader_lane) (PAIR ? mma_f16_ts_pair : mma_f16_ts)(zd, p_hi, bl, id2, 1u);
+              if (leader_lane) (PAIR ? mma_f16_ts_pair : mma_f16_ts)(zd, p_lo, bh, id2, 1u);
+              if (leader_lane) (PAIR ? tc_commit_pair : tc_commit)(&bars[slot]);
             }
           }
-          if (leader_lane) tc_commit(&bars[B_G2_DONE]);
+          if (leader_lane) (PAIR ? tc_commit_pair : tc_commit)(&bars[B_G2_DONE]);
         }
-        if (leader_lane) tc_commit(&bars[B_Z_FULL]);
+        if (leader_lane) (PAIR ? tc_commit_pair : tc_commit)(&bars[B_Z_FULL]);
         if (last_of_tile) ++v;
       }
       pc[0] = now() - t_start;
@@ -425,10 +503,23 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t n_raw = 0;
     int64_t j = 0;
 
+    // worker -> MMA-issuer signals: per thread locally, per warp (count 32) to the pair leader
+    auto signal_leader = [&](uint64_t* bar, bool tmem_only) {
+      if (PAIR) {
+        __syncwarp();
+        if (lane == 0) {
+          if (tmem_only) arrive_leader<PAIR, true>(bar, 32, rank);
+          else arrive_leader<PAIR>(bar, 32, rank);
+        }
+      } else {
+        mbar_arrive(bar);
+      }
+    };
     auto convert = [&](int64_t u, int64_t iu) {
       const Unit cu = unit_of(u, t.ngroups);
       const int buf = static_cast<int>(iu & 1);
-      const bool tma = tile_tma_ok(rs, cu.tile);
+      const int64_t tile = my_tile(cu.tile);
+      const bool tma = tile_tma_ok(rs, tile);
       named_bar_sync(1, kWorkers);  // part_sh / raw of the previous conversion fully consumed
       if (tma) {
         mbar_wait(&bars[B_RAW_FULL], n_raw & 1);
@@ -436,7 +527,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       } else {
         // gather path: the raw region must be free (in-place: previous GEMM 1 retired)
         if (t.raw_inplace && iu > 0) mbar_wait(&bars[B_XY_FREE], static_cast<uint32_t>((iu - 1) & 1));
-        const int64_t row0 = cu.tile * BM;
+        const int64_t row0 = tile * BM;
         for (int idx = wt; idx < BM * t.din1; idx += kWorkers) {
           const int rr = idx / t.din1;
           raw_x[idx] = (row0 + rr < rs.rows) ? __ldg(rs.x + row0 * t.din1 + idx) : 0.f;
@@ -466,7 +557,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_arrive(&bars[B_RAW_FREE]);
       }
       fence_proxy_async_smem();
-      mbar_arrive(&bars[B_XY_READY]);
+      signal_leader(&bars[B_XY_READY], false);
     };
 
     int64_t i = 0;  // unit counter
@@ -483,7 +574,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const auto tp0 = now();
         for (int s = h; s < t.nslices; s += 2) {
           if (t.dbg & 1) {
-            mbar_arrive(&bars[B_P_READY + s]);
+            signal_leader(&bars[B_P_READY + s], true);
             continue;
           }
           uint32_t vx[16], vy[16];
@@ -504,7 +595,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           tmem_st8(lane_base + fx + 16 * s + 8, lw);
           tmem_wait_st();
           tc_fence_before();
-          mbar_arrive(&bars[B_P_READY + s]);
+          signal_leader(&bars[B_P_READY + s], true);
         }
         pc[10] += now() - tp0;
       }
@@ -519,7 +610,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const auto te0 = now();
       tc_fence_after();
       const int e_row = ex_sh[buf][r] + ey_sh[buf][r] - t.a_shift;
-      const int64_t row0 = cu.tile * BM + q * 32;
+      const int64_t row0 = my_tile(cu.tile) * BM + q * 32;
       const int col0 = cu.g * t.zg;
       const int col_end = min(col0 + t.zg, t.dout_eff);
       const int nblk = t.zg / 16;
@@ -544,7 +635,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         __syncwarp();
       }
       tc_fence_before();
-      mbar_arrive(&bars[B_Z_EMPTY]);
+      signal_leader(&bars[B_Z_EMPTY], true);
       pc[13] += now() - te0;
       // degrees past the product band are exactly zero (proj/src/gtp.cpp:237-258)
       if (cu.g == t.ngroups - 1 && t.dout_total > t.dout_eff && h == 0) {
@@ -561,16 +652,20 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int k = 8; k < kProfSlots; ++k) g_prof[blockIdx.x * kProfSlots + k] = pc[k];
   }
   tc_fence_before();
-  __syncthreads();
+  if (PAIR) cluster_sync_all();
+  else __syncthreads();
   tc_fence_after();
-  if (warp == 1) tmem_dealloc(tmem, 512);
+  if (warp == 1) {
+    if (PAIR) tmem_dealloc_pair(tmem, 512);
+    else tmem_dealloc(tmem, 512);
+  }
 }
 
 }  // namespace
 
 int gtp_grid_tc_max_smem() {
   cudaFuncAttributes a{};
-  if (cudaFuncGetAttributes(&a, gtp_grid_tc_kernel<false>) != cudaSuccess) return 0;
+  if (cudaFuncGetAttributes(&a, gtp_grid_tc_kernel<false, true>) != cudaSuccess) return 0;
   int dev = 0, optin = 0;
   cudaGetDevice(&dev);
   if (cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess) return 0;
@@ -583,26 +678,43 @@ cudaError_t launch_gtp_grid_tc(const GridTcTables& t, const RowSpec& rs, int num
     const char* v = std::getenv("TPO_GRID_PROF");
     return v && *v == '1';
   }();
-  auto kern = prof ? gtp_grid_tc_kernel<true> : gtp_grid_tc_kernel<false>;
+  auto kern = t.pair ? (prof ? gtp_grid_tc_kernel<true, true> : gtp_grid_tc_kernel<false, true>)
+                     : (prof ? gtp_grid_tc_kernel<true, false> : gtp_grid_tc_kernel<false, false>);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, t.smem_bytes);
   if (e != cudaSuccess) return e;
-  const int64_t units = ((rs.rows + BM - 1) / BM) * t.ngroups;
-  const int grid = static_cast<int>(std::min<int64_t>(units, num_sms));
+  const int kp = t.pair ? 2 : 1;
+  const int64_t units = ((rs.rows + BM * kp - 1) / (BM * kp)) * t.ngroups;
+  const int grid = kp * static_cast<int>(std::min<int64_t>(units, num_sms / kp));
   unsigned long long* buf = nullptr;
   if (prof) {
     cudaMalloc(&buf, sizeof(unsigned long long) * kProfSlots * grid);
     cudaMemset(buf, 0, sizeof(unsigned long long) * kProfSlots * grid);
     cudaMemcpyToSymbol(g_prof, &buf, sizeof(buf));
   }
-  kern<<<grid, kThreads, t.smem_bytes, s>>>(t, rs);
-  e = cudaGetLastError();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = t.smem_bytes;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = kp;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  e = cudaLaunchKernelEx(&cfg, kern, t, rs);
   if (prof && e == cudaSuccess) {
     std::vector<unsigned long long> h(kProfSlots * grid);
     cudaStreamSynchronize(s);
     cudaMemcpy(h.data(), buf, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+    // MMA slots averaged over the MMA-issuing CTAs (pair leaders), worker slots over all
     double avg[kProfSlots] = {};
+    int n_mma = 0;
+    for (int b = 0; b < grid; ++b) n_mma += h[b * kProfSlots] != 0;
     for (int b = 0; b < grid; ++b)
-      for (int k = 0; k < kProfSlots; ++k) avg[k] += static_cast<double>(h[b * kProfSlots + k]) / grid;
+      for (int k = 0; k < kProfSlots; ++k)
+        avg[k] += static_cast<double>(h[b * kProfSlots + k]) / (k < 8 ? std::max(n_mma, 1) : grid);
     std::fprintf(stderr,
                  "[tpo-prof] units=%lld grid=%d MMA: total %.0f xy_ready %.0f s_ring %.0f p_ready %.0f z_empty %.0f "
                  "g2_done %.0f a_ring %.0f | worker: total %.0f f_full %.0f product %.0f convert %.0f z_full %.0f epilogue %.0f\n",

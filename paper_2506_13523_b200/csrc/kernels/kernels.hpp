@@ -56,6 +56,7 @@ struct GridTcTables {
   uint32_t s_stage_bytes, a_stage_bytes;
   int raw_inplace;           // raw input tiles land in the X/Y operand buffers
   int safe_war;              // wait for GEMM 2 of chunk c before GEMM 1 of chunk c+1
+  int pair;                  // CTA pairs, tcgen05 cta_group::2 (M = 256); slices stored as two row halves
   int dbg;                   // timing experiments only (results invalid): 1 no product, 2 no epilogue, 4 no convert
   int smem_bytes;
   uint32_t off_x, off_y, off_raw, off_sring, off_aring, off_stage;  // dynamic shared-memory carve-up

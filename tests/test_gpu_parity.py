@@ -275,3 +275,35 @@ def test_native_library_loaded(tpo, orc):
     assert ctx.launches > before
     with open("/proc/self/maps") as f:
         assert "libtpo_b200.so" in f.read()
+
+
+def test_gtp_cta_pair_path():
+    # opt-in tcgen05 cta_group::2 path (CTA pairs, M = 256): parity in a fresh
+    # process because the mode is fixed when the device tables are built
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parents[1]
+    code = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, %r); sys.path.insert(0, %r)
+import oracle, paper_2506_13523_b200 as tpo
+tpo.context(0).set_grid_path("tc")
+worst = 0.0
+for kind in ("gtp_grid", "gtp_fourier"):
+    for L, B in ((1, 300), (4, 700), (7, 300), (10, 300)):
+        rng = np.random.default_rng(900 + L)
+        d = (L + 1) ** 2
+        x = rng.standard_normal((B, d)).astype(np.float32); y = rng.standard_normal((B, d)).astype(np.float32)
+        out = tpo.run(kind, torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda(), L, L, 2 * L).cpu().numpy()
+        ref = oracle.batch_mimo(kind, L, x.astype(np.float64)[:, None], y.astype(np.float64)[:, None])[:, 0]
+        err = (np.abs(out - ref).max(axis=1) / np.maximum(np.abs(ref).max(axis=1), 1e-300)).max()
+        worst = max(worst, float(err))
+print(worst)
+""" % (str(root), str(root / "oracle"))
+    env = dict(os.environ, TPO_GRID_PAIR="1")
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=240, env=env)
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert float(r.stdout.strip().splitlines()[-1]) <= TOL
