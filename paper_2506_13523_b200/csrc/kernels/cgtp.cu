@@ -33,34 +33,66 @@ constexpr int kRows = 32;  // rows per tile
 // (shared-y tiles) instead of 32 LDS + 32 FFMA.
 constexpr int kPitch = kRows + 4;  // 144 B: consecutive coefficients start 4 banks apart
 
+constexpr int kPf = 8;  // prefetch registers per thread and input (tiles of din <= 64)
+
 template <bool kEdgeTile>
 __global__ void __launch_bounds__(kCgtpChunk)
     cgtp_kernel(const __grid_constant__ CgtpTables t, const __grid_constant__ RowSpec rs) {
   extern __shared__ __align__(16) float sm[];
-  float* xs = sm;                          // [din1][kPitch]
-  float* ys = sm + t.din1 * kPitch;        // [din2][kPitch] (edge tiles: [din2])
+  const int buf_floats = (t.din1 + t.din2) * kPitch;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t ntiles = (rs.rows + kRows - 1) / kRows;
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+  // element e of a tile is (row e % 32, coefficient e / 32): consecutive lanes take consecutive
+  // rows, so the transposed shared-memory stores xs[k][r] hit consecutive banks
+  // register prefetch of the next tile for shared-y edge tiles (config C4); other shapes load
+  // synchronously with coalesced reads (fewer registers -> more resident blocks)
+  const bool prefetch = kEdgeTile && t.din1 * kRows <= kPf * kCgtpChunk;
+  float px[kPf];
+  auto load_regs = [&](int64_t tile) {
+    const int64_t row0 = tile * kRows;
+#pragma unroll
+    for (int q = 0; q < kPf; ++q) {
+      const int e = tid + q * kCgtpChunk;
+      const int r = e & (kRows - 1), k = e >> 5;
+      const int64_t g = row0 + r;
+      px[q] = (k < t.din1 && tile < ntiles && g < rs.rows) ? __ldg(rs.x + g * t.din1 + k) : 0.f;
+
+    }
+  };
+  int b = 0;
+  if (prefetch) load_regs(blockIdx.x);
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, b ^= (prefetch ? 1 : 0)) {
     const int64_t row0 = tile * kRows;
     const int64_t left = rs.rows - row0;
     const int nr = left < kRows ? static_cast<int>(left) : kRows;
-    __syncthreads();  // previous tile's readers are done
-    for (int i = tid; i < kRows * t.din1; i += kCgtpChunk) {
-      const int r = i / t.din1, k = i - r * t.din1;
-      xs[k * kPitch + r] = r < nr ? __ldg(rs.x + row0 * t.din1 + i) : 0.f;
-    }
-    if (kEdgeTile) {
-      for (int k = tid; k < t.din2; k += kCgtpChunk) ys[k] = __ldg(rs.y + (row0 / rs.channels) * t.din2 + k);
-    } else {
-      for (int i = tid; i < kRows * t.din2; i += kCgtpChunk) {
-        const int r = i / t.din2, k = i - r * t.din2;
-        const int64_t g = row0 + r;
-        const int64_t yr = rs.y_shared ? g / rs.channels : g;
-        ys[k * kPitch + r] = r < nr ? __ldg(rs.y + yr * t.din2 + k) : 0.f;
+    float* xs = sm + b * buf_floats;       // [din1][kPitch]
+    float* ys = xs + t.din1 * kPitch;      // [din2][kPitch] (edge tiles: [din2])
+    if (prefetch) {
+      // double-buffered tiles: the readers of buffer b finished before the previous barrier
+#pragma unroll
+      for (int q = 0; q < kPf; ++q) {
+        const int e = tid + q * kCgtpChunk;
+        const int r = e & (kRows - 1), k = e >> 5;
+        if (k < t.din1) xs[k * kPitch + r] = px[q];
       }
+    } else {
+      __syncthreads();  // single buffer: previous tile's readers are done
+      for (int i = tid; i < kRows * t.din1; i += kCgtpChunk) {  // coalesced rows
+        const int r = i / t.din1, k = i - r * t.din1;
+        xs[k * kPitch + r] = r < nr ? __ldg(rs.x + row0 * t.din1 + i) : 0.f;
+      }
+      if (!kEdgeTile)
+        for (int i = tid; i < kRows * t.din2; i += kCgtpChunk) {
+          const int r = i / t.din2, k = i - r * t.din2;
+          const int64_t g = row0 + r;
+          const int64_t yr = rs.y_shared ? g / rs.channels : g;
+          ys[k * kPitch + r] = r < nr ? __ldg(rs.y + yr * t.din2 + k) : 0.f;
+        }
     }
+    if (kEdgeTile)
+      for (int k = tid; k < t.din2; k += kCgtpChunk) ys[k] = __ldg(rs.y + (row0 / rs.channels) * t.din2 + k);
     __syncthreads();
+    if (prefetch) load_regs(tile + gridDim.x);  // in flight during this tile's compute
     for (int q = 0; q < t.nchunks; ++q) {
       const int o = q * kCgtpChunk + tid;
       const int wid = q * (kCgtpChunk / 32) + warp;
@@ -112,7 +144,9 @@ cudaError_t launch_cgtp(const CgtpTables& t, const RowSpec& rs, int num_sms, cud
   if (rs.rows <= 0) return cudaSuccess;
   // every tile inside one edge: channels a multiple of the tile height
   const bool edge = rs.y_shared && rs.channels % kRows == 0;
-  const size_t smem = sizeof(float) * kPitch * (t.din1 + t.din2);
+  // edge tiles with register prefetch use a double-buffered tile
+  const bool dbl = edge && t.din1 * kRows <= kPf * kCgtpChunk;
+  const size_t smem = (dbl ? 2 : 1) * sizeof(float) * kPitch * (t.din1 + t.din2);
   auto kern = edge ? cgtp_kernel<true> : cgtp_kernel<false>;
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
