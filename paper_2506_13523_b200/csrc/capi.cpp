@@ -2,6 +2,7 @@
 #include "tpo_capi.h"
 
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <string>
 #include <vector>
@@ -292,7 +293,11 @@ int tpo_run_host_f32(tpo_ctx* ctx, int kind, int L1, int L2, int L3, int l_tilde
     const int64_t d1 = (L1 + 1) * (L1 + 1), d2 = (L2 + 1) * (L2 + 1);
     // chunk = whole batch entries (y_shared rows stay with their channels), ~8 MiB of traffic
     const int64_t bytes_per_b = 4 * channels * (d1 + dout + (y_shared ? 0 : d2)) + (y_shared ? 4 * d2 : 0);
-    int64_t bc = std::max<int64_t>(1, (8ll << 20) / std::max<int64_t>(bytes_per_b, 1));
+    static const int64_t chunk_bytes = [] {
+      const char* v = std::getenv("TPO_HOST_CHUNK_KB");
+      return (v && *v) ? std::atoll(v) * 1024 : (16ll << 20);  // measured best: 8-16 MiB (tools/e2e_chunks.py)
+    }();
+    int64_t bc = std::max<int64_t>(1, chunk_bytes / std::max<int64_t>(bytes_per_b, 1));
     bc = std::min(bc, batch);
     const int nb = Context::kPipeBufs;
     float* dx[Context::kPipeBufs];
