@@ -161,6 +161,9 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=1.0, help="CPU baseline seconds per L")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extras", action="store_true", help="skip the per-kind side measurements")
+    ap.add_argument("--no-graph", action="store_true",
+                    help="eager launches instead of CUDA-graph replay (for ncu launch lists; ncu cannot replay "
+                         "kernels inside stream capture)")
     args = ap.parse_args()
     world, rank, local = dist_setup()
 
@@ -198,15 +201,28 @@ def main():
     sweep(LS)
     torch.cuda.synchronize()
     launches0 = ctx.launches
-    graph = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(graph):
+    if args.no_graph:
+        class _Eager:  # same interface as a captured graph
+            def __init__(self, Ls):
+                self.Ls = Ls
+
+            def replay(self):
+                sweep(self.Ls)
+
+        graph = _Eager(LS)
         sweep(LS)
-    launches_per_step = ctx.launches - launches0
-    graphs_L = {}
-    for L in LS:
-        graphs_L[L] = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(graphs_L[L]):
-            sweep([L])
+        launches_per_step = ctx.launches - launches0
+        graphs_L = {L: _Eager([L]) for L in LS}
+    else:
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            sweep(LS)
+        launches_per_step = ctx.launches - launches0
+        graphs_L = {}
+        for L in LS:
+            graphs_L[L] = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graphs_L[L]):
+                sweep([L])
     torch.cuda.synchronize()
 
     per_L = {L: 0.0 for L in LS}
