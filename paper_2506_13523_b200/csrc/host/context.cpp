@@ -3,6 +3,7 @@
 #include "context.hpp"
 
 #include <cuda_fp16.h>
+#include <cudaTypedefs.h>
 
 #include <algorithm>
 #include <cmath>
@@ -377,6 +378,30 @@ GridTcEntry Context::build_dense_tc(const DenseOps& ops, const char* label) {
             }
     t.a_slice_bytes = static_cast<uint32_t>(64 * t.zp);
     t.a = reinterpret_cast<const uint8_t*>(upload(a));
+  }
+  if (t.pair) {
+    // 2-D TMA views of the tables, [bytes / 64][64 B], one box = one half slice
+    // (the cta_group::2 tensor copy signals the pair leader's barrier directly)
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
+      void* fn = nullptr;
+      cudaDriverEntryPointQueryResult q{};
+      cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
+      return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }();
+    if (!encode) throw CudaFailure("cuTensorMapEncodeTiled unavailable");
+    auto make = [&](CUtensorMap* m, const void* base, size_t bytes, uint32_t box_rows) {
+      const cuuint64_t dims[2] = {64, bytes / 64};
+      const cuuint64_t strides[1] = {64};
+      const cuuint32_t box[2] = {64, box_rows};
+      const cuuint32_t es[2] = {1, 1};
+      const CUresult r = encode(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides, box, es,
+                                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      if (r != CUDA_SUCCESS) throw CudaFailure("cuTensorMapEncodeTiled failed");
+    };
+    make(&t.tm_s1, t.s1, s1.size() * 2, t.s_stage_bytes / 64);
+    make(&t.tm_s2, t.s2, (t.same_s ? s1.size() : s2.size()) * 2, t.s_stage_bytes / 64);
+    make(&t.tm_a, t.a, a.size() * 2, t.a_stage_bytes / 64);
   }
   ent.fits = true;
   return ent;

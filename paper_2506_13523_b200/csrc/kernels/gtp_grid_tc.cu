@@ -215,9 +215,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (i == B_RAW_FREE) cnt = kWorkers;
       if (i == B_XY_READY || i == B_Z_EMPTY) cnt = kWorkers * kPair;
       if (i >= B_P_READY && i < B_P_READY + kMaxSlices) cnt = BM * kPair;
-      // the leader's ring slots complete with its own bulk copy + the peer's forward
-      if (PAIR && leader && ((i >= B_SFULL && i < B_SFULL + kMaxStages) || (i >= B_AFULL && i < B_AFULL + kMaxStages)))
-        cnt = 2;
       mbar_init(&bars[i], cnt);
     }
     fence_mbar_init();
@@ -261,12 +258,19 @@ __global__ void __launch_bounds__(kThreads, 1)
     {
       int stage = 0;
       uint32_t ph = 0;
-      auto push = [&](const uint8_t* src, uint32_t bytes) {
+      auto push = [&](const uint8_t* src, uint32_t bytes, bool second) {
         mbar_wait(&bars[B_SEMPTY + stage], ph ^ 1);
-        if (pl) mbar_arrive_expect_tx(&bars[B_SFULL + stage], t.s_stage_bytes);
-        if (pl)
-          bulk_g2s(sring + stage * t.s_stage_bytes, src + (PAIR ? rank * t.s_stage_bytes : 0u), t.s_stage_bytes,
-                   &bars[B_SFULL + stage]);
+        if (PAIR) {
+          // both CTAs' halves complete on the leader's slot barrier (tensor TMA, cta_group::2)
+          if (pl && leader) mbar_arrive_expect_tx(&bars[B_SFULL + stage], 2 * t.s_stage_bytes);
+          const CUtensorMap* tm = second ? &t.tm_s2 : &t.tm_s1;
+          const uint8_t* base = second ? t.s2 : t.s1;
+          const int row = static_cast<int>((src - base + rank * t.s_stage_bytes) / 64);
+          if (pl) tma2d_load_pair(sring + stage * t.s_stage_bytes, tm, 0, row, &bars[B_SFULL + stage]);
+        } else {
+          if (pl) mbar_arrive_expect_tx(&bars[B_SFULL + stage], t.s_stage_bytes);
+          if (pl) bulk_g2s(sring + stage * t.s_stage_bytes, src, t.s_stage_bytes, &bars[B_SFULL + stage]);
+        }
         if (++stage == t.s_stages) {
           stage = 0;
           ph ^= 1;
@@ -296,10 +300,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         const bool has_next = next_u < u_end;
         for (int c = 0; c < t.nchunks; ++c) {
           for (int ks = 0; ks < t.k1p / 16; ++ks)
-            push(t.s1 + static_cast<size_t>(c * (t.k1p / 16) + ks) * t.s1_slice_bytes, t.s1_slice_bytes);
+            push(t.s1 + static_cast<size_t>(c * (t.k1p / 16) + ks) * t.s1_slice_bytes, t.s1_slice_bytes, false);
           if (!t.same_s)
             for (int ks = 0; ks < t.k2p / 16; ++ks)
-              push(t.s2 + static_cast<size_t>(c * (t.k2p / 16) + ks) * t.s2_slice_bytes, t.s2_slice_bytes);
+              push(t.s2 + static_cast<size_t>(c * (t.k2p / 16) + ks) * t.s2_slice_bytes, t.s2_slice_bytes, true);
           const bool raw_point = t.raw_inplace ? (last_of_tile && c == t.nchunks - 1) : (first_of_tile && c == 0);
           if (raw_point && has_next) {
             const Unit nu = unit_of(next_u, t.ngroups);
@@ -321,11 +325,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int n = t.nchunks * t.nslices * t.nparts;
         for (int k = 0; k < n; ++k) {
           mbar_wait(&bars[B_AEMPTY + stage], ph ^ 1);
-          if (pl) mbar_arrive_expect_tx(&bars[B_AFULL + stage], t.a_stage_bytes);
-          if (pl)
-            bulk_g2s(aring + stage * t.a_stage_bytes,
-                     t.a + (abase + k) * t.a_slice_bytes + (PAIR ? rank * t.a_stage_bytes : 0u), t.a_stage_bytes,
-                     &bars[B_AFULL + stage]);
+          if (PAIR) {
+            if (pl && leader) mbar_arrive_expect_tx(&bars[B_AFULL + stage], 2 * t.a_stage_bytes);
+            const int row = static_cast<int>(((abase + k) * t.a_slice_bytes + rank * t.a_stage_bytes) / 64);
+            if (pl) tma2d_load_pair(aring + stage * t.a_stage_bytes, &t.tm_a, 0, row, &bars[B_AFULL + stage]);
+          } else {
+            if (pl) mbar_arrive_expect_tx(&bars[B_AFULL + stage], t.a_stage_bytes);
+            if (pl)
+              bulk_g2s(aring + stage * t.a_stage_bytes, t.a + (abase + k) * t.a_slice_bytes, t.a_stage_bytes,
+                       &bars[B_AFULL + stage]);
+          }
           if (++stage == t.a_stages) {
             stage = 0;
             ph ^= 1;
@@ -341,30 +350,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // MMA, which lowers the per-instruction issue cost of the single issuer.
     const bool leader_lane = elect_one_sync();
     if (PAIR && !leader) {
-      // rank 1: forward "my half of this ring slot landed" to the leader's slot,
-      // in the order the leader consumes the rings (chunk: S slices, A slices)
-      int s_stage = 0, a_stage = 0;
-      uint32_t s_ph = 0, a_ph = 0;
-      const int s_per_chunk = t.k1p / 16 + (t.same_s ? 0 : t.k2p / 16);
-      for (int64_t u = u_begin; u < u_end; ++u)
-        for (int c = 0; c < t.nchunks; ++c) {
-          for (int k = 0; k < s_per_chunk; ++k) {
-            mbar_wait(&bars[B_SFULL + s_stage], s_ph);
-            if (leader_lane) arrive_leader<PAIR>(&bars[B_SFULL + s_stage], 1, rank);
-            if (++s_stage == t.s_stages) {
-              s_stage = 0;
-              s_ph ^= 1;
-            }
-          }
-          for (int k = 0; k < t.nslices * t.nparts; ++k) {
-            mbar_wait(&bars[B_AFULL + a_stage], a_ph);
-            if (leader_lane) arrive_leader<PAIR>(&bars[B_AFULL + a_stage], 1, rank);
-            if (++a_stage == t.a_stages) {
-              a_stage = 0;
-              a_ph ^= 1;
-            }
-          }
-        }
+      // rank 1: nothing to issue -- its TMA halves complete on the leader's barriers
     } else {
       int s_stage = 0, a_stage = 0;
       uint32_t s_ph = 0, a_ph = 0;

@@ -3,6 +3,7 @@
 // owned by the tpo_ctx; launchers are asynchronous on the given stream.
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -64,6 +65,10 @@ struct GridTcTables {
   const uint8_t* s2;
   const uint8_t* a;
   uint32_t s1_slice_bytes, s2_slice_bytes, a_slice_bytes;
+  // pair mode: 2-D TMA views [bytes / 64][64 B] of the tables, box = one half slice
+  alignas(64) CUtensorMap tm_s1;
+  alignas(64) CUtensorMap tm_s2;
+  alignas(64) CUtensorMap tm_a;
 };
 cudaError_t launch_gtp_grid_tc(const GridTcTables& t, const RowSpec& rs, int num_sms, cudaStream_t s);
 int gtp_grid_tc_max_smem();

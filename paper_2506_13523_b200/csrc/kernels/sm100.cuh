@@ -171,6 +171,19 @@ __device__ __forceinline__ void tmem_relinquish_pair() {
 __device__ __forceinline__ void tmem_dealloc_pair(uint32_t taddr, uint32_t ncols) {
   asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols) : "memory");
 }
+// 2-D tensor TMA into this CTA's shared memory whose completion (tx bytes) is
+// signalled on the PAIR LEADER's mbarrier: `bar_local` is this CTA's copy of the
+// barrier, the rank bit (bit 24 of the shared::cluster window) is cleared so the
+// bytes land on rank 0's barrier (as CUTLASS SM100_TMA_2SM_LOAD does)
+__device__ __forceinline__ void tma2d_load_pair(void* dst, const void* tmap, int c0, int c1, uint64_t* bar_local) {
+  const uint32_t mbar = smem_u32(bar_local) & 0xFEFFFFFFu;
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+      "[%4];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(c0), "r"(c1), "r"(mbar)
+      : "memory");
+}
+
 // completion of this thread's prior tcgen05 ops arrives on `bar` (same offset)
 // in both CTAs of the pair
 __device__ __forceinline__ void tc_commit_pair(uint64_t* bar) {
