@@ -84,6 +84,27 @@ int min_lt(int L1, int L2, int L3) { return (std::max({L1, L2, L3}) + 1) / 2; }
 
 void run_cgtp(tpo_ctx* ctx, int L1, int L2, const RowSpec& rs, cudaStream_t s) {
   const auto& t = ctx->impl.cgtp(L1, L2);
+  // shared y per edge (config C4): per-edge dense GEMMs on tcgen05 when the shape allows
+  const int kp = (t.din1 + 15) / 16 * 16, dout_pad = (t.dout + 15) / 16 * 16;
+  const bool aligned = (reinterpret_cast<uintptr_t>(rs.x) % 16 == 0) && (reinterpret_cast<uintptr_t>(rs.out) % 16 == 0);
+  static const bool edge_tc_on = [] {
+    const char* v = std::getenv("TPO_CGTP_EDGE_TC");
+    return !(v && *v == '0');
+  }();
+  if (edge_tc_on && rs.y_shared && rs.channels % 128 == 0 && t.din1 % 4 == 0 && kp <= 64 && t.din2 <= 64 &&
+      dout_pad <= 256 && t.dout % 4 == 0 && aligned &&
+      tpo_b200::cgtp_edge_tc_smem(t, kp, dout_pad) <= 227 * 1024) {
+    tpo_b200::EdgeTcParams p{};
+    p.kp = kp;
+    p.dout_pad = dout_pad;
+    p.tmem_cols = 32;  // two Z buffers of dout_pad rounded to the 32-column store box
+    while (p.tmem_cols < 2 * ((dout_pad + 31) / 32 * 32)) p.tmem_cols *= 2;
+    tpo_b200::encode_tmap_2d(&p.tm_out, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, rs.out, static_cast<uint64_t>(t.dout),
+                             static_cast<uint64_t>(rs.rows), static_cast<uint64_t>(t.dout) * 4, 32, 128,
+                             CU_TENSOR_MAP_SWIZZLE_128B);
+    launched(ctx, tpo_b200::launch_cgtp_edge_tc(t, p, rs, ctx->impl.num_sms(), s), "cgtp edge tcgen05 kernel");
+    return;
+  }
   launched(ctx, tpo_b200::launch_cgtp(t, rs, ctx->impl.num_sms(), s), "cgtp kernel");
 }
 

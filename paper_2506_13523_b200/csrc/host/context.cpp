@@ -21,6 +21,24 @@ void cuda_check(cudaError_t e, const char* what) {
   if (e != cudaSuccess) throw CudaFailure(std::string(what) + ": " + cudaGetErrorString(e));
 }
 
+void encode_tmap_2d(CUtensorMap* m, CUtensorMapDataType dt, const void* base, uint64_t inner, uint64_t outer,
+                    uint64_t row_stride_bytes, uint32_t box_inner, uint32_t box_outer, CUtensorMapSwizzle sw) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }();
+  if (!encode) throw CudaFailure("cuTensorMapEncodeTiled unavailable");
+  const cuuint64_t dims[2] = {inner, outer};
+  const cuuint64_t strides[1] = {row_stride_bytes};
+  const cuuint32_t box[2] = {box_inner, box_outer};
+  const cuuint32_t es[2] = {1, 1};
+  const CUresult r = encode(m, dt, 2, const_cast<void*>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                            sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw CudaFailure("cuTensorMapEncodeTiled failed (" + std::to_string(r) + ")");
+}
+
 namespace {
 inline int pad_to(int v, int m) { return (v + m - 1) / m * m; }
 inline int flat(int l, int m) { return l * l + m + l; }
@@ -382,22 +400,9 @@ GridTcEntry Context::build_dense_tc(const DenseOps& ops, const char* label) {
   if (t.pair) {
     // 2-D TMA views of the tables, [bytes / 64][64 B], one box = one half slice
     // (the cta_group::2 tensor copy signals the pair leader's barrier directly)
-    static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
-      void* fn = nullptr;
-      cudaDriverEntryPointQueryResult q{};
-      cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
-      return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
-    }();
-    if (!encode) throw CudaFailure("cuTensorMapEncodeTiled unavailable");
     auto make = [&](CUtensorMap* m, const void* base, size_t bytes, uint32_t box_rows) {
-      const cuuint64_t dims[2] = {64, bytes / 64};
-      const cuuint64_t strides[1] = {64};
-      const cuuint32_t box[2] = {64, box_rows};
-      const cuuint32_t es[2] = {1, 1};
-      const CUresult r = encode(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides, box, es,
-                                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-      if (r != CUDA_SUCCESS) throw CudaFailure("cuTensorMapEncodeTiled failed");
+      encode_tmap_2d(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, base, 64, bytes / 64, 64, 64, box_rows,
+                     CU_TENSOR_MAP_SWIZZLE_NONE);
     };
     make(&t.tm_s1, t.s1, s1.size() * 2, t.s_stage_bytes / 64);
     make(&t.tm_s2, t.s2, (t.same_s ? s1.size() : s2.size()) * 2, t.s_stage_bytes / 64);

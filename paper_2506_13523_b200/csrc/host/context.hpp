@@ -30,6 +30,10 @@ struct CudaFailure : std::runtime_error {
 
 void cuda_check(cudaError_t e, const char* what);
 
+// 2-D TMA tensor map (driver cuTensorMapEncodeTiled through the runtime's entry point)
+void encode_tmap_2d(CUtensorMap* m, CUtensorMapDataType dt, const void* base, uint64_t inner, uint64_t outer,
+                    uint64_t row_stride_bytes, uint32_t box_inner, uint32_t box_outer, CUtensorMapSwizzle sw);
+
 struct GridTcEntry {
   bool fits = false;
   GridTcTables t{};

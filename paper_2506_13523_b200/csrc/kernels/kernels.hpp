@@ -35,6 +35,19 @@ struct CgtpTables {
 };
 cudaError_t launch_cgtp(const CgtpTables& t, const RowSpec& rs, int num_sms, cudaStream_t s);
 
+// Shared-y CGTP (one y per edge, channels a multiple of 128) as per-edge dense
+// GEMMs on tcgen05: out[c] = x[c] . M_y (cgtp_edge_tc.cu).  tm_out: 2-D TMA
+// view of out [rows][dout] fp32, box 32 x 128, 128B swizzle (built per call).
+struct EdgeTcParams {
+  int kp;        // Din1 padded to 16 (<= 64)
+  int dout_pad;  // Dout padded to 16 (<= 256: two TMEM accumulators)
+  int tmem_cols;
+  alignas(64) CUtensorMap tm_out;
+};
+int cgtp_edge_tc_smem(const CgtpTables& t, int kp, int dout_pad);
+cudaError_t launch_cgtp_edge_tc(const CgtpTables& t, const EdgeTcParams& p, const RowSpec& rs, int num_sms,
+                                cudaStream_t s);
+
 // ---------------------------------------------------------------- GTP grid, tcgen05
 // Dense operators of the reference's product grid, pre-split into fp16 hi/lo
 // and pre-tiled on the host in the UMMA canonical K-major layout, one

@@ -101,6 +101,17 @@ def test_cgtp(tpo, orc, L):
     _check_batch(tpo, orc, "cgtp", L, 257, 300 + L)
 
 
+@pytest.mark.parametrize("L,C,B", [(3, 128, 7), (3, 256, 3), (1, 128, 5)])
+def test_cgtp_edge_tensor_cores(tpo, orc, L, C, B):
+    # shared y, channels a multiple of 128: per-edge dense GEMM x . M_y on tcgen05
+    x, y = _inputs(B, L, L, 340 + C + L, C=C, shared=True)
+    x[0, 3] *= 1e-3  # rows of different magnitude (per-row power-of-two scaling)
+    x[1, 5] *= 1e3
+    out = _gpu(tpo, "cgtp", x, y, L, L, 0)
+    ref = orc.batch_mimo("cgtp", L, x.astype(np.float64), y.astype(np.float64), channels=C, y_shared=True)
+    assert _normwise(out, ref) <= TOL
+
+
 @pytest.mark.parametrize("C", [32, 96])
 def test_cgtp_edge_tiles(tpo, orc, C):
     # shared-y fast path (channels a multiple of the 32-row tile), ragged batch tail
