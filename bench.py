@@ -332,7 +332,7 @@ def main():
 
     extras = None
     if not args.no_extras and rank == 0:
-        extras = side_measurements(tpo, dev, stream, flush)
+        extras = side_measurements(tpo, dev, stream, flush, load_peaks())
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -363,12 +363,14 @@ def main():
         dist.destroy_process_group()
 
 
-def side_measurements(tpo, dev, stream, flush):
-    """Throughput of the other three TPO kinds on BASELINE configs (device time)."""
+def side_measurements(tpo, dev, stream, flush, peaks):
+    """Throughput and roofline fraction of the other kinds at their BASELINE configs (device time,
+    one launch, L2 flushed).  Bounds: dense GEMM flops on the 3xFP16 tensor peak
+    for the tcgen05 kinds, HBM bytes for CGTP, max(HBM, FP32 SIMT) for the SIMT MTP."""
     import torch
 
-    def timeit(fn, reps=5):
-        for _ in range(2):
+    def timeit(fn, reps=10):
+        for _ in range(3):
             fn()
         tot = 0.0
         for _ in range(reps):
@@ -378,15 +380,37 @@ def side_measurements(tpo, dev, stream, flush):
             tot += a.elapsed_time(b)
         return tot / reps
 
+    tc_peak = peaks["bf16_tflops"] / 3.0 * 1e12
+    hbm = peaks["hbm_gbs"] * 1e9
+    fp32 = 2 * 148 * 128 * 1.965e9  # FFMA peak (nominal clock; not in MEASURED_PEAKS.json)
     res = {}
     g = torch.Generator(device=dev); g.manual_seed(7)
-    for kind, L, B in (("gtp_fourier", 6, 65536), ("mtp", 6, 65536), ("gtp_grid", 6, 65536)):
-        x = torch.randn((B, (L + 1) ** 2), generator=g, device=dev)
-        y = torch.randn((B, (L + 1) ** 2), generator=g, device=dev)
-        o = torch.empty((B, (2 * L + 1) ** 2), device=dev)
+    L, B = 6, 65536
+    din, dout = (L + 1) ** 2, (2 * L + 1) ** 2
+    byts = 4 * (2 * din + dout) * B
+    x = torch.randn((B, din), generator=g, device=dev)
+    y = torch.randn((B, din), generator=g, device=dev)
+    o = torch.empty((B, dout), device=dev)
+    for kind in ("gtp_grid", "gtp_fourier", "mtp"):
         ms = timeit(lambda: tpo.run(kind, x, y, L, L, 2 * L, out=o))
-        res[f"{kind}_L{L}_B{B}"] = {"ms": round(ms, 4), "tp_per_s": round(B / ms * 1e3, 1)}
-    # channel-wise CGTP, config C4 shape (L=3, 128 channels, y shared) on a 2^14-edge chunk
+        t = ms / 1e3
+        if kind == "gtp_grid":
+            G = (2 * L + 1) * (4 * L + 1)
+            fl = 2 * G * (2 * din + dout) * B
+            roof = max(byts / hbm, fl / tc_peak)
+            bound = "tensor (dense S2-grid operators, 3xFP16)"
+        elif kind == "gtp_fourier":
+            N = 4 * L + 1
+            fl = 2 * N * N * (2 * din + dout) * B
+            roof = max(byts / hbm, fl / tc_peak)
+            bound = "tensor (dense torus-grid operators, 3xFP16)"
+        else:
+            fl = 2 * 6378 * B  # 2 x reference sparse muls
+            roof = max(byts / hbm, fl / fp32)
+            bound = "max(HBM, FP32 SIMT at nominal clock)"
+        res[f"{kind}_L{L}_B{B}"] = {"ms": round(ms, 4), "tp_per_s": round(B / t, 1), "tflops": round(fl / t / 1e12, 2),
+                                     "gbs": round(byts / t / 1e9, 1), "roofline_frac": round(roof / t, 4), "bound": bound}
+    # channel-wise CGTP, config C4 shape (L=3, 128 channels, y shared per edge) on a 2^14-edge chunk
     L, C, B = 3, 128, 1 << 14
     x = torch.randn((B, C, 16), generator=g, device=dev)
     y = torch.randn((B, 16), generator=g, device=dev)
@@ -395,7 +419,8 @@ def side_measurements(tpo, dev, stream, flush):
     byts = B * (C * 16 * 4 + 16 * 4 + C * 256 * 4)
     res[f"cgtp_L3_C128_B{B}"] = {"ms": round(ms, 4), "edges_per_s": round(B / ms * 1e3, 1),
                                   "channel_tp_per_s": round(B * C / ms * 1e3, 1),
-                                  "gbs": round(byts / ms / 1e6, 1)}
+                                  "gbs": round(byts / ms / 1e6, 1), "roofline_frac": round(byts / hbm / (ms / 1e3), 4),
+                                  "bound": "HBM (139,328 B per edge)"}
     return res
 
 
