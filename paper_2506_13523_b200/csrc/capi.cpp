@@ -167,9 +167,13 @@ void run_kind(tpo_ctx* ctx, int kind, int L1, int L2, int L3, int lt, const floa
         if (lt > kMaxL) throw InvalidArgument("mtp: l_tilde above the supported maximum");
         l = lt;
       }
-      if (rs.rows > 0)
-        launched(ctx, tpo_b200::launch_mtp(ctx->impl.mtp(L1, L2, L3, l), rs, ctx->impl.num_sms(), s),
-                 "mtp kernel");
+      if (rs.rows > 0) {
+        if (const tpo_b200::MtpTcTables* tc = ctx->impl.mtp_tc(L1, L2, L3, l))
+          launched(ctx, tpo_b200::launch_mtp_tc(*tc, rs, ctx->impl.num_sms(), s), "mtp tcgen05 kernel");
+        else
+          launched(ctx, tpo_b200::launch_mtp(ctx->impl.mtp(L1, L2, L3, l), rs, ctx->impl.num_sms(), s),
+                   "mtp kernel");
+      }
       return;
     }
     default:

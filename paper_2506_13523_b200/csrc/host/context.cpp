@@ -653,6 +653,99 @@ const MtpDevTables& Context::mtp(int L1, int L2, int L3, int lt) {
   return mtp_.emplace(std::array<int, 4>{L1, L2, L3, lt}, t).first->second;
 }
 
+// ------------------------------------------------------------------ MTP, tcgen05
+// Dense embed / extract operators in the TMEM orders of mtp_tc.cu
+// (kernels.hpp, MtpTcTables), same CG tables as Context::mtp
+// (proj/src/mtp.cpp:20-97).
+const MtpTcTables* Context::mtp_tc(int L1, int L2, int L3, int lt) {
+  std::lock_guard<std::mutex> g(mu_);
+  auto it = mtp_tc_.find({L1, L2, L3, lt});
+  if (it != mtp_tc_.end()) return it->second.first ? &it->second.second : nullptr;
+  auto fail = [&]() -> const MtpTcTables* {
+    mtp_tc_.emplace(std::array<int, 4>{L1, L2, L3, lt}, std::make_pair(false, MtpTcTables{}));
+    return nullptr;
+  };
+  const char* env = std::getenv("TPO_MTP_TC");
+  const int dt = 2 * lt + 1;
+  if ((env && env[0] == '0') || dt > 13) return fail();
+  MtpTcTables t{};
+  t.dt = dt;
+  t.din1 = (L1 + 1) * (L1 + 1);
+  t.din2 = (L2 + 1) * (L2 + 1);
+  const int L3e = std::min(L3, 2 * lt);
+  t.dout_eff = (L3e + 1) * (L3e + 1);
+  t.dout_total = (L3 + 1) * (L3 + 1);
+  t.n1 = pad_to(dt * dt, 16);
+  t.n2 = pad_to(t.dout_eff, 16);
+  t.k1 = pad_to(t.din1, 16);
+  t.k2 = pad_to(t.din2, 16);
+  if (t.k1 > 64 || t.k2 > 64) return fail();
+  const int j1 = (dt + 1) / 2, j2 = dt - j1;
+  const int p0 = pad_to(dt * j1, 16), p1 = pad_to(dt * j2, 16);
+  t.kz = p0 + p1;
+  t.zgrp_col[0] = 2 * t.n1;
+  if (2 * t.n1 + p0 > 512) return fail();
+  if (2 * t.n1 + p0 + p1 <= 512) t.zgrp_col[1] = 2 * t.n1 + p0;
+  else if (p1 <= dt * j1) t.zgrp_col[1] = t.n1;  // Y block 0, dead once pass 0 is done
+  else return fail();
+  // dense operators (double), rows in TMEM order
+  std::vector<double> e1(static_cast<size_t>(t.n1) * t.k1, 0.0), e2(static_cast<size_t>(t.n1) * t.k2, 0.0);
+  auto xpos = [&](int i, int k) { return k * dt + i; };
+  auto ypos = [&](int k, int j) { return j < j1 ? k * j1 + j : dt * j1 + k * j2 + (j - j1); };
+  auto zpos = [&](int i, int j) { return j < j1 ? i * j1 + j : p0 + i * j2 + (j - j1); };
+  for (int l = 0; l <= std::max(L1, L2); ++l)  // proj/src/mtp.cpp:20-39
+    for (const CGEntry& e : real_cg(lt, lt, l)) {
+      const int a = e.m1 + lt, b = e.m2 + lt, in = flat(l, e.m3);
+      if (l <= L1) e1[static_cast<size_t>(xpos(a, b)) * t.k1 + in] += e.v;
+      if (l <= L2) e2[static_cast<size_t>(ypos(a, b)) * t.k2 + in] += e.v;
+    }
+  std::vector<double> ex(static_cast<size_t>(t.n2) * t.kz, 0.0);
+  for (int l3 = 0; l3 <= L3e; ++l3)  // proj/src/mtp.cpp:60-97
+    for (const CGEntry& e : real_cg(lt, lt, l3))
+      ex[static_cast<size_t>(flat(l3, e.m3)) * t.kz + zpos(e.m1 + lt, e.m2 + lt)] += e.v;
+  // per K-step [hi | lo][rows x 16] canonical
+  auto tile = [&](const std::vector<double>& m, int rows, int kdim) {
+    const int nks = kdim / 16;
+    std::vector<uint16_t> buf(static_cast<size_t>(nks) * 2 * rows * 16, 0);
+    for (int ks = 0; ks < nks; ++ks) {
+      uint16_t* hi = buf.data() + static_cast<size_t>(ks) * 2 * rows * 16;
+      uint16_t* lo = hi + rows * 16;
+      for (int r = 0; r < rows; ++r)
+        for (int kk = 0; kk < 16; ++kk) {
+          uint16_t hv, lv;
+          split_half(m[static_cast<size_t>(r) * kdim + ks * 16 + kk], hv, lv);
+          const uint32_t o = sm100::canon_off(r, kk, rows) / 2;
+          hi[o] = hv;
+          lo[o] = lv;
+        }
+    }
+    return buf;
+  };
+  t.e1 = reinterpret_cast<const uint8_t*>(upload(tile(e1, t.n1, t.k1)));
+  t.e2 = reinterpret_cast<const uint8_t*>(upload(tile(e2, t.n1, t.k2)));
+  t.ext = reinterpret_cast<const uint8_t*>(upload(tile(ex, t.n2, t.kz)));
+  // shared memory: ring | X op | Y op | x staging | y staging | epilogue staging
+  t.stage_bytes = 64 * t.n1;
+  // raw input staging doubles as output half buffer 1; output half buffer 0 doubles as the
+  // per-warp staging of the direct-store epilogue
+  const int raw_bytes = std::max(128 * (t.din1 + t.din2) * 4, 64 * t.dout_total * 4);
+  const int out_bytes = std::max(64 * t.dout_total * 4, 8 * 32 * 17 * 4);
+  const int fixed = 128 * t.k1 * 4 + 128 * t.k2 * 4 + raw_bytes + out_bytes;
+  const int budget = 220 * 1024;
+  t.stages = std::min(8, (budget - fixed) / t.stage_bytes);
+  if (t.stages < 2) return fail();
+  t.off_xop = t.stages * t.stage_bytes;
+  t.off_yop = t.off_xop + 128 * t.k1 * 4;
+  t.off_stx = t.off_yop + 128 * t.k2 * 4;
+  t.off_sty = t.off_stx + 128 * t.din1 * 4;
+  t.off_out = t.off_stx + pad_to(raw_bytes, 128);
+  t.smem_bytes = t.off_out + out_bytes + 1024;
+  if (std::getenv("TPO_VERBOSE"))
+    std::fprintf(stderr, "[tpo] mtp tcgen05 dt=%d n1=%d n2=%d k=(%d,%d) kz=%d zcols=(%d,%d) stages=%d smem=%d\n", dt,
+                 t.n1, t.n2, t.k1, t.k2, t.kz, t.zgrp_col[0], t.zgrp_col[1], t.stages, t.smem_bytes);
+  return &mtp_tc_.emplace(std::array<int, 4>{L1, L2, L3, lt}, std::make_pair(true, t)).first->second.second;
+}
+
 const float* Context::degree_weights(const std::vector<double>& w) {
   std::lock_guard<std::mutex> g(mu_);
   auto it = weights_.find(w);

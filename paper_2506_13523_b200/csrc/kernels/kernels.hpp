@@ -135,6 +135,27 @@ struct MtpDevTables {
 };
 cudaError_t launch_mtp(const MtpDevTables& t, const RowSpec& rs, int num_sms, cudaStream_t s);
 
+// MTP on tcgen05 (mtp_tc.cu), carrier dt = 2 lt + 1 <= 13.  Embed and extract
+// are dense 3xFP16 GEMMs whose B operands are streamed per K-step through a
+// TMA ring; the dt x dt per-product matmul runs on SIMT straight from TMEM.
+// TMEM columns (512 per CTA): X^T at [0, n1) (X[i][k] at k*dt + i), Y at
+// [n1, 2 n1) in two column blocks (j < j1: k*j1 + j; j >= j1: dt*j1 + k*(dt-j1)
+// + j - j1), Z pass p (cells (i, j in block p), i*nj + j) at zgrp_col[p] as
+// fp16 hi/lo K-steps, GEMM-2 output at [0, n2).
+//   e1[ks] / e2[ks]: [hi | lo] x [n1 rows (X / Y position)][16 (input idx 16ks..)] canonical
+//   ext[ks]        : [hi | lo] x [n2 rows (output)][16 (Z position 16ks..)] canonical
+struct MtpTcTables {
+  int dt, n1, n2, k1, k2, kz;  // padded GEMM dims
+  int din1, din2, dout_eff, dout_total;
+  int zgrp_col[2];             // TMEM column of Z pass 0 / 1
+  int stages, stage_bytes, smem_bytes;
+  int off_xop, off_yop, off_stx, off_sty, off_out;  // dynamic shared memory layout
+  const uint8_t* e1;
+  const uint8_t* e2;
+  const uint8_t* ext;
+};
+cudaError_t launch_mtp_tc(const MtpTcTables& t, const RowSpec& rs, int num_sms, cudaStream_t s);
+
 // ---------------------------------------------------------------- weighted epilogue helpers
 // x[r][(l,m)] *= w[l] (per-degree scaling, proj/src/gtp.cpp:34-44)
 cudaError_t launch_scale_degrees(const float* in, float* out, int64_t rows, int L, const float* w,

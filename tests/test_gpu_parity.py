@@ -156,6 +156,45 @@ def test_mtp(tpo, orc, L):
     _check_batch(tpo, orc, "mtp", L, 129 if L <= 8 else 16, 500 + L)
 
 
+@pytest.mark.parametrize("L", [0, 1, 2, 3, 4, 5, 6])
+def test_mtp_tensor_cores_many_tiles(tpo, orc, L):
+    # tcgen05 path (carrier dt <= 13): several 128-row tiles per CTA, ragged tail
+    B = 148 * 128 * 2 + 77 if L >= 5 else 5000
+    x, y = _inputs(B, L, L, 560 + L)
+    out = _gpu(tpo, "mtp", x, y, L, L, 2 * L)
+    ref = orc.batch_mimo("mtp", L, x.astype(np.float64)[:, None], y.astype(np.float64)[:, None])[:, 0]
+    assert _normwise(out, ref) <= TOL
+
+
+def test_mtp_simt_path():
+    # SIMT kernel (used past the tcgen05 carrier limit) forced in a fresh process
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parents[1]
+    code = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, %r); sys.path.insert(0, %r)
+import oracle, paper_2506_13523_b200 as tpo
+worst = 0.0
+for L, B in ((1, 300), (3, 300), (6, 300)):
+    rng = np.random.default_rng(950 + L)
+    d = (L + 1) ** 2
+    x = rng.standard_normal((B, d)).astype(np.float32); y = rng.standard_normal((B, d)).astype(np.float32)
+    out = tpo.run("mtp", torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda(), L, L, 2 * L).cpu().numpy()
+    ref = oracle.batch_mimo("mtp", L, x.astype(np.float64)[:, None], y.astype(np.float64)[:, None])[:, 0]
+    err = (np.abs(out - ref).max(axis=1) / np.maximum(np.abs(ref).max(axis=1), 1e-300)).max()
+    worst = max(worst, float(err))
+print(worst)
+""" % (str(root), str(root / "oracle"))
+    env = dict(os.environ, TPO_MTP_TC="0")
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=240, env=env)
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert float(r.stdout.strip().splitlines()[-1]) <= TOL
+
+
 # ---------------------------------------------------------------- shapes / edge cases
 def test_ragged_batch_and_empty(tpo, orc):
     for kind in ("gtp_grid", "cgtp", "gtp_fourier", "mtp"):
