@@ -680,19 +680,29 @@ const MtpTcTables* Context::mtp_tc(int L1, int L2, int L3, int lt) {
   t.k1 = pad_to(t.din1, 16);
   t.k2 = pad_to(t.din2, 16);
   if (t.k1 > 64 || t.k2 > 64) return fail();
-  const int j1 = (dt + 1) / 2, j2 = dt - j1;
-  const int p0 = pad_to(dt * j1, 16), p1 = pad_to(dt * j2, 16);
-  t.kz = p0 + p1;
+  // per-row matmul split by carrier rows between the two warps of a TMEM lane quarter:
+  // Z group 0 = rows i < i1, group 1 (+ tail group 2) = rows i >= i1, cells (i - i0) * dt + j
+  const int i1 = (dt + 1) / 2;
+  const int size0 = pad_to(i1 * dt, 16), size1 = pad_to((dt - i1) * dt, 16);
+  t.kz = size0 + size1;
   t.zgrp_col[0] = 2 * t.n1;
-  if (2 * t.n1 + p0 > 512) return fail();
-  if (2 * t.n1 + p0 + p1 <= 512) t.zgrp_col[1] = 2 * t.n1 + p0;
-  else if (p1 <= dt * j1) t.zgrp_col[1] = t.n1;  // Y block 0, dead once pass 0 is done
-  else return fail();
+  t.zgrp_size[0] = size0;
+  if (t.zgrp_col[0] + size0 > 512) return fail();
+  const int room = (512 - (t.zgrp_col[0] + size0)) / 16 * 16;
+  t.zgrp_col[1] = t.zgrp_col[0] + size0;
+  t.zgrp_size[1] = std::min(size1, room);
+  // the tail goes to the Y columns once both halves finished reading them
+  t.zgrp_col[2] = t.n1;
+  t.zgrp_size[2] = size1 - t.zgrp_size[1];
+  t.zgrp_col[3] = 0;
+  t.zgrp_size[3] = 0;
+  t.y0_reuse = t.zgrp_size[2] > 0;
+  if (t.zgrp_size[2] > t.n1) return fail();
   // dense operators (double), rows in TMEM order
   std::vector<double> e1(static_cast<size_t>(t.n1) * t.k1, 0.0), e2(static_cast<size_t>(t.n1) * t.k2, 0.0);
   auto xpos = [&](int i, int k) { return k * dt + i; };
-  auto ypos = [&](int k, int j) { return j < j1 ? k * j1 + j : dt * j1 + k * j2 + (j - j1); };
-  auto zpos = [&](int i, int j) { return j < j1 ? i * j1 + j : p0 + i * j2 + (j - j1); };
+  auto ypos = [&](int k, int j) { return k * dt + j; };
+  auto zpos = [&](int i, int j) { return i < i1 ? i * dt + j : size0 + (i - i1) * dt + j; };
   for (int l = 0; l <= std::max(L1, L2); ++l)  // proj/src/mtp.cpp:20-39
     for (const CGEntry& e : real_cg(lt, lt, l)) {
       const int a = e.m1 + lt, b = e.m2 + lt, in = flat(l, e.m3);
@@ -741,8 +751,9 @@ const MtpTcTables* Context::mtp_tc(int L1, int L2, int L3, int lt) {
   t.off_out = t.off_stx + pad_to(raw_bytes, 128);
   t.smem_bytes = t.off_out + out_bytes + 1024;
   if (std::getenv("TPO_VERBOSE"))
-    std::fprintf(stderr, "[tpo] mtp tcgen05 dt=%d n1=%d n2=%d k=(%d,%d) kz=%d zcols=(%d,%d) stages=%d smem=%d\n", dt,
-                 t.n1, t.n2, t.k1, t.k2, t.kz, t.zgrp_col[0], t.zgrp_col[1], t.stages, t.smem_bytes);
+    std::fprintf(stderr, "[tpo] mtp tcgen05 dt=%d n1=%d n2=%d k=(%d,%d) kz=%d zcols=(%d,%d,%d,%d) y0=%d stages=%d smem=%d\n",
+                 dt, t.n1, t.n2, t.k1, t.k2, t.kz, t.zgrp_col[0], t.zgrp_col[1], t.zgrp_col[2], t.zgrp_col[3],
+                 t.y0_reuse, t.stages, t.smem_bytes);
   return &mtp_tc_.emplace(std::array<int, 4>{L1, L2, L3, lt}, std::make_pair(true, t)).first->second.second;
 }
 

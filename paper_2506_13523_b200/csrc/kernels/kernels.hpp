@@ -139,15 +139,16 @@ cudaError_t launch_mtp(const MtpDevTables& t, const RowSpec& rs, int num_sms, cu
 // are dense 3xFP16 GEMMs whose B operands are streamed per K-step through a
 // TMA ring; the dt x dt per-product matmul runs on SIMT straight from TMEM.
 // TMEM columns (512 per CTA): X^T at [0, n1) (X[i][k] at k*dt + i), Y at
-// [n1, 2 n1) in two column blocks (j < j1: k*j1 + j; j >= j1: dt*j1 + k*(dt-j1)
-// + j - j1), Z pass p (cells (i, j in block p), i*nj + j) at zgrp_col[p] as
-// fp16 hi/lo K-steps, GEMM-2 output at [0, n2).
+// [n1, 2 n1) (Y[k][j] at k*dt + j), Z of carrier rows i < i1 = (dt+1)/2 (group 0)
+// and i >= i1 (group 1, its tail in group 2 = the Y columns once read) as fp16
+// hi/lo K-steps, cells (i - i0) * dt + j, K order g = 0..3; GEMM-2 output at [0, n2).
 //   e1[ks] / e2[ks]: [hi | lo] x [n1 rows (X / Y position)][16 (input idx 16ks..)] canonical
 //   ext[ks]        : [hi | lo] x [n2 rows (output)][16 (Z position 16ks..)] canonical
 struct MtpTcTables {
   int dt, n1, n2, k1, k2, kz;  // padded GEMM dims
   int din1, din2, dout_eff, dout_total;
-  int zgrp_col[2];             // TMEM column of Z pass 0 / 1
+  int zgrp_col[4], zgrp_size[4];  // Z groups in K order: TMEM column, K extent
+  int y0_reuse;                   // group 2 lives in the Y columns (row halves sync before writing it)
   int stages, stage_bytes, smem_bytes;
   int off_xop, off_yop, off_stx, off_sty, off_out;  // dynamic shared memory layout
   const uint8_t* e1;

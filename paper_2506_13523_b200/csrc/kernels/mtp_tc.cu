@@ -53,54 +53,15 @@ __device__ __forceinline__ uint32_t pack_half2(float a, float b) {
   const __half2 h = __floats2half2_rn(a, b);
   return *reinterpret_cast<const uint32_t*>(&h);
 }
-__device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&r)[8]) {
-  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
-               : "r"(taddr));
-}
-__device__ __forceinline__ void tmem_ld4(uint32_t taddr, uint32_t* r) {
-  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
-               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
-               : "r"(taddr));
-}
-__device__ __forceinline__ void tmem_ld2(uint32_t taddr, uint32_t* r) {
-  asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0,%1}, [%2];" : "=r"(r[0]), "=r"(r[1]) : "r"(taddr));
-}
-__device__ __forceinline__ void tmem_ld1(uint32_t taddr, uint32_t* r) {
-  asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(r[0]) : "r"(taddr));
-}
 __device__ __forceinline__ void tmem_ld8p(uint32_t taddr, uint32_t* r) {
   asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
                : "r"(taddr));
 }
-// columns [c, c + n) of this lane into d[0, n) as naturally aligned x8 / x4 / x2 / x1 pieces
-// (c and n are compile-time constants once the caller's loops are unrolled)
-__device__ __forceinline__ void tmem_load_run(uint32_t lb, int c, int n, uint32_t* d) {
-#pragma unroll
-  for (int piece = 0; piece < 8; ++piece) {
-    if (n > 0) {
-      if ((c & 7) == 0 && n >= 8) {
-        tmem_ld8p(lb + c, d);
-        d += 8; c += 8; n -= 8;
-      } else if ((c & 3) == 0 && n >= 4) {
-        tmem_ld4(lb + c, d);
-        d += 4; c += 4; n -= 4;
-      } else if ((c & 1) == 0 && n >= 2) {
-        tmem_ld2(lb + c, d);
-        d += 2; c += 2; n -= 2;
-      } else {
-        tmem_ld1(lb + c, d);
-        d += 1; c += 1; n -= 1;
-      }
-    }
-  }
-}
 // wait for this thread's outstanding TMEM loads; the loaded registers pass through the
 // asm so no use of them can be scheduled above the wait
-constexpr bool kWideLd = true;
-constexpr int kRun = 24;  // X column (x16, dt <= 13) + Y row block (x8, <= 7)
-__device__ __forceinline__ void tmem_wait_ld_bind(uint32_t (&a)[kRun]) {
+
+__device__ __forceinline__ void tmem_wait_ld_bind24(uint32_t (&a)[24]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;"
                : "+r"(a[0]), "+r"(a[1]), "+r"(a[2]), "+r"(a[3]), "+r"(a[4]), "+r"(a[5]), "+r"(a[6]), "+r"(a[7]),
                  "+r"(a[8]), "+r"(a[9]), "+r"(a[10]), "+r"(a[11]), "+r"(a[12]), "+r"(a[13]), "+r"(a[14]),
@@ -127,86 +88,92 @@ __device__ __forceinline__ void bulk_wait_read_all() { asm volatile("cp.async.bu
 template <int DT>
 struct Carrier {
   static constexpr int N1 = (DT * DT + 15) / 16 * 16;
-  static constexpr int J1 = (DT + 1) / 2;
+  static constexpr int J1 = (DT + 1) / 2;  // Y column block 0: j < J1
+  static constexpr int IA = (DT + 1) / 2;  // carrier rows of warp half 0: i < IA
 };
 
-// One pass of the per-row matmul: Z[i][j] = sum_k X[i][k] Y[k][j] for all i and the
-// j of column block P, written to TMEM at column zc as fp16 hi / lo K-steps.  Loads of
-// step k + 1 are in flight while step k computes (packed f32x2 FMAs along j).
-template <int DT, int P>
-__device__ __forceinline__ void middle_pass(uint32_t lb, uint32_t zc) {
-  constexpr int N1 = Carrier<DT>::N1, J1 = Carrier<DT>::J1;
-  constexpr int NJ = P ? DT - J1 : J1;
-  if constexpr (NJ > 0) {
-    constexpr int YOFF = N1 + (P ? DT * J1 : 0);
-    constexpr int YR = kWideLd ? 16 : DT;  // Y values start here in the loaded registers
-    constexpr int NP = NJ / 2;        // packed pairs along j
-    constexpr bool ODD = (NJ & 1) != 0;  // plus one scalar column
-    float2 acc[DT][NP > 0 ? NP : 1];
-    float acc1[DT];
+// Row half H of the per-row matmul
+//   Z[i][j] = sum_k X[i][k] Y[k][j],  i in half H (i < IA or i >= IA), all j,
+// accumulated in registers (packed f32x2 FMAs along j).  Each k step is one x8 TMEM
+// load of X column k (rows of this half) and one x16 load of Y row k, both at
+// unaligned column starts (extra columns ignored); loads of step k + 1 fly while
+// step k computes.  Written to TMEM as fp16 hi / lo K-steps (cells (i - i0) * DT + j,
+// padded to 16 with zeros): K-steps b < nb1 at column zc1 + 16 b, the rest at
+// zc2 + 16 (b - nb1) after `sync` (the other half of the quarter finished reading Y).
+template <int DT, int H>
+__device__ __forceinline__ void middle_half(uint32_t lb, uint32_t zc1, int nb1, uint32_t zc2, bool sync2, int barid) {
+  constexpr int N1 = Carrier<DT>::N1, IA = Carrier<DT>::IA;
+  constexpr int I0 = H ? IA : 0, NI = H ? DT - IA : IA;
+  constexpr int NJ = DT, NP = NJ / 2;  // packed pairs along j, plus one scalar column (DT odd)
+  if constexpr (NI > 0) {
+    float2 acc[NI][NP > 0 ? NP : 1];
+    float acc1[NI];
 #pragma unroll
-    for (int i = 0; i < DT; ++i) {
+    for (int i = 0; i < NI; ++i) {
 #pragma unroll
       for (int j = 0; j < NP; ++j) acc[i][j] = make_float2(0.f, 0.f);
       acc1[i] = 0.f;
     }
-    uint32_t cur[kRun], nxt[kRun];
+    uint32_t cur[24], nxt[24];  // [X column k rows (x8) | Y row k (x16)]
 #pragma unroll
-    for (int e = 0; e < kRun; ++e) cur[e] = nxt[e] = 0u;
+    for (int e = 0; e < 24; ++e) cur[e] = nxt[e] = 0u;
     auto issue = [&](int k, uint32_t* d) {
-      if constexpr (kWideLd) {  // one x16 (X column k) + one x8 (Y row k) at unaligned column starts
-        tmem_ld16p(lb + k * DT, d);
-        tmem_ld8p(lb + YOFF + k * NJ, d + 16);
-      } else {
-        tmem_load_run(lb, k * DT, DT, d);
-        tmem_load_run(lb, YOFF + k * NJ, NJ, d + DT);
-      }
+      tmem_ld8p(lb + k * DT + I0, d);
+      tmem_ld16p(lb + N1 + k * DT, d + 8);
     };
-    issue(0, cur);
-    tmem_wait_ld_bind(cur);
-#pragma unroll
-    for (int k = 0; k < DT; ++k) {
-      if (k + 1 < DT) issue(k + 1, nxt);
+    auto step = [&](const uint32_t* v) {
       float2 yp[NP > 0 ? NP : 1];
 #pragma unroll
-      for (int j = 0; j < NP; ++j) yp[j] = make_float2(__uint_as_float(cur[YR + 2 * j]), __uint_as_float(cur[YR + 2 * j + 1]));
-      const float ylast = __uint_as_float(cur[YR + NJ - 1]);
+      for (int j = 0; j < NP; ++j) yp[j] = make_float2(__uint_as_float(v[8 + 2 * j]), __uint_as_float(v[9 + 2 * j]));
+      const float ylast = __uint_as_float(v[8 + NJ - 1]);
 #pragma unroll
-      for (int i = 0; i < DT; ++i) {
-        const float xv = __uint_as_float(cur[i]);
+      for (int i = 0; i < NI; ++i) {
+        const float xv = __uint_as_float(v[i]);
         const float2 x2 = make_float2(xv, xv);
 #pragma unroll
         for (int j = 0; j < NP; ++j) acc[i][j] = __ffma2_rn(x2, yp[j], acc[i][j]);
-        if (ODD) acc1[i] = fmaf(xv, ylast, acc1[i]);
+        acc1[i] = fmaf(xv, ylast, acc1[i]);
       }
+    };
+    // runtime k loop (small code: a fully unrolled form missed in the instruction cache)
+    issue(0, cur);
+    tmem_wait_ld_bind24(cur);
+#pragma unroll 1
+    for (int k = 0; k < DT; k += 2) {
+      if (k + 1 < DT) issue(k + 1, nxt);
+      step(cur);
       if (k + 1 < DT) {
-        tmem_wait_ld_bind(nxt);
-#pragma unroll
-        for (int e = 0; e < kRun; ++e) cur[e] = nxt[e];
+        tmem_wait_ld_bind24(nxt);
+        if (k + 2 < DT) issue(k + 2, cur);
+        step(nxt);
+        if (k + 2 < DT) tmem_wait_ld_bind24(cur);
       }
     }
-    constexpr int NC = DT * NJ;
+    if (sync2) named_bar_sync(barid, 64);  // both halves done reading: part 2 may overwrite Y
+    constexpr int NC = NI * NJ;
 #pragma unroll
     for (int b = 0; b < (NC + 15) / 16; ++b) {
       uint32_t hw[8], lw[8];
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
-        const int c0 = b * 16 + 2 * q, c1 = c0 + 1;
         auto z = [&](int c) {
           const int i = c / NJ, j = c % NJ;
           if (c >= NC) return 0.f;
-          if (ODD && j == NJ - 1) return acc1[i];
+          if (j == NJ - 1) return acc1[i];
           return (j & 1) ? acc[i][j >> 1].y : acc[i][j >> 1].x;
         };
-        const float a0 = z(c0), a1 = z(c1);
+        const float a0 = z(b * 16 + 2 * q), a1 = z(b * 16 + 2 * q + 1);
         const __half2 hh = __floats2half2_rn(a0, a1);
         const float2 hf = __half22float2(hh);
         hw[q] = *reinterpret_cast<const uint32_t*>(&hh);
         lw[q] = pack_half2(a0 - hf.x, a1 - hf.y);
       }
-      tmem_st8(lb + zc + 16 * b, hw);
-      tmem_st8(lb + zc + 16 * b + 8, lw);
+      const uint32_t zc = b < nb1 ? zc1 + 16 * b : zc2 + 16 * (b - nb1);
+      tmem_st8(lb + zc, hw);
+      tmem_st8(lb + zc + 8, lw);
     }
+  } else {
+    if (sync2) named_bar_sync(barid, 64);
   }
 }
 
@@ -215,21 +182,29 @@ __device__ __forceinline__ void middle_pass(uint32_t lb, uint32_t zc) {
 // the exact scale 2^-e.
 __device__ __forceinline__ int convert_row(const float* st, int din, int kp, uint8_t* hi, uint8_t* lo, int r) {
   const float* src = st + r * din;
-  float ss = 0.f;
-  for (int k = 0; k < din; ++k) ss = fmaf(src[k], src[k], ss);
+  float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+  int k = 0;
+  for (; k + 4 <= din; k += 4) {
+    const float a = src[k], b = src[k + 1], c = src[k + 2], d = src[k + 3];
+    s0 = fmaf(a, a, s0); s1 = fmaf(b, b, s1); s2 = fmaf(c, c, s2); s3 = fmaf(d, d, s3);
+  }
+  for (; k < din; ++k) s0 = fmaf(src[k], src[k], s0);
+  const float ss = (s0 + s1) + (s2 + s3);
   int e = 0;
   if (ss > 0.f && ss < 3.0e38f) e = max(-120, min(120, ilogbf(ss) / 2 + 1));
   const float sc = pow2i(-e);
+#pragma unroll 2
   for (int k0 = 0; k0 < kp; k0 += 8) {
+    float v[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) v[q] = k0 + q < din ? src[k0 + q] * sc : 0.f;
     uint32_t hw[4], lw[4];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      const int k = k0 + 2 * q;
-      const float a0 = k < din ? src[k] * sc : 0.f, a1 = k + 1 < din ? src[k + 1] * sc : 0.f;
-      const __half2 hh = __floats2half2_rn(a0, a1);
+      const __half2 hh = __floats2half2_rn(v[2 * q], v[2 * q + 1]);
       const float2 hf = __half22float2(hh);
       hw[q] = *reinterpret_cast<const uint32_t*>(&hh);
-      lw[q] = pack_half2(a0 - hf.x, a1 - hf.y);
+      lw[q] = pack_half2(v[2 * q] - hf.x, v[2 * q + 1] - hf.y);
     }
     const uint32_t off = canon_off(r, k0, BM);
     *reinterpret_cast<uint4*>(hi + off) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
@@ -239,8 +214,8 @@ __device__ __forceinline__ int convert_row(const float* st, int din, int kp, uin
 }
 
 // optional in-kernel cycle accounting (env TPO_MTP_PROF=1), kProfSlots per CTA:
-// 0 conv total, 1 staging, 2 wait G1, 3 convert, 4 wait G2, 5 epilogue | 6 middle wait G1, 7 pass 0,
-// 8 pass 1 | 9 MMA wait ops, 10 GEMM 1 issue, 11 wait D free, 12 wait Z, 13 GEMM 2 issue, 14 MMA total
+// half A: 0 total, 1 staging, 2 wait G1, 15 middle, 3 convert, 4 wait G2, 5 epilogue | half B: 6 wait G1,
+// 7 middle, 8 convert | 9 MMA wait ops, 10 GEMM 1 issue, 11 wait D free, 12 wait Z, 13 GEMM 2 issue, 14 MMA total
 constexpr int kProfSlots = 16;
 __device__ unsigned long long* g_mtp_prof = nullptr;
 __device__ __forceinline__ long long now() { return clock64(); }
@@ -252,7 +227,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   __shared__ __align__(8) uint64_t bars[kBars];
   __shared__ uint32_t tmem_sh;
-  __shared__ int e_sh[2][BM];  // row scale exponents by tile parity (for the middle warps' epilogue half)
+  __shared__ int ex_sh[2][BM], ey_sh[2][BM];  // row scale exponents of x / y by tile parity
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t ntiles = (rs.rows + BM - 1) / BM;
@@ -269,9 +244,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&bars[i], 1);
       mbar_init(&bars[kMaxStages + i], 1);
     }
-    mbar_init(&bars[B_OPS_READY], BM);
+    mbar_init(&bars[B_OPS_READY], 2 * BM);
     mbar_init(&bars[B_G1_DONE], 1);
-    mbar_init(&bars[B_Z_READY], BM);
+    mbar_init(&bars[B_Z_READY], 2 * BM);
     mbar_init(&bars[B_G2_DONE], 1);
     mbar_init(&bars[B_D_FREE], 2 * BM);
     mbar_init(&bars[B_STAGE_FULL], 1);
@@ -353,10 +328,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   };
 
-  if (warp < 4) {
-    // ============================================= staging + conversion + epilogue (thread = row)
-    const int r = tid;
-    const uint32_t lb = tmem + (static_cast<uint32_t>(warp * 32) << 16);
+  if (warp < 8) {
+    // ============================================= workers: warp half hw of lane quarter q (thread = tile row)
+    // hw 0: middle rows i < IA, converts x; hw 1: middle rows i >= IA, converts y; both drain
+    // half of the output column blocks
+    const int q = warp & 3, hw = warp >> 2;
+    const int r = q * 32 + lane;
+    const uint32_t lb = tmem + (static_cast<uint32_t>(q * 32) << 16);
     // whole tiles of 16 B aligned inputs are staged by TMA bulk copies one tile ahead
     const bool aligned =
         ((reinterpret_cast<uintptr_t>(rs.x) | (rs.y_shared ? 0 : reinterpret_cast<uintptr_t>(rs.y))) & 15) == 0;
@@ -369,137 +347,117 @@ __global__ void __launch_bounds__(kThreads, 1)
       bulk_g2s(stx, rs.x + tl * BM * t.din1, bx, &bars[B_STAGE_FULL]);
       if (by) bulk_g2s(sty, rs.y + tl * BM * t.din2, by, &bars[B_STAGE_FULL]);
     };
-    // the rest (ragged tile, shared y): 16 rows per batch, all loads in flight before the first store
-    auto stage_rows = [&](int64_t tile, bool do_x, bool do_y) {
+    // the rest (ragged tile, shared y): this quarter's 32 rows of one input, 16 rows per
+    // batch with all loads in flight before the first store
+    auto stage_rows = [&](int64_t tile, bool is_y) {
+      const int din = is_y ? t.din2 : t.din1;
+      float* dst = is_y ? sty : stx;
       constexpr int kRB = 16;
 #pragma unroll 1
       for (int r0 = 0; r0 < 32; r0 += kRB) {
-        float vx[kRB][2], vy[kRB][2];
+        float v[kRB][2];
 #pragma unroll
         for (int rr = 0; rr < kRB; ++rr) {
-          const int64_t g = tile * BM + warp * 32 + r0 + rr;
+          const int64_t g = tile * BM + q * 32 + r0 + rr;
           const bool ok = g < rs.rows;
-          const float* xs = rs.x + (ok ? g : 0) * t.din1;
-          const float* ys = rs.y + (ok ? (rs.y_shared ? g / rs.channels : g) : 0) * t.din2;
+          const float* src = is_y ? rs.y + (ok ? (rs.y_shared ? g / rs.channels : g) : 0) * t.din2
+                                  : rs.x + (ok ? g : 0) * t.din1;
 #pragma unroll
-          for (int q = 0; q < 2; ++q) {
-            const int k = lane + 32 * q;
-            vx[rr][q] = (do_x && ok && k < t.din1) ? __ldg(xs + k) : 0.f;
-            vy[rr][q] = (do_y && ok && k < t.din2) ? __ldg(ys + k) : 0.f;
+          for (int c = 0; c < 2; ++c) {
+            const int k = lane + 32 * c;
+            v[rr][c] = (ok && k < din) ? __ldg(src + k) : 0.f;
           }
         }
 #pragma unroll
-        for (int rr = 0; rr < kRB; ++rr) {
-          const int row = warp * 32 + r0 + rr;
+        for (int rr = 0; rr < kRB; ++rr)
 #pragma unroll
-          for (int q = 0; q < 2; ++q) {
-            const int k = lane + 32 * q;
-            if (do_x && k < t.din1) stx[row * t.din1 + k] = vx[rr][q];
-            if (do_y && k < t.din2) sty[row * t.din2 + k] = vy[rr][q];
+          for (int c = 0; c < 2; ++c) {
+            const int k = lane + 32 * c;
+            if (k < din) dst[(q * 32 + r0 + rr) * din + k] = v[rr][c];
           }
-        }
       }
       __syncwarp();
     };
     int ns = 0;  // TMA stagings consumed (B_STAGE_FULL phase)
-    auto land_stage = [&](int64_t tl) {
+    auto land = [&](int64_t tl) {
       if (tma_x(tl)) {
         mbar_wait(&bars[B_STAGE_FULL], ns & 1);
         ++ns;
       }
-      if (!tma_y(tl)) stage_rows(tl, !tma_x(tl), true);
+      if (hw == 0 && !tma_x(tl)) stage_rows(tl, false);
+      if (hw == 1 && !tma_y(tl)) stage_rows(tl, true);
     };
-    auto convert = [&](int slot) {
-      const int ex = convert_row(stx, t.din1, t.k1, xop, xop + BM * t.k1 * 2, r);
-      const int ey = convert_row(sty, t.din2, t.k2, yop, yop + BM * t.k2 * 2, r);
-      e_sh[slot][r] = ex + ey;
+    auto convert_mine = [&](int slot) {
+      if (hw == 0) ex_sh[slot][r] = convert_row(stx, t.din1, t.k1, xop, xop + BM * t.k1 * 2, r);
+      else ey_sh[slot][r] = convert_row(sty, t.din2, t.k2, yop, yop + BM * t.k2 * 2, r);
       fence_proxy_async_smem();
       mbar_arrive(&bars[B_OPS_READY]);
-      return ex + ey;
+    };
+    auto middle_mine = [&]() {
+      // half 0: Z group 0 in one piece; half 1: group 1, its tail (if any) in the Y columns
+      if (hw == 0)
+        middle_half<DT, 0>(lb, static_cast<uint32_t>(t.zgrp_col[0]), 64, 0u, t.y0_reuse != 0, 4 + q);
+      else
+        middle_half<DT, 1>(lb, static_cast<uint32_t>(t.zgrp_col[1]), t.zgrp_size[1] / 16,
+                           static_cast<uint32_t>(t.zgrp_col[2]), t.y0_reuse != 0, 4 + q);
     };
     int it = 0;
     int64_t tile = blockIdx.x;
-    int e_cur = 0;
     const long long tstart = now();
     if (tile < ntiles) {
       if (tid == 0) issue_stage(tile);
-      land_stage(tile);
-      e_cur = convert(0);
-      named_bar_sync(1, BM);  // staging consumed
+      land(tile);
+      convert_mine(0);
+      named_bar_sync(1, 2 * BM);  // staging consumed
       if (tid == 0 && tile + gridDim.x < ntiles) issue_stage(tile + gridDim.x);
     }
     for (; tile < ntiles; tile += gridDim.x, ++it) {
       const int64_t nxt = tile + gridDim.x;
-      int e_nxt = 0;
-      if (nxt < ntiles) {
-        long long t0 = now();
-        land_stage(nxt);
-        tick(1, t0);
-        t0 = now();
-        mbar_wait(&bars[B_G1_DONE], it & 1);  // X / Y operands consumed
-        tick(2, t0);
-        t0 = now();
-        e_nxt = convert((it + 1) & 1);
-        named_bar_sync(1, BM);
-        tick(3, t0);
-      }
-      long long t0 = now();
-      mbar_wait(&bars[B_G2_DONE], it & 1);
-      tick(4, t0);
-      t0 = now();
-      tc_fence_after();
-      const int64_t row0 = tile * BM + warp * 32;
-      const bool bulk = bulk_ok(tile);
-      if (bulk) {
-        epilogue_bulk(lb, e_cur, tile, warp, 0);
-      } else {
-        epilogue_part(lb, e_cur, row0, 0);
-        tc_fence_before();
-        mbar_arrive(&bars[B_D_FREE]);
-      }
-      // raw inputs of the tile after next (the staging buffer was the output half buffer 1)
-      if (tid == 64 && nxt + gridDim.x < ntiles) issue_stage(nxt + gridDim.x);
-      tick(5, t0);
-      // degrees past the carrier band are exactly zero (proj/src/mtp.cpp:126)
-      if (!bulk && t.dout_total > t.dout_eff)
-        for (int rr = 0; rr < 32; ++rr) {
-          const int64_t g = row0 + rr;
-          if (g >= rs.rows) break;
-          for (int col = t.dout_eff + lane; col < t.dout_total; col += 32) rs.out[g * t.dout_total + col] = 0.f;
-        }
-      e_cur = e_nxt;
-    }
-    tick(0, tstart);
-    if (PROF && tid == 0)
-      for (int k = 0; k < 6; ++k) g_mtp_prof[blockIdx.x * kProfSlots + k] = pc[k];
-  } else if (warp < 8) {
-    // ============================================= middle: Z = X Y per TMEM lane; other half of the epilogue
-    const uint32_t lb = tmem + (static_cast<uint32_t>((warp & 3) * 32) << 16);
-    int it = 0;
-    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
       long long t0 = now();
       mbar_wait(&bars[B_G1_DONE], it & 1);
       tc_fence_after();
-      tick(6, t0);
+      tick(hw ? 6 : 2, t0);
       t0 = now();
-      middle_pass<DT, 0>(lb, static_cast<uint32_t>(t.zgrp_col[0]));
-      tick(7, t0);
-      t0 = now();
-      middle_pass<DT, 1>(lb, static_cast<uint32_t>(t.zgrp_col[1]));  // may reuse Y block 0 (own lane only)
+      middle_mine();
       tmem_wait_st();
-      tick(8, t0);
       tc_fence_before();
       mbar_arrive(&bars[B_Z_READY]);
+      tick(hw ? 7 : 15, t0);
+      t0 = now();
+      if (nxt < ntiles) land(nxt);  // the TMA had the whole middle to land
+      if (!hw) tick(1, t0);
+      t0 = now();
+      if (nxt < ntiles) convert_mine((it + 1) & 1);
+      named_bar_sync(1, 2 * BM);  // raw staging consumed: it may now hold output rows 64-127
+      tick(hw ? 8 : 3, t0);
+      t0 = now();
       mbar_wait(&bars[B_G2_DONE], it & 1);
       tc_fence_after();
-      if (bulk_ok(tile)) {
-        epilogue_bulk(lb, e_sh[it & 1][tid - BM], tile, warp & 3, 1);
+      if (!hw) tick(4, t0);
+      t0 = now();
+      const int e_row = ex_sh[it & 1][r] + ey_sh[it & 1][r];
+      const bool bulk = bulk_ok(tile);
+      if (bulk) {
+        epilogue_bulk(lb, e_row, tile, q, hw);
       } else {
-        epilogue_part(lb, e_sh[it & 1][tid - BM], tile * BM + (warp & 3) * 32, 1);
+        epilogue_part(lb, e_row, tile * BM + q * 32, hw);
         tc_fence_before();
         mbar_arrive(&bars[B_D_FREE]);
       }
+      // raw inputs of the tile after next (the staging buffer was output half buffer 1)
+      if (tid == 64 && nxt + gridDim.x < ntiles) issue_stage(nxt + gridDim.x);
+      // degrees past the carrier band are exactly zero (proj/src/mtp.cpp:126)
+      if (!bulk && hw == 0 && t.dout_total > t.dout_eff)
+        for (int rr = 0; rr < 32; ++rr) {
+          const int64_t g = tile * BM + q * 32 + rr;
+          if (g >= rs.rows) break;
+          for (int col = t.dout_eff + lane; col < t.dout_total; col += 32) rs.out[g * t.dout_total + col] = 0.f;
+        }
+      if (!hw) tick(5, t0);
     }
+    if (!hw) tick(0, tstart);
+    if (PROF && tid == 0)
+      for (int k : {0, 1, 2, 3, 4, 5, 15}) g_mtp_prof[blockIdx.x * kProfSlots + k] = pc[k];
     if (PROF && tid == 128)
       for (int k = 6; k < 9; ++k) g_mtp_prof[blockIdx.x * kProfSlots + k] = pc[k];
   } else if (warp == 8) {
@@ -549,7 +507,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         __syncwarp();
       }
     };
-    const int p0 = t.kz - ((DT * (DT - Carrier<DT>::J1) + 15) / 16 * 16);  // K extent of Z pass 0
     int it = 0;
     const long long tstart = now();
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
@@ -576,18 +533,19 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_after();
       tick(12, t0);
       t0 = now();
-      for (int ks = 0; ks < t.kz / 16; ++ks) {
-        const int s = take();
-        const uint32_t sb = smem_u32(ring + s * t.stage_bytes);
-        const int kc = ks * 16;
-        const uint32_t zh = tmem + static_cast<uint32_t>(kc < p0 ? t.zgrp_col[0] + kc : t.zgrp_col[1] + kc - p0);
-        const uint64_t bh = make_sdesc(sb, lbo2, 128), bl = make_sdesc(sb + half2, lbo2, 128);
-        if (el) mma_f16_ts(tmem, zh, bh, id2, ks > 0 ? 1u : 0u);
-        if (el) mma_f16_ts(tmem, zh, bl, id2, 1u);
-        if (el) mma_f16_ts(tmem, zh + 8, bh, id2, 1u);
-        if (el) tc_commit(&bars[kMaxStages + s]);
-        __syncwarp();
-      }
+      int ks = 0;
+      for (int g = 0; g < 4; ++g)  // Z groups in K order: (block 0, half 0), (0, 1), (1, 0), (1, 1)
+        for (int c = 0; c < t.zgrp_size[g]; c += 16, ++ks) {
+          const int s = take();
+          const uint32_t sb = smem_u32(ring + s * t.stage_bytes);
+          const uint32_t zh = tmem + static_cast<uint32_t>(t.zgrp_col[g] + c);
+          const uint64_t bh = make_sdesc(sb, lbo2, 128), bl = make_sdesc(sb + half2, lbo2, 128);
+          if (el) mma_f16_ts(tmem, zh, bh, id2, ks > 0 ? 1u : 0u);
+          if (el) mma_f16_ts(tmem, zh, bl, id2, 1u);
+          if (el) mma_f16_ts(tmem, zh + 8, bh, id2, 1u);
+          if (el) tc_commit(&bars[kMaxStages + s]);
+          __syncwarp();
+        }
       if (el) tc_commit(&bars[B_G2_DONE]);
       __syncwarp();
       tick(13, t0);
