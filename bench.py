@@ -407,7 +407,7 @@ def side_measurements(tpo, dev, stream, flush, peaks):
         else:
             fl = 2 * 6378 * B  # 2 x reference sparse muls
             roof = max(byts / hbm, fl / fp32)
-            bound = "max(HBM, FP32 SIMT at nominal clock)"
+            bound = "max(HBM, FP32 at the reference sparse op count, nominal clock)"
         res[f"{kind}_L{L}_B{B}"] = {"ms": round(ms, 4), "tp_per_s": round(B / t, 1), "tflops": round(fl / t / 1e12, 2),
                                      "gbs": round(byts / t / 1e9, 1), "roofline_frac": round(roof / t, 4), "bound": bound}
     # channel-wise CGTP, config C4 shape (L=3, 128 channels, y shared per edge) on a 2^14-edge chunk
