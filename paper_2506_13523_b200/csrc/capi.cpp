@@ -105,6 +105,16 @@ void run_cgtp(tpo_ctx* ctx, int L1, int L2, const RowSpec& rs, cudaStream_t s) {
     launched(ctx, tpo_b200::launch_cgtp_edge_tc(t, p, rs, ctx->impl.num_sms(), s), "cgtp edge tcgen05 kernel");
     return;
   }
+  // larger degrees: per-(l1, l2) block GEMMs on tcgen05 (output-write bound)
+  static const int tc_min_l = [] {
+    const char* v = std::getenv("TPO_CGTP_TC_MINL");
+    return v ? std::atoi(v) : 5;  // measured: SIMT wins at L <= 3, even at L = 4
+  }();
+  if (std::max(L1, L2) >= tc_min_l)
+    if (const tpo_b200::CgtpTcTables* tc = ctx->impl.cgtp_tc(L1, L2)) {
+      launched(ctx, tpo_b200::launch_cgtp_tc(*tc, rs, ctx->impl.num_sms(), s), "cgtp tcgen05 kernel");
+      return;
+    }
   launched(ctx, tpo_b200::launch_cgtp(t, rs, ctx->impl.num_sms(), s), "cgtp kernel");
 }
 

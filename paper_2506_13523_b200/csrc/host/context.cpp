@@ -653,6 +653,107 @@ const MtpDevTables& Context::mtp(int L1, int L2, int L3, int lt) {
   return mtp_.emplace(std::array<int, 4>{L1, L2, L3, lt}, t).first->second;
 }
 
+// ------------------------------------------------------------------ CGTP, tcgen05 blocks
+// W_{l1 l2}[o][k]: o = position of (l3, m3) inside the block (l3 ascending from
+// |l1 - l2|, m3 = -l3..l3, the reference's path order, proj/src/cgtp.cpp:152-163),
+// k = (m1 + l1)(2 l2 + 1) + m2 + l2; values = real CG (proj/src/wigner.cpp:114-151).
+const CgtpTcTables* Context::cgtp_tc(int L1, int L2) {
+  std::lock_guard<std::mutex> g(mu_);
+  auto it = cgtp_tc_.find({L1, L2});
+  if (it != cgtp_tc_.end()) return it->second.first ? &it->second.second : nullptr;
+  auto fail = [&]() -> const CgtpTcTables* {
+    cgtp_tc_.emplace(std::array<int, 2>{L1, L2}, std::make_pair(false, CgtpTcTables{}));
+    return nullptr;
+  };
+  const char* env = std::getenv("TPO_CGTP_TC");
+  if ((env && env[0] == '0') || L1 > 10 || L2 > 10) return fail();
+  CgtpTcTables t{};
+  t.din1 = (L1 + 1) * (L1 + 1);
+  t.din2 = (L2 + 1) * (L2 + 1);
+  std::vector<CgtpTcUnit> units;
+  std::vector<uint16_t> w;
+  int out_off = 0, max_npad = 16;
+  for (int l1 = 0; l1 <= L1; ++l1)
+    for (int l2 = 0; l2 <= L2; ++l2) {
+      const int n1 = 2 * l1 + 1, n2 = 2 * l2 + 1, n = n1 * n2;
+      std::vector<double> W(static_cast<size_t>(n) * n, 0.0);
+      int o0 = 0;
+      for (int l3 = std::abs(l1 - l2); l3 <= l1 + l2; ++l3) {
+        for (const CGEntry& e : real_cg(l1, l2, l3))
+          W[static_cast<size_t>(o0 + e.m3 + l3) * n + (e.m1 + l1) * n2 + (e.m2 + l2)] += e.v;
+        o0 += 2 * l3 + 1;
+      }
+      // K order k = m1 * n2p + m2 (n2p = n2 padded to 8; zero columns at the padding)
+      const int n2p = pad_to(n2, 8), kw = n1 * n2p;
+      const int kpad = pad_to(kw, 16), npad_all = pad_to(n, 16);
+      const int parts = (npad_all + 255) / 256;
+      const int np = pad_to((n + parts - 1) / parts, 16);
+      for (int p = 0; p < parts; ++p) {
+        CgtpTcUnit u{};
+        u.l1 = l1;
+        u.l2 = l2;
+        u.out_off = out_off + p * np;
+        u.n_valid = std::min(np, n - p * np);
+        u.n_pad = pad_to(u.n_valid, 16);
+        u.ksteps = kpad / 16;
+        u.w_off = static_cast<int>(w.size() * 2);
+        max_npad = std::max(max_npad, u.n_pad);
+        const size_t base = w.size();
+        w.resize(base + static_cast<size_t>(u.ksteps) * 2 * u.n_pad * 16, 0);
+        for (int ks = 0; ks < u.ksteps; ++ks) {
+          uint16_t* hi = w.data() + base + static_cast<size_t>(ks) * 2 * u.n_pad * 16;
+          uint16_t* lo = hi + u.n_pad * 16;
+          for (int r = 0; r < u.n_valid; ++r)
+            for (int kk = 0; kk < 16; ++kk) {
+              const int k = ks * 16 + kk, m1 = k / n2p, m2 = k % n2p;
+              if (k >= kw || m2 >= n2) continue;
+              uint16_t hv, lv;
+              split_half(W[static_cast<size_t>(p * np + r) * n + m1 * n2 + m2], hv, lv);
+              const uint32_t o = sm100::canon_off(r, kk, u.n_pad) / 2;
+              hi[o] = hv;
+              lo[o] = lv;
+            }
+        }
+        units.push_back(u);
+      }
+      out_off += n;
+    }
+  // super-units: consecutive units packed into one 256-column accumulator
+  for (size_t i = 0, col = 0; i < units.size(); ++i) {
+    if (col + units[i].n_pad > 256) {
+      units[i - 1].dcol_last |= 1 << 16;
+      col = 0;
+    }
+    units[i].dcol_last = static_cast<int>(col);
+    col += units[i].n_pad;
+  }
+  units.back().dcol_last |= 1 << 16;
+  t.dout = out_off;
+  t.nunits = static_cast<int>(units.size());
+  t.units = upload(units);
+  t.w = reinterpret_cast<const uint8_t*>(upload(w));
+  // shared memory: A ring (8 KB stages) | W ring | per-row x | y staging (odd pitch)
+  t.b_stage_bytes = 64 * max_npad;
+  t.xy_pitch = (t.din2 + 21 + 8) | 1;  // y row | x_{l1} (reads may run 7 past a y segment)
+  const int xy_bytes = 128 * t.xy_pitch * 4;
+  const int budget = 186 * 1024 - xy_bytes;  // the kernel's static staging takes ~35 KB
+  t.a_stages = 4;  // 16 KB stages (two K-steps)
+  t.b_stages = std::min(8, (budget - t.a_stages * 16384) / t.b_stage_bytes);
+  while (t.b_stages < 4 && t.a_stages > 2) {
+    --t.a_stages;
+    t.b_stages = std::min(8, (budget - t.a_stages * 16384) / t.b_stage_bytes);
+  }
+  if (t.b_stages < 2) return fail();
+  t.off_a = 0;
+  t.off_b = t.a_stages * 16384;
+  t.off_xy = t.off_b + t.b_stages * t.b_stage_bytes;
+  t.smem_bytes = t.off_xy + xy_bytes;
+  if (std::getenv("TPO_VERBOSE"))
+    std::fprintf(stderr, "[tpo] cgtp tcgen05 L=(%d,%d) units=%d dout=%d w=%zu B stages a=%d b=%d smem=%d\n", L1, L2,
+                 t.nunits, t.dout, w.size() * 2, t.a_stages, t.b_stages, t.smem_bytes);
+  return &cgtp_tc_.emplace(std::array<int, 2>{L1, L2}, std::make_pair(true, t)).first->second.second;
+}
+
 // ------------------------------------------------------------------ MTP, tcgen05
 // Dense embed / extract operators in the TMEM orders of mtp_tc.cu
 // (kernels.hpp, MtpTcTables), same CG tables as Context::mtp

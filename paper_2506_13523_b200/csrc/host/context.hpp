@@ -49,6 +49,7 @@ class Context {
   void activate() const;
 
   const CgtpTables& cgtp(int L1, int L2);
+  const CgtpTcTables* cgtp_tc(int L1, int L2);  // nullptr: shape not on the tcgen05 block path
   const GridTcEntry& grid_tc(int L1, int L2, int L3);
   const GridTcEntry& fourier_tc(int L1, int L2, int L3);  // Fourier GTP as torus-grid dense operators
   const GridSimtTables& grid_simt(int L1, int L2, int L3);
@@ -85,6 +86,7 @@ class Context {
   std::mutex mu_;
   std::vector<void*> allocs_;
   std::map<std::array<int, 2>, CgtpTables> cgtp_;
+  std::map<std::array<int, 2>, std::pair<bool, CgtpTcTables>> cgtp_tc_;
   std::map<std::array<int, 3>, GridTcEntry> grid_tc_;
   std::map<std::array<int, 3>, GridTcEntry> fourier_tc_;
   GridTcEntry build_dense_tc(const struct DenseOps& ops, const char* label);

@@ -48,6 +48,24 @@ int cgtp_edge_tc_smem(const CgtpTables& t, int kp, int dout_pad);
 cudaError_t launch_cgtp_edge_tc(const CgtpTables& t, const EdgeTcParams& p, const RowSpec& rs, int num_sms,
                                 cudaStream_t s);
 
+// General CGTP on tcgen05 (cgtp_tc.cu): per (l1, l2) block one dense GEMM
+// out_block = (x_{l1} (x) y_{l2}) . W^T with the square real-CG block W.  A unit is
+// (block, N part of <= 256 outputs); consecutive units share one accumulator
+// ("super-unit", <= 256 columns, one hand-off to the epilogue); w holds per unit and K-step
+// [hi | lo][n_pad rows (block outputs)][16 (k = m1 (2 l2 + 1) + m2)] canonical.
+struct CgtpTcUnit {
+  int l1, l2, out_off, n_valid, n_pad, ksteps, w_off;
+  int dcol_last;  // column inside the 256-column accumulator | (last unit of its super-unit) << 16
+};
+struct CgtpTcTables {
+  int din1, din2, dout, nunits;
+  int a_stages, b_stages, b_stage_bytes, smem_bytes;
+  int off_a, off_b, off_xy, xy_pitch;  // xy: per-row staging [128][xy_pitch], x row | y row
+  const CgtpTcUnit* units;
+  const uint8_t* w;
+};
+cudaError_t launch_cgtp_tc(const CgtpTcTables& t, const RowSpec& rs, int num_sms, cudaStream_t s);
+
 // ---------------------------------------------------------------- GTP grid, tcgen05
 // Dense operators of the reference's product grid, pre-split into fp16 hi/lo
 // and pre-tiled on the host in the UMMA canonical K-major layout, one

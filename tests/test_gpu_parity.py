@@ -122,6 +122,60 @@ def test_cgtp_edge_tiles(tpo, orc, C):
     assert _normwise(out, ref) <= TOL
 
 
+@pytest.mark.parametrize("L,B", [(5, 148 * 128 * 2 + 77), (6, 148 * 128 + 5), (7, 700), (8, 300), (10, 200)])
+def test_cgtp_tensor_cores(tpo, orc, L, B):
+    # per-(l1, l2) block GEMMs on tcgen05: several tiles per CTA, ragged tail, rows of
+    # very different magnitude (per-row power-of-two scaling)
+    x, y = _inputs(B, L, L, 360 + L)
+    x[0] *= 1e-3
+    y[1] *= 1e3
+    out = _gpu(tpo, "cgtp", x, y, L, L, 0)
+    ref = orc.batch_mimo("cgtp", L, x.astype(np.float64)[:, None], y.astype(np.float64)[:, None])[:, 0]
+    assert _normwise(out, ref) <= TOL
+
+
+def test_cgtp_tc_unequal_and_shared(tpo, orc):
+    # block path with L1 != L2, and with y shared per edge at a channel count the
+    # edge kernel does not take
+    x, y = _inputs(90, 5, 3, 380)
+    out = _gpu(tpo, "cgtp", x, y, 5, 3, 0)
+    ref = np.stack([_ref_single(orc, "cgtp", x[b], y[b], 5, 3, 0) for b in range(90)])
+    assert _normwise(out, ref) <= TOL
+    x, y = _inputs(7, 5, 5, 381, C=24, shared=True)
+    out = _gpu(tpo, "cgtp", x, y, 5, 5, 0)
+    ref = orc.batch_mimo("cgtp", 5, x.astype(np.float64), y.astype(np.float64), channels=24, y_shared=True)
+    assert _normwise(out, ref) <= TOL
+
+
+def test_cgtp_simt_path():
+    # SIMT kernel (the default below L = 5; forced here in a fresh process at larger L)
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parents[1]
+    code = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, %r); sys.path.insert(0, %r)
+import oracle, paper_2506_13523_b200 as tpo
+worst = 0.0
+for L, B in ((5, 200), (6, 100)):
+    rng = np.random.default_rng(970 + L)
+    d = (L + 1) ** 2
+    x = rng.standard_normal((B, d)).astype(np.float32); y = rng.standard_normal((B, d)).astype(np.float32)
+    out = tpo.run("cgtp", torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda(), L, L, 0).cpu().numpy()
+    ref = oracle.batch_mimo("cgtp", L, x.astype(np.float64)[:, None], y.astype(np.float64)[:, None])[:, 0]
+    err = (np.abs(out - ref).max(axis=1) / np.maximum(np.abs(ref).max(axis=1), 1e-300)).max()
+    worst = max(worst, float(err))
+print(worst)
+""" % (str(root), str(root / "oracle"))
+    env = dict(os.environ, TPO_CGTP_TC="0")
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=240, env=env)
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert float(r.stdout.strip().splitlines()[-1]) <= TOL
+
+
 @pytest.mark.parametrize("L", [12, 16])
 def test_cgtp_large(tpo, orc, L):
     _check_batch(tpo, orc, "cgtp", L, 8, 310 + L)
@@ -354,6 +408,35 @@ for kind in ("gtp_grid", "gtp_fourier"):
 print(worst)
 """ % (str(root), str(root / "oracle"))
     env = dict(os.environ, TPO_GRID_PAIR="1")
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=240, env=env)
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert float(r.stdout.strip().splitlines()[-1]) <= TOL
+
+
+def test_cgtp_block_path_small_degrees():
+    # the tcgen05 block kernel at L <= 4 (not the default there), fresh process
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parents[1]
+    code = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, %r); sys.path.insert(0, %r)
+import oracle, paper_2506_13523_b200 as tpo
+worst = 0.0
+for L, B in ((0, 50), (1, 300), (2, 129), (3, 5000), (4, 700)):
+    rng = np.random.default_rng(990 + L)
+    d = (L + 1) ** 2
+    x = rng.standard_normal((B, d)).astype(np.float32); y = rng.standard_normal((B, d)).astype(np.float32)
+    out = tpo.run("cgtp", torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda(), L, L, 0).cpu().numpy()
+    ref = oracle.batch_mimo("cgtp", L, x.astype(np.float64)[:, None], y.astype(np.float64)[:, None])[:, 0]
+    err = (np.abs(out - ref).max(axis=1) / np.maximum(np.abs(ref).max(axis=1), 1e-300)).max()
+    worst = max(worst, float(err))
+print(worst)
+""" % (str(root), str(root / "oracle"))
+    env = dict(os.environ, TPO_CGTP_TC_MINL="0")
     r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=240, env=env)
     assert r.returncode == 0, r.stderr[-2000:]
     assert float(r.stdout.strip().splitlines()[-1]) <= TOL
