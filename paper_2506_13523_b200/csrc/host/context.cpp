@@ -737,15 +737,17 @@ const CgtpTcTables* Context::cgtp_tc(int L1, int L2) {
   t.xy_pitch = (t.din2 + 21 + 8) | 1;  // y row | x_{l1} (reads may run 7 past a y segment)
   const int xy_bytes = 128 * t.xy_pitch * 4;
   const int budget = 186 * 1024 - xy_bytes;  // the kernel's static staging takes ~35 KB
-  t.a_stages = 4;  // 16 KB stages (two K-steps)
-  t.b_stages = std::min(8, (budget - t.a_stages * 16384) / t.b_stage_bytes);
+  const char* as_env = std::getenv("TPO_CGTP_ASTAGES");
+  constexpr int kAStageBytes = 16384;  // two K-steps (cgtp_tc.cu kKps)
+  t.a_stages = as_env ? std::max(2, std::min(8, std::atoi(as_env))) : 4;
+  t.b_stages = std::min(8, (budget - t.a_stages * kAStageBytes) / t.b_stage_bytes);
   while (t.b_stages < 4 && t.a_stages > 2) {
     --t.a_stages;
-    t.b_stages = std::min(8, (budget - t.a_stages * 16384) / t.b_stage_bytes);
+    t.b_stages = std::min(8, (budget - t.a_stages * kAStageBytes) / t.b_stage_bytes);
   }
   if (t.b_stages < 2) return fail();
   t.off_a = 0;
-  t.off_b = t.a_stages * 16384;
+  t.off_b = t.a_stages * kAStageBytes;
   t.off_xy = t.off_b + t.b_stages * t.b_stage_bytes;
   t.smem_bytes = t.off_xy + xy_bytes;
   if (std::getenv("TPO_VERBOSE"))

@@ -36,7 +36,8 @@ constexpr int BM = 128;
 constexpr int kThreads = 576;  // 18 warps
 constexpr int kMaxStages = 8;
 constexpr int kStageStride = 33;  // epilogue staging row pitch (32-column blocks)
-constexpr int kAStage = 2 * BM * 32 * 2;  // two K-steps: hi + lo, 128 x 32 fp16 each
+constexpr int kKps = 2;                         // K-steps per A stage (4: fewer stages fit, slower at L = 10)
+constexpr int kAStage = 2 * BM * 16 * kKps * 2;  // hi + lo, 128 x (16 kKps) fp16 each
 // barriers: A full [8], A empty [8], B full [8], B empty [8], D full [2], D empty [2]
 constexpr int B_AF = 0, B_AE = 8, B_BF = 16, B_BE = 24, B_DF = 32, B_DE = 34, kBars = 36;
 
@@ -147,7 +148,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t id = idesc_f16(BM, un.n_pad);
         const uint32_t lbo_b = (un.n_pad / 8) * 128, half_b = 32u * un.n_pad;
         for (int ks = 0; ks < un.ksteps; ++ks) {
-          const int j = ks & 1;  // K-step inside the A stage (a stage holds two; units start a new stage)
+          const int j = ks & (kKps - 1);  // K-step inside the A stage (units start a new stage)
           long long t0 = now();
           if (j == 0) mbar_wait(&bars[B_AF + sa], pa);
           tick(3, t0);
@@ -163,7 +164,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (el) mma_f16_ss(dc, ah, bl, id, 1u);
           if (el) mma_f16_ss(dc, al, bh, id, 1u);
           if (el) tc_commit(&bars[B_BE + sb]);
-          if (j == 1 || ks + 1 == un.ksteps) {
+          if (j == kKps - 1 || ks + 1 == un.ksteps) {
             if (el) tc_commit(&bars[B_AE + sa]);
             if (++sa == t.a_stages) {
               sa = 0;
@@ -248,40 +249,32 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         const float* xs = row + t.din2;
         const float* ys = row + un.l2 * un.l2;
-        int m1 = 0, cm = h;  // this thread's chunk: x index m1, y offset 8 cm
-        while (cm >= cpr) {
-          cm -= cpr;
-          ++m1;
-        }
-        for (int ks0 = 0; ks0 < un.ksteps; ks0 += 2) {  // one A stage = two K-steps
+        // chunk c (8 products: x index c / cpr, y offset 8 (c % cpr)); cpr <= 3 for l2 <= 10
+        const int cdiv = cpr == 1 ? 0 : (cpr == 2 ? 1 : 2);
+        int c = h;
+        for (int ks0 = 0; ks0 < un.ksteps; ks0 += kKps, c += 2 * kKps) {  // one A stage = kKps K-steps
           const long long t0 = now();
           if (na++ >= t.a_stages) mbar_wait(&bars[B_AE + sa], pa ^ 1);
           tick(8, t0);
           uint8_t* st = ring_a + sa * kAStage;
-          const int nj = min(2, un.ksteps - ks0);
 #pragma unroll
-          for (int j = 0; j < 2; ++j) {
-            if (j < nj) {
-              const float xv = m1 < n1 ? xs[m1] : 0.f;
-              const float* yp = ys + 8 * cm;
-              uint32_t hw[4], lw[4];
+          for (int j = 0; j < kKps; ++j) {  // (tail sub-steps past the unit are built but never issued)
+            const int cc = c + 2 * j;
+            const int m1 = cdiv == 0 ? cc : (cdiv == 1 ? cc >> 1 : (cc * 0xAAAB) >> 17);
+            const float xv = m1 < n1 ? xs[m1] : 0.f;
+            const float* yp = ys + 8 * (cc - m1 * cpr);
+            uint32_t hw[4], lw[4];
 #pragma unroll
-              for (int q = 0; q < 4; ++q) {
-                const float p0 = xv * yp[2 * q], p1 = xv * yp[2 * q + 1];
-                const __half2 hh = __floats2half2_rn(p0, p1);
-                const float2 hf = __half22float2(hh);
-                hw[q] = *reinterpret_cast<const uint32_t*>(&hh);
-                lw[q] = pack_half2(p0 - hf.x, p1 - hf.y);
-              }
-              cm += 2;  // the other half takes the chunk in between
-              while (cm >= cpr) {
-                cm -= cpr;
-                ++m1;
-              }
-              *reinterpret_cast<uint4*>(st + canon_off(r, 16 * j + 8 * h, BM)) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
-              *reinterpret_cast<uint4*>(st + kAStage / 2 + canon_off(r, 16 * j + 8 * h, BM)) =
-                  make_uint4(lw[0], lw[1], lw[2], lw[3]);
+            for (int q = 0; q < 4; ++q) {
+              const float p0 = xv * yp[2 * q], p1 = xv * yp[2 * q + 1];
+              const __half2 hh = __floats2half2_rn(p0, p1);
+              const float2 hf = __half22float2(hh);
+              hw[q] = *reinterpret_cast<const uint32_t*>(&hh);
+              lw[q] = pack_half2(p0 - hf.x, p1 - hf.y);
             }
+            *reinterpret_cast<uint4*>(st + canon_off(r, 16 * j + 8 * h, BM)) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+            *reinterpret_cast<uint4*>(st + kAStage / 2 + canon_off(r, 16 * j + 8 * h, BM)) =
+                make_uint4(lw[0], lw[1], lw[2], lw[3]);
           }
           const long long tf = now();
           fence_proxy_async_smem();
@@ -390,7 +383,7 @@ cudaError_t launch_cgtp_tc(const CgtpTcTables& t, const RowSpec& rs, int num_sms
       for (int k = 0; k < kProfSlots; ++k) avg[k] += static_cast<double>(h[b * kProfSlots + k]) / grid;
     std::fprintf(stderr,
                  "[tpo-prof] cgtp tiles=%lld | producer %.0f ring %.0f | mma %.0f a_wait %.0f b_wait %.0f d_empty %.0f | "
-                 "builder %.0f staging %.0f a_empty %.0f | epilogue %.0f d_full %.0f\n",
+                 "builder %.0f staging %.0f a_empty %.0f fence %.0f | epilogue %.0f d_full %.0f\n",
                  static_cast<long long>(ntiles), avg[0], avg[1], avg[2], avg[3], avg[4], avg[5], avg[6], avg[7], avg[8],
                  avg[11], avg[9], avg[10]);
     cudaFree(buf);
