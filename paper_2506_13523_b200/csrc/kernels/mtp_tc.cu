@@ -223,8 +223,9 @@ __device__ __forceinline__ long long now() { return clock64(); }
 template <int DT, bool PROF>
 __global__ void __launch_bounds__(kThreads, 1)
     mtp_tc_kernel(const __grid_constant__ MtpTcTables t, const __grid_constant__ RowSpec rs) {
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // used directly (no pointer re-alignment): every access stays in the shared space (LDS / STS);
+  // the SWIZZLE_NONE operand layouts need 16 B alignment only
+  extern __shared__ __align__(128) uint8_t smem[];
   __shared__ __align__(8) uint64_t bars[kBars];
   __shared__ uint32_t tmem_sh;
   __shared__ int ex_sh[2][BM], ey_sh[2][BM];  // row scale exponents of x / y by tile parity
