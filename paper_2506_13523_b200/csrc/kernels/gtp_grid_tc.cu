@@ -138,13 +138,27 @@ __device__ __noinline__ void convert_input(const float* raw, int din, int kp, ui
   const int nv = min(kh, din - k0);  // valid raw values of this half (may be <= 0)
   float v[kKHalfMax];
   float ss = 0.f;
+  if ((din & 3) == 0) {
+    // rows of a multiple of 4 floats sit a multiple of 16 B apart: 128-bit reads (a scalar
+    // read of the same k by 32 rows would hit one bank 32 / gcd-fold, e.g. 32-way at din = 64)
+    const float4* src4 = reinterpret_cast<const float4*>(src);
 #pragma unroll
-  for (int j0 = 0; j0 < kKHalfMax; j0 += 8) {
-    if (j0 < kh) {
+    for (int j0 = 0; j0 < kKHalfMax; j0 += 4) {
+      if (j0 < kh) {
+        const float4 a = (j0 < nv) ? src4[j0 >> 2] : make_float4(0.f, 0.f, 0.f, 0.f);
+        v[j0] = a.x; v[j0 + 1] = a.y; v[j0 + 2] = a.z; v[j0 + 3] = a.w;
+        ss = fmaf(a.x, a.x, fmaf(a.y, a.y, fmaf(a.z, a.z, fmaf(a.w, a.w, ss))));
+      }
+    }
+  } else {
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        v[j0 + q] = (j0 + q < nv) ? src[j0 + q] : 0.f;
-        ss = fmaf(v[j0 + q], v[j0 + q], ss);
+    for (int j0 = 0; j0 < kKHalfMax; j0 += 8) {
+      if (j0 < kh) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          v[j0 + q] = (j0 + q < nv) ? src[j0 + q] : 0.f;
+          ss = fmaf(v[j0 + q], v[j0 + q], ss);
+        }
       }
     }
   }
