@@ -615,21 +615,28 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int col_end = min(col0 + t.zg, t.dout_eff);
       const int nblk = t.zg / 16;
       const int half_lane = lane >> 4, cl = lane & 15;
+      const float s_lo = pow2i(e_row >> 1), s_hi = pow2i(e_row - (e_row >> 1));  // exact 2^e_row, split for range
+      const int64_t stride2 = 2 * static_cast<int64_t>(t.dout_total);
+      const int64_t left = rs.rows - row0 - half_lane;  // rows of this half-lane in the quarter
+      const bool full = left >= 32;
+      const float* sp0 = stage + half_lane * kStageStride + cl;
+      float* op0 = rs.out + (row0 + half_lane) * t.dout_total + col0 + cl;
       for (int cb = h; cb < ((t.dbg & 2) ? 0 : nblk); cb += 2) {
         uint32_t v0[16];
         tmem_ld16(lane_base + cb * 16, v0);
         tmem_wait_ld();
 #pragma unroll
-        for (int qq = 0; qq < 16; ++qq) stage[lane * kStageStride + qq] = mul_pow2(__uint_as_float(v0[qq]), e_row);
+        for (int qq = 0; qq < 16; ++qq) stage[lane * kStageStride + qq] = __uint_as_float(v0[qq]) * s_lo * s_hi;
         __syncwarp();
         // two rows per store instruction: lanes 0-15 row rr, lanes 16-31 row rr + 1
-        const int col = col0 + cb * 16 + cl;
-        if (col < col_end) {
-          float* op = rs.out + (row0 + half_lane) * t.dout_total + col;
-          const int64_t rows_left = rs.rows - row0 - half_lane;
-#pragma unroll 4
-          for (int rr = 0; rr < 32; rr += 2) {
-            if (rr < rows_left) op[static_cast<int64_t>(rr) * t.dout_total] = stage[(rr + half_lane) * kStageStride + cl];
+        if (col0 + cb * 16 + cl < col_end) {
+          float* op = op0 + cb * 16;
+          const float* sp = sp0;
+          if (full) {
+#pragma unroll
+            for (int rr = 0; rr < 32; rr += 2, op += stride2, sp += 2 * kStageStride) *op = *sp;
+          } else {
+            for (int rr = 0; rr < left; rr += 2, op += stride2, sp += 2 * kStageStride) *op = *sp;
           }
         }
         __syncwarp();
