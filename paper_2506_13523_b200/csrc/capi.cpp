@@ -344,10 +344,24 @@ int tpo_run_host_f32(tpo_ctx* ctx, int kind, int L1, int L2, int L3, int l_tilde
       dz[b] = c.scratch(3 * b + 2, static_cast<size_t>(bc * channels * dout));
     }
     const cudaStream_t si = c.h2d_stream(), sc = c.host_stream(), so = c.d2h_stream();
+    // optional (TPO_HOST_RAMP=1) chunk ramp bc/8 .. bc .. bc/8 to shorten the unoverlapped first
+    // copy-in / last copy-out; measured slower than uniform chunks (more per-chunk overhead)
+    static const bool ramp = [] {
+      const char* v = std::getenv("TPO_HOST_RAMP");
+      return v && *v == '1';
+    }();
+    const int64_t bmin = std::max<int64_t>(1, bc / 8);
+    auto next_chunk = [&](int64_t b0, int64_t k) {
+      const int64_t left = batch - b0;
+      if (!ramp) return std::min(bc, left);
+      int64_t sz = std::min(bc, bmin << std::min<int64_t>(k, 3));  // ramp up
+      if (left <= 2 * sz) sz = std::max(bmin, (left + 1) / 2);     // ramp down
+      return std::min(sz, left);
+    };
     int64_t k = 0;
-    for (int64_t b0 = 0; b0 < batch; b0 += bc, ++k) {
+    for (int64_t b0 = 0, nbt = 0; b0 < batch; b0 += nbt, ++k) {
       const int b = static_cast<int>(k % nb);
-      const int64_t nbt = std::min(bc, batch - b0);
+      nbt = next_chunk(b0, k);
       const int64_t r0 = b0 * channels, nr = nbt * channels;
       const int64_t yr0 = y_shared ? b0 : r0, ynr = y_shared ? nbt : nr;
       if (k >= nb) cuda_check_s(cudaStreamWaitEvent(si, c.pipe_event(2, b), 0), "wait d2h");
