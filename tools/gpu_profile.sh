@@ -18,5 +18,7 @@ timeout -s KILL 300 ncu --set full --clock-control none --import-source on -k re
   -o gpurun_out/$TAG/fourier_L6 python tools/profile_kernel.py --kind gtp_fourier --L 6 > gpurun_out/$TAG/ncu_fourier.log 2>&1
 timeout -s KILL 300 ncu --set full --clock-control none --import-source on -k regex:mtp -s 2 -c 1 \
   -o gpurun_out/$TAG/mtp_L6 python tools/profile_kernel.py --kind mtp --L 6 > gpurun_out/$TAG/ncu_mtp.log 2>&1
+timeout -s KILL 300 ncu --set full --clock-control none --import-source on -k regex:cgtp_tc -s 2 -c 1 \
+  -o gpurun_out/$TAG/cgtp_L6 python tools/profile_kernel.py --kind cgtp --L 6 > gpurun_out/$TAG/ncu_cgtp_L6.log 2>&1
 fi
 ls -la gpurun_out/$TAG
