@@ -129,7 +129,9 @@ __device__ __forceinline__ uint32_t pack_half2(float a, float b) {
 // scaled by 2^-e with ||row||_2 * 2^-e in [0.5, 1).  Thread (r, h) owns half
 // h of row r.  Two phases separated by a worker barrier, so the raw rows may
 // alias the destination (in-place mode).
-__device__ __noinline__ void convert_input(const float* raw, int din, int kp, uint8_t* dst_hi, uint8_t* dst_lo,
+// in-place staging (raw rows share the operand buffers): every value is read into registers
+// before the barrier, so no thread overwrites a raw value another thread has yet to read
+__device__ __noinline__ void convert_input_regs(const float* raw, int din, int kp, uint8_t* dst_hi, uint8_t* dst_lo,
                                               float* part, int* e_out, int r, int h, bool wait_free,
                                               uint64_t* xy_free, uint32_t xy_free_par) {
   const int kh = kp >> 1;  // multiple of 8
@@ -186,6 +188,68 @@ __device__ __noinline__ void convert_input(const float* raw, int din, int kp, ui
       *reinterpret_cast<uint4*>(dst_hi + off) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
       *reinterpret_cast<uint4*>(dst_lo + off) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
     }
+  }
+  if (h == 0) e_out[r] = e;
+}
+
+__device__ __noinline__ void convert_input(const float* raw, int din, int kp, uint8_t* dst_hi, uint8_t* dst_lo,
+                                              float* part, int* e_out, int r, int h, bool wait_free,
+                                              uint64_t* xy_free, uint32_t xy_free_par) {
+  // two short passes over the staged row (norm, then scale + split): small code, which
+  // matters because this runs once per tile and is otherwise cold in the instruction cache
+  const int kh = kp >> 1;  // multiple of 8
+  const int k0 = h * kh;
+  const float* src = raw + r * din + k0;
+  const int nv = min(kh, din - k0);  // valid raw values of this half (may be <= 0)
+  // rows of a multiple of 4 floats sit a multiple of 16 B apart: 128-bit reads (a scalar read of
+  // the same k by 32 rows would hit one bank up to 32-fold, e.g. din = 64)
+  const bool vec = (din & 3) == 0;
+  auto load8 = [&](int j0, float (&v)[8]) {
+    if (vec) {
+      const float4* s4 = reinterpret_cast<const float4*>(src + j0);
+      const float4 a = j0 < nv ? s4[0] : make_float4(0.f, 0.f, 0.f, 0.f);
+      const float4 b = j0 + 4 < nv ? s4[1] : make_float4(0.f, 0.f, 0.f, 0.f);
+      v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+    } else {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) v[q] = j0 + q < nv ? src[j0 + q] : 0.f;
+    }
+  };
+  float ss0 = 0.f, ss1 = 0.f;
+#pragma unroll 1
+  for (int j0 = 0; j0 < kh; j0 += 8) {
+    float v[8];
+    load8(j0, v);
+#pragma unroll
+    for (int q = 0; q < 8; q += 2) {
+      ss0 = fmaf(v[q], v[q], ss0);
+      ss1 = fmaf(v[q + 1], v[q + 1], ss1);
+    }
+  }
+  part[h * BM + r] = ss0 + ss1;
+  named_bar_sync(1, kWorkers);
+  if (wait_free) mbar_wait(xy_free, xy_free_par);  // the previous unit's GEMM 1 has retired
+  const float tot = part[r] + part[BM + r];
+  int e = 0;
+  if (tot > 0.f && tot < 3.0e38f) e = max(-120, min(120, ilogbf(tot) / 2 + 1));
+  // |x| * 2^-e <= 2: fp16 hi/lo stay normal for the row's dominant entries
+  const float sc = pow2i(-e);
+#pragma unroll 1
+  for (int j0 = 0; j0 < kh; j0 += 8) {
+    float v[8];
+    load8(j0, v);
+    uint32_t hw[4], lw[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float a0 = v[2 * q] * sc, a1 = v[2 * q + 1] * sc;
+      const __half2 hh = __floats2half2_rn(a0, a1);
+      const float2 hf = __half22float2(hh);
+      hw[q] = *reinterpret_cast<const uint32_t*>(&hh);
+      lw[q] = pack_half2(a0 - hf.x, a1 - hf.y);
+    }
+    const uint32_t off = canon_off(r, k0 + j0, BM);
+    *reinterpret_cast<uint4*>(dst_hi + off) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+    *reinterpret_cast<uint4*>(dst_lo + off) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
   }
   if (h == 0) e_out[r] = e;
 }
@@ -546,9 +610,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (wait_free) mbar_wait(&bars[B_XY_FREE], par);
         if (!t.raw_inplace) mbar_arrive(&bars[B_RAW_FREE]);
       } else if (t.raw_inplace) {
-        convert_input(raw_x, t.din1, t.k1p, xh, xl, part_sh, ex_sh[buf], r, h, wait_free, &bars[B_XY_FREE], par);
+        convert_input_regs(raw_x, t.din1, t.k1p, xh, xl, part_sh, ex_sh[buf], r, h, wait_free, &bars[B_XY_FREE], par);
         named_bar_sync(1, kWorkers);
-        convert_input(raw_y, t.din2, t.k2p, yh, yl, part_sh, ey_sh[buf], r, h, false, &bars[B_XY_FREE], par);
+        convert_input_regs(raw_y, t.din2, t.k2p, yh, yl, part_sh, ey_sh[buf], r, h, false, &bars[B_XY_FREE], par);
       } else {
         // both inputs are read before the raw buffer is handed back to the producer
         convert_input(raw_x, t.din1, t.k1p, xh, xl, part_sh, ex_sh[buf], r, h, wait_free, &bars[B_XY_FREE], par);
