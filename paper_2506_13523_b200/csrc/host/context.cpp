@@ -230,8 +230,11 @@ GridTcEntry Context::build_dense_tc(const DenseOps& ops, const char* label) {
   int best_g = 0, best_nc = 0, best_chunks = 0, best_zg = 0;
   for (int ng = 1; ng <= 8; ++ng) {
     if (force_groups && ng != force_groups) continue;
-    const int zg = pad_to((t.dout_eff + ng - 1) / ng, 16);
-    if (zg > 256) continue;
+    // a group wider than one MMA (N <= 256) is split into GEMM-2 parts; wide single groups
+    // avoid recomputing GEMM 1 per group at the price of narrower grid chunks
+    int zg = pad_to((t.dout_eff + ng - 1) / ng, 16);
+    if (zg > 256) zg = pad_to(zg, 32);
+    if (zg > env_int("TPO_GRID_ZG_MAX", 448)) continue;
     for (int cand = 128; cand >= 16; cand -= 16) {
       if (force_nc && cand != force_nc) continue;
       if (zg + 2 * cand > 512) continue;
