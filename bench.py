@@ -336,22 +336,35 @@ def main():
         ho = {L: torch.empty(outs[L].shape, pin_memory=True) for L in LS}
         lib = tpo.lib()
 
-        def e2e_step():
+        def e2e_step_per_call():  # one synchronous tpo_run_host_f32 per L
             for L in LS:
                 tpo.check(lib.tpo_run_host_f32(ctx.handle, tpo.KINDS["gtp_grid"], L, L, 2 * L, -1,
                                                hx[L].data_ptr(), hy[L].data_ptr(), ho[L].data_ptr(), B, 1, 0))
 
-        for _ in range(2):
-            e2e_step()
+        reqs = [("gtp_grid", hx[L], hy[L], ho[L], L, L, 2 * L) for L in LS]
+
+        def e2e_step_batch():  # the sweep's 10 requests in one tpo_run_host_batch_f32 call
+            tpo.run_host_batch(reqs, local)
+
         n_e2e = max(2, min(args.steps, 5))
-        t0 = time.perf_counter()
-        for _ in range(n_e2e):
-            e2e_step()
-        et = max_over_ranks((time.perf_counter() - t0) / n_e2e, dev)
+
+        def timed(fn):
+            for _ in range(2):
+                fn()
+            t0 = time.perf_counter()
+            for _ in range(n_e2e):
+                fn()
+            return max_over_ranks((time.perf_counter() - t0) / n_e2e, dev)
+
+        et_call = timed(e2e_step_per_call)
+        et = timed(e2e_step_batch)
         e2e = {"value": round(world * len(LS) * B / et, 1), "unit": UNIT,
                "h2d_bytes_per_step": int(sum(2 * B * (L + 1) ** 2 * 4 for L in LS)),
                "d2h_bytes_per_step": int(sum(B * (2 * L + 1) ** 2 * 4 for L in LS)),
-               "ms_per_step": round(et * 1e3, 3), "path": "tpo_run_host_f32 (C ABI, pinned host buffers)"}
+               "ms_per_step": round(et * 1e3, 3),
+               "path": "tpo_run_host_batch_f32 (C ABI, pinned host buffers, the 10 requests in one call)",
+               "per_call": {"value": round(world * len(LS) * B / et_call, 1), "ms_per_step": round(et_call * 1e3, 3),
+                            "path": "one tpo_run_host_f32 per L"}}
 
     extras = None
     if not args.no_extras and rank == 0:

@@ -107,6 +107,19 @@ int tpo_run_host_f32(tpo_ctx* ctx, int kind, int L1, int L2, int L3, int l_tilde
                      const float* x_host, const float* y_host, float* out_host, int64_t batch,
                      int64_t channels, int y_shared);
 
+/* Several independent host-buffer requests in one call (serving-style batching of
+ * heterogeneous products): their chunks flow back to back through the same copy-in /
+ * compute / copy-out pipeline, so the pipeline does not drain between requests.
+ * Synchronous; equivalent to n calls of tpo_run_host_f32 (same results). */
+typedef struct tpo_host_request {
+  int kind, L1, L2, L3, l_tilde, y_shared;
+  int64_t batch, channels;
+  const float* x;
+  const float* y;
+  float* out;
+} tpo_host_request;
+int tpo_run_host_batch_f32(tpo_ctx* ctx, const tpo_host_request* reqs, int n);
+
 /* Table introspection ------------------------------------------------------
  * Real-basis CG table of (l1,l2)->l3 as the device kernels use it (mirrors
  * tpo::cg_real, proj/include/tpo/wigner.hpp:59-64, and the pybind

@@ -19,7 +19,7 @@ module lives in :mod:`paper_2506_13523_b200.so3tpo`.
 """
 from __future__ import annotations
 
-from ._lib import KINDS, Context, TpoError, check, context, lib
+from ._lib import KINDS, Context, HostRequest, TpoError, check, context, lib
 
 __all__ = [
     "cgtp", "gtp_grid", "gtp_fourier", "mtp", "weighted_gtp", "run", "out_dim", "tower_dim",
@@ -93,6 +93,36 @@ def run(kind: str, x, y, L1: int, L2: int, L3: int = 0, l_tilde: int = -1, out=N
     check(lib().tpo_run_f32(ctx.handle, KINDS[kind], L1, L2, L3, l_tilde, x.data_ptr(), y.data_ptr(),
                             o.data_ptr(), B, C, ys, stream))
     return o
+
+
+def run_host_batch(requests, device: int = 0):
+    """Several independent products with HOST tensors in one synchronous call
+    (tpo_run_host_batch_f32): each request is (kind, x, y, out, L1, L2, L3[, l_tilde])
+    with contiguous fp32 CPU tensors (pinned for full copy/compute overlap), x
+    [B, Din] or [B, C, Din], y [B, Din2] (shared per b when x has channels) or like x,
+    out preallocated.  Results equal one tpo_run_host_f32 call per request."""
+    import ctypes as C
+
+    import torch
+
+    reqs = (HostRequest * len(requests))()
+    keep = []
+    for i, r in enumerate(requests):
+        kind, x, y, out, L1, L2, L3 = r[:7]
+        lt = r[7] if len(r) > 7 else -1
+        for t in (x, y, out):
+            if t.device.type != "cpu" or not t.is_contiguous() or t.dtype != torch.float32:
+                raise ValueError("run_host_batch: host tensors must be contiguous fp32 on the CPU")
+        B = x.shape[0]
+        Cn = x.shape[1] if x.dim() == 3 else 1
+        ys = 1 if (x.dim() == 3 and y.dim() == 2) else 0
+        q = reqs[i]
+        q.kind, q.L1, q.L2, q.L3, q.l_tilde, q.y_shared = KINDS[kind], L1, L2, L3, lt, ys
+        q.batch, q.channels = B, Cn
+        q.x, q.y, q.out = x.data_ptr(), y.data_ptr(), out.data_ptr()
+        keep.append((x, y, out))
+    check(lib().tpo_run_host_batch_f32(context(device).handle, C.cast(reqs, C.c_void_p), len(requests)))
+    return [k[2] for k in keep]
 
 
 def cgtp(x, y, L1: int, L2: int, out=None):

@@ -22,6 +22,14 @@ KIND_CGTP, KIND_GTP_GRID, KIND_GTP_FOURIER, KIND_MTP = 0, 1, 2, 3
 KINDS = {"cgtp": KIND_CGTP, "gtp_grid": KIND_GTP_GRID, "gtp_fourier": KIND_GTP_FOURIER, "mtp": KIND_MTP}
 
 
+class HostRequest(C.Structure):
+    """Mirror of tpo_host_request (include/tpo_capi.h)."""
+
+    _fields_ = [("kind", C.c_int), ("L1", C.c_int), ("L2", C.c_int), ("L3", C.c_int), ("l_tilde", C.c_int),
+                ("y_shared", C.c_int), ("batch", C.c_int64), ("channels", C.c_int64), ("x", C.c_void_p),
+                ("y", C.c_void_p), ("out", C.c_void_p)]
+
+
 class TpoError(RuntimeError):
     """CUDA / runtime failure inside libtpo_b200 (TPO_ECUDA, TPO_ERUNTIME)."""
 
@@ -60,6 +68,7 @@ def lib():
             "tpo_weighted_gtp_f32": (i, [p, i, i, i, p, p, p, p, p, p, i64, i64, i, p]),
             "tpo_run_f32": (i, [p, i, i, i, i, i, p, p, p, i64, i64, i, p]),
             "tpo_run_host_f32": (i, [p, i, i, i, i, i, p, p, p, i64, i64, i]),
+            "tpo_run_host_batch_f32": (i, [p, p, i]),
             "tpo_set_gtp_grid_path": (i, [p, i]),
             "tpo_cg_real": (i, [i, i, i, p, p, p, p, i]),
             "tpo_fourier_table": (i, [i, i, p, p, p, p, p, i]),
@@ -77,6 +86,7 @@ EXPORTED = [
     "tpo_last_error", "tpo_version", "tpo_ctx_create", "tpo_ctx_destroy", "tpo_ctx_launches",
     "tpo_tower_dim", "tpo_out_dim", "tpo_mtp_l_tilde", "tpo_cgtp_mimo_f32", "tpo_gtp_grid_f32",
     "tpo_gtp_fourier_f32", "tpo_mtp_f32", "tpo_weighted_gtp_f32", "tpo_run_f32", "tpo_run_host_f32",
+    "tpo_run_host_batch_f32",
     "tpo_set_gtp_grid_path", "tpo_last_gtp_grid_path", "tpo_cg_real", "tpo_fourier_table",
 ]
 

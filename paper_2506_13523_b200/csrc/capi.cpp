@@ -310,78 +310,123 @@ namespace {
 void cuda_check_s(cudaError_t e, const char* what) { tpo_b200::cuda_check(e, what); }
 }  // namespace
 
-int tpo_run_host_f32(tpo_ctx* ctx, int kind, int L1, int L2, int L3, int l_tilde, const float* x_host,
-                     const float* y_host, float* out_host, int64_t batch, int64_t channels, int y_shared) {
-  // Host buffers in, host buffers out, synchronous like the reference's call.
-  // The batch is cut into chunks that flow through three streams (copy-in,
-  // compute, copy-out) and kPipeBufs device buffer sets, so both PCIe
-  // directions and the kernels overlap (full overlap needs pinned host memory;
-  // pageable buffers still work, the copies are then staged by the driver).
-  return guarded([&] {
-    check_args(ctx, L1, L2, x_host, y_host, out_host, batch, channels);
-    const int64_t dout = out_dim(kind, L1, L2, L3);
-    Context& c = ctx->impl;
-    c.activate();
-    const int64_t rows = batch * channels;
-    if (rows == 0) return;
-    std::lock_guard<std::mutex> lk(c.host_path_mutex());
-    const int64_t d1 = (L1 + 1) * (L1 + 1), d2 = (L2 + 1) * (L2 + 1);
-    // chunk = whole batch entries (y_shared rows stay with their channels), ~8 MiB of traffic
-    const int64_t bytes_per_b = 4 * channels * (d1 + dout + (y_shared ? 0 : d2)) + (y_shared ? 4 * d2 : 0);
-    static const int64_t chunk_bytes = [] {
-      const char* v = std::getenv("TPO_HOST_CHUNK_KB");
-      return (v && *v) ? std::atoll(v) * 1024 : (16ll << 20);  // measured best: 8-16 MiB (tools/e2e_chunks.py)
-    }();
-    int64_t bc = std::max<int64_t>(1, chunk_bytes / std::max<int64_t>(bytes_per_b, 1));
-    bc = std::min(bc, batch);
-    const int nb = Context::kPipeBufs;
-    float* dx[Context::kPipeBufs];
-    float* dy[Context::kPipeBufs];
-    float* dz[Context::kPipeBufs];
-    for (int b = 0; b < nb; ++b) {
-      dx[b] = c.scratch(3 * b + 0, static_cast<size_t>(bc * channels * d1));
-      dy[b] = c.scratch(3 * b + 1, static_cast<size_t>(bc * (y_shared ? 1 : channels) * d2));
-      dz[b] = c.scratch(3 * b + 2, static_cast<size_t>(bc * channels * dout));
-    }
-    const cudaStream_t si = c.h2d_stream(), sc = c.host_stream(), so = c.d2h_stream();
-    // optional (TPO_HOST_RAMP=1) chunk ramp bc/8 .. bc .. bc/8 to shorten the unoverlapped first
-    // copy-in / last copy-out; measured slower than uniform chunks (more per-chunk overhead)
-    static const bool ramp = [] {
-      const char* v = std::getenv("TPO_HOST_RAMP");
-      return v && *v == '1';
-    }();
-    const int64_t bmin = std::max<int64_t>(1, bc / 8);
-    auto next_chunk = [&](int64_t b0, int64_t k) {
-      const int64_t left = batch - b0;
+namespace {
+// Host buffers in, host buffers out, synchronous like the reference's call.  Each
+// request's batch is cut into chunks that flow through three streams (copy-in,
+// compute, copy-out) and kPipeBufs device buffer sets, so both PCIe directions and
+// the kernels overlap (full overlap needs pinned host memory; pageable buffers still
+// work, the copies are then staged by the driver).  Consecutive requests share the
+// pipeline: it drains once, at the end.
+void run_host_requests(tpo_ctx* ctx, const tpo_host_request* reqs, int n) {
+  if (n < 0 || (n > 0 && !reqs)) throw InvalidArgument("tpo_run_host_batch: bad request list");
+  struct Plan {
+    int64_t d1, d2, dout, bc;
+  };
+  std::vector<Plan> plan(static_cast<size_t>(n));
+  static const int64_t chunk_bytes = [] {
+    const char* v = std::getenv("TPO_HOST_CHUNK_KB");
+    return (v && *v) ? std::atoll(v) * 1024 : (16ll << 20);  // measured best: 8-16 MiB (tools/e2e_chunks.py)
+  }();
+  size_t need_x = 1, need_y = 1, need_z = 1;
+  for (int i = 0; i < n; ++i) {
+    const tpo_host_request& q = reqs[i];
+    check_args(ctx, q.L1, q.L2, q.x, q.y, q.out, q.batch, q.channels);
+    Plan& pl = plan[static_cast<size_t>(i)];
+    pl.dout = out_dim(q.kind, q.L1, q.L2, q.L3);
+    pl.d1 = (q.L1 + 1) * (q.L1 + 1);
+    pl.d2 = (q.L2 + 1) * (q.L2 + 1);
+    // chunk = whole batch entries (y_shared rows stay with their channels), ~16 MiB of traffic
+    const int64_t bytes_per_b =
+        4 * q.channels * (pl.d1 + pl.dout + (q.y_shared ? 0 : pl.d2)) + (q.y_shared ? 4 * pl.d2 : 0);
+    pl.bc = std::min<int64_t>(std::max<int64_t>(1, chunk_bytes / std::max<int64_t>(bytes_per_b, 1)),
+                              std::max<int64_t>(q.batch, 1));
+    need_x = std::max(need_x, static_cast<size_t>(pl.bc * q.channels * pl.d1));
+    need_y = std::max(need_y, static_cast<size_t>(pl.bc * (q.y_shared ? 1 : q.channels) * pl.d2));
+    need_z = std::max(need_z, static_cast<size_t>(pl.bc * q.channels * pl.dout));
+  }
+  Context& c = ctx->impl;
+  c.activate();
+  std::lock_guard<std::mutex> lk(c.host_path_mutex());
+  const int nb = Context::kPipeBufs;
+  float* dx[Context::kPipeBufs];
+  float* dy[Context::kPipeBufs];
+  float* dz[Context::kPipeBufs];
+  for (int b = 0; b < nb; ++b) {
+    dx[b] = c.scratch(3 * b + 0, need_x);
+    dy[b] = c.scratch(3 * b + 1, need_y);
+    dz[b] = c.scratch(3 * b + 2, need_z);
+  }
+  const cudaStream_t si = c.h2d_stream(), sc = c.host_stream(), so = c.d2h_stream();
+  // optional (TPO_HOST_RAMP=1) chunk ramp bc/8 .. bc .. bc/8 to shorten the unoverlapped first
+  // copy-in / last copy-out; measured slower than uniform chunks (more per-chunk overhead)
+  static const bool ramp = [] {
+    const char* v = std::getenv("TPO_HOST_RAMP");
+    return v && *v == '1';
+  }();
+  int64_t k = 0;  // chunk counter over all requests (buffer rotation)
+  for (int i = 0; i < n; ++i) {
+    const tpo_host_request& q = reqs[i];
+    const Plan& pl = plan[static_cast<size_t>(i)];
+    const int64_t rows = q.batch * q.channels;
+    if (rows == 0) continue;
+    const int64_t bc = pl.bc, bmin = std::max<int64_t>(1, bc / 8);
+    auto next_chunk = [&](int64_t b0, int64_t kk) {
+      const int64_t left = q.batch - b0;
       if (!ramp) return std::min(bc, left);
-      int64_t sz = std::min(bc, bmin << std::min<int64_t>(k, 3));  // ramp up
-      if (left <= 2 * sz) sz = std::max(bmin, (left + 1) / 2);     // ramp down
+      int64_t sz = std::min(bc, bmin << std::min<int64_t>(kk, 3));  // ramp up
+      if (left <= 2 * sz) sz = std::max(bmin, (left + 1) / 2);      // ramp down
       return std::min(sz, left);
     };
-    int64_t k = 0;
-    for (int64_t b0 = 0, nbt = 0; b0 < batch; b0 += nbt, ++k) {
+    int64_t kk = 0;
+    for (int64_t b0 = 0, nbt = 0; b0 < q.batch; b0 += nbt, ++k, ++kk) {
       const int b = static_cast<int>(k % nb);
-      nbt = next_chunk(b0, k);
-      const int64_t r0 = b0 * channels, nr = nbt * channels;
-      const int64_t yr0 = y_shared ? b0 : r0, ynr = y_shared ? nbt : nr;
+      nbt = next_chunk(b0, kk);
+      const int64_t r0 = b0 * q.channels, nr = nbt * q.channels;
+      const int64_t yr0 = q.y_shared ? b0 : r0, ynr = q.y_shared ? nbt : nr;
       if (k >= nb) cuda_check_s(cudaStreamWaitEvent(si, c.pipe_event(2, b), 0), "wait d2h");
-      cuda_check_s(cudaMemcpyAsync(dx[b], x_host + r0 * d1, nr * d1 * sizeof(float), cudaMemcpyHostToDevice, si),
+      cuda_check_s(cudaMemcpyAsync(dx[b], q.x + r0 * pl.d1, nr * pl.d1 * sizeof(float), cudaMemcpyHostToDevice, si),
                    "H2D x");
-      cuda_check_s(cudaMemcpyAsync(dy[b], y_host + yr0 * d2, ynr * d2 * sizeof(float), cudaMemcpyHostToDevice, si),
-                   "H2D y");
+      cuda_check_s(
+          cudaMemcpyAsync(dy[b], q.y + yr0 * pl.d2, ynr * pl.d2 * sizeof(float), cudaMemcpyHostToDevice, si),
+          "H2D y");
       cuda_check_s(cudaEventRecord(c.pipe_event(0, b), si), "record h2d");
       cuda_check_s(cudaStreamWaitEvent(sc, c.pipe_event(0, b), 0), "wait h2d");
-      run_kind(ctx, kind, L1, L2, L3, l_tilde, dx[b], dy[b], dz[b], nbt, channels, y_shared, sc);
+      run_kind(ctx, q.kind, q.L1, q.L2, q.L3, q.l_tilde, dx[b], dy[b], dz[b], nbt, q.channels, q.y_shared, sc);
       cuda_check_s(cudaEventRecord(c.pipe_event(1, b), sc), "record compute");
       cuda_check_s(cudaStreamWaitEvent(so, c.pipe_event(1, b), 0), "wait compute");
-      cuda_check_s(cudaMemcpyAsync(out_host + r0 * dout, dz[b], nr * dout * sizeof(float), cudaMemcpyDeviceToHost, so),
+      cuda_check_s(cudaMemcpyAsync(q.out + r0 * pl.dout, dz[b], nr * pl.dout * sizeof(float),
+                                   cudaMemcpyDeviceToHost, so),
                    "D2H");
       cuda_check_s(cudaEventRecord(c.pipe_event(2, b), so), "record d2h");
     }
-    cuda_check_s(cudaStreamSynchronize(so), "sync");
-    cuda_check_s(cudaStreamSynchronize(sc), "sync");
-    cuda_check_s(cudaStreamSynchronize(si), "sync");
+  }
+  cuda_check_s(cudaStreamSynchronize(so), "sync");
+  cuda_check_s(cudaStreamSynchronize(sc), "sync");
+  cuda_check_s(cudaStreamSynchronize(si), "sync");
+}
+}  // namespace
+
+int tpo_run_host_f32(tpo_ctx* ctx, int kind, int L1, int L2, int L3, int l_tilde, const float* x_host,
+                     const float* y_host, float* out_host, int64_t batch, int64_t channels, int y_shared) {
+  return guarded([&] {
+    tpo_host_request q{};
+    q.kind = kind;
+    q.L1 = L1;
+    q.L2 = L2;
+    q.L3 = L3;
+    q.l_tilde = l_tilde;
+    q.y_shared = y_shared;
+    q.batch = batch;
+    q.channels = channels;
+    q.x = x_host;
+    q.y = y_host;
+    q.out = out_host;
+    run_host_requests(ctx, &q, 1);
   });
+}
+
+int tpo_run_host_batch_f32(tpo_ctx* ctx, const tpo_host_request* reqs, int n) {
+  return guarded([&] { run_host_requests(ctx, reqs, n); });
 }
 
 int tpo_cg_real(int l1, int l2, int l3, int* m1, int* m2, int* m3, double* value, int cap) {

@@ -440,3 +440,26 @@ print(worst)
     r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=240, env=env)
     assert r.returncode == 0, r.stderr[-2000:]
     assert float(r.stdout.strip().splitlines()[-1]) <= TOL
+
+
+def test_host_batch_api(tpo, orc):
+    # tpo_run_host_batch_f32: heterogeneous requests through one pipeline == one call each
+    import torch
+
+    reqs, singles = [], []
+    for kind, L, B, C, shared in (("gtp_grid", 3, 3000, None, False), ("mtp", 2, 700, None, False),
+                                  ("cgtp", 2, 40, 24, True), ("gtp_fourier", 1, 5000, None, False),
+                                  ("cgtp", 6, 300, None, False)):
+        x, y = _inputs(B, L, L, 990 + L, C=C, shared=shared)
+        xt, yt = torch.from_numpy(x).pin_memory(), torch.from_numpy(y).pin_memory()
+        L3 = 0 if kind == "cgtp" else 2 * L
+        dout = tpo.out_dim(kind, L, L, L3)
+        o = torch.empty(((B, dout) if C is None else (B, C, dout)), pin_memory=True)
+        reqs.append((kind, xt, yt, o, L, L, L3))
+        singles.append((kind, xt, yt, L, L3, C is not None and shared))
+    outs = tpo.run_host_batch(reqs)
+    for (kind, xt, yt, L, L3, ys), o in zip(singles, outs):
+        ref = tpo.run(kind, xt.cuda(), yt.cuda(), L, L, L3).cpu()
+        assert torch.equal(o, ref), kind
+    # empty list and empty batch are fine
+    tpo.run_host_batch([])
