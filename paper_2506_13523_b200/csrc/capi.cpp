@@ -282,6 +282,24 @@ int tpo_weighted_gtp_f32(tpo_ctx* ctx, int L1, int L2, int L3, const double* a, 
     const cudaStream_t s = static_cast<cudaStream_t>(stream);
     const int64_t rows = batch * channels;
     if (rows == 0) return;
+    // tcgen05 path: the weights ride in the kernel parameters, applied in the input
+    // conversion and the epilogue (no extra passes, no temporaries)
+    Context& c0 = ctx->impl;
+    if (c0.grid_path != 2 && L1 <= 16 && L2 <= 16 && L3 <= 32) {
+      const auto& e = c0.grid_tc(L1, L2, L3);
+      if (e.fits) {
+        tpo_b200::DegreeWeights dw{};
+        dw.on = 1;
+        for (int i = 0; i <= L1; ++i) dw.a[i] = static_cast<float>(a[i]);
+        for (int i = 0; i <= L2; ++i) dw.b[i] = static_cast<float>(b[i]);
+        for (int i = 0; i <= L3; ++i) dw.c[i] = static_cast<float>(c[i]);
+        c0.last_grid_path = 1;
+        launched(ctx, tpo_b200::launch_gtp_grid_tc(e.t, rows_of(x, y, out, batch, channels, y_shared), c0.num_sms(), s,
+                                                   &dw),
+                 "weighted gtp_grid tcgen05 kernel");
+        return;
+      }
+    }
     const int64_t yrows = y_shared ? batch : rows;
     const int64_t d1 = (L1 + 1) * (L1 + 1), d2 = (L2 + 1) * (L2 + 1);
     float *xs = nullptr, *ys = nullptr, *wd = nullptr;

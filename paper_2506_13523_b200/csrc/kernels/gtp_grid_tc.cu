@@ -113,6 +113,8 @@ __device__ __forceinline__ bool tile_tma_ok(const RowSpec& rs, int64_t tile) {
 
 // 2^k for |k| <= 126, exact (exponent bits)
 __device__ __forceinline__ float pow2i(int k) { return __int_as_float((127 + k) << 23); }
+// degree of flat index k = l^2 + m + l (exact for k < 2^20)
+__device__ __forceinline__ int degree_of(int k) { return __float2int_rd(sqrtf(static_cast<float>(k) + 0.5f)); }
 // v * 2^k, exact for |k| <= 252 unless the result itself is subnormal
 __device__ __forceinline__ float mul_pow2(float v, int k) {
   const int k1 = k >> 1;
@@ -131,9 +133,9 @@ __device__ __forceinline__ uint32_t pack_half2(float a, float b) {
 // alias the destination (in-place mode).
 // in-place staging (raw rows share the operand buffers): every value is read into registers
 // before the barrier, so no thread overwrites a raw value another thread has yet to read
-__device__ __noinline__ void convert_input_regs(const float* raw, int din, int kp, uint8_t* dst_hi, uint8_t* dst_lo,
-                                              float* part, int* e_out, int r, int h, bool wait_free,
-                                              uint64_t* xy_free, uint32_t xy_free_par) {
+__device__ __noinline__ void convert_input_regs(const float* raw, const float* wdeg, int din, int kp, uint8_t* dst_hi,
+                                                   uint8_t* dst_lo, float* part, int* e_out, int r, int h,
+                                                   bool wait_free, uint64_t* xy_free, uint32_t xy_free_par) {
   const int kh = kp >> 1;  // multiple of 8
   const int k0 = h * kh;
   const float* src = raw + r * din + k0;
@@ -149,7 +151,6 @@ __device__ __noinline__ void convert_input_regs(const float* raw, int din, int k
       if (j0 < kh) {
         const float4 a = (j0 < nv) ? src4[j0 >> 2] : make_float4(0.f, 0.f, 0.f, 0.f);
         v[j0] = a.x; v[j0 + 1] = a.y; v[j0 + 2] = a.z; v[j0 + 3] = a.w;
-        ss = fmaf(a.x, a.x, fmaf(a.y, a.y, fmaf(a.z, a.z, fmaf(a.w, a.w, ss))));
       }
     }
   } else {
@@ -159,11 +160,18 @@ __device__ __noinline__ void convert_input_regs(const float* raw, int din, int k
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
           v[j0 + q] = (j0 + q < nv) ? src[j0 + q] : 0.f;
-          ss = fmaf(v[j0 + q], v[j0 + q], ss);
         }
       }
     }
   }
+  if (wdeg) {  // fused per-degree input weights (weighted GTP)
+#pragma unroll
+    for (int j = 0; j < kKHalfMax; ++j)
+      if (j < kh) v[j] *= wdeg[k0 + j];
+  }
+#pragma unroll
+  for (int j = 0; j < kKHalfMax; ++j)
+    if (j < kh) ss = fmaf(v[j], v[j], ss);
   part[h * BM + r] = ss;
   named_bar_sync(1, kWorkers);
   if (wait_free) mbar_wait(xy_free, xy_free_par);  // the previous unit's GEMM 1 has retired
@@ -192,8 +200,8 @@ __device__ __noinline__ void convert_input_regs(const float* raw, int din, int k
   if (h == 0) e_out[r] = e;
 }
 
-__device__ __noinline__ void convert_input(const float* raw, int din, int kp, uint8_t* dst_hi, uint8_t* dst_lo,
-                                              float* part, int* e_out, int r, int h, bool wait_free,
+__device__ __noinline__ void convert_input(const float* raw, const float* wdeg, int din, int kp, uint8_t* dst_hi,
+                                              uint8_t* dst_lo, float* part, int* e_out, int r, int h, bool wait_free,
                                               uint64_t* xy_free, uint32_t xy_free_par) {
   // two short passes over the staged row (norm, then scale + split): small code, which
   // matters because this runs once per tile and is otherwise cold in the instruction cache
@@ -213,6 +221,10 @@ __device__ __noinline__ void convert_input(const float* raw, int din, int kp, ui
     } else {
 #pragma unroll
       for (int q = 0; q < 8; ++q) v[q] = j0 + q < nv ? src[j0 + q] : 0.f;
+    }
+    if (wdeg) {  // fused per-degree input weights (weighted GTP)
+#pragma unroll
+      for (int q = 0; q < 8; ++q) v[q] *= wdeg[k0 + j0 + q];
     }
   };
   float ss0 = 0.f, ss1 = 0.f;
@@ -271,7 +283,8 @@ __device__ unsigned long long* g_prof = nullptr;
 // forwards "my half landed" to rank 0's ring slots; workers signal rank 0.
 template <bool PROF, bool PAIR>
 __global__ void __launch_bounds__(kThreads, 1)
-    gtp_grid_tc_kernel(const __grid_constant__ GridTcTables t, const __grid_constant__ RowSpec rs) {
+    gtp_grid_tc_kernel(const __grid_constant__ GridTcTables t, const __grid_constant__ RowSpec rs,
+                       const __grid_constant__ DegreeWeights dw) {
   unsigned long long pc[kProfSlots];
 #pragma unroll
   for (int k = 0; k < kProfSlots; ++k) pc[k] = 0;
@@ -282,6 +295,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   __shared__ uint32_t tmem_sh;
   __shared__ int ex_sh[2][BM], ey_sh[2][BM];
   __shared__ float part_sh[2 * BM];
+  // weighted GTP: per-column weights (flat (l,m) index -> weight of degree l), filled once
+  __shared__ float wtab_x[128], wtab_y[128], wtab_c[448];
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t rank = PAIR ? cluster_ctarank() : 0u;
@@ -579,6 +594,18 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_arrive(bar);
       }
     };
+    if (dw.on) {  // fused per-degree weights (weighted GTP): per-column tables, broadcast reads
+      for (int k = wt; k < 448; k += kWorkers) {
+        if (k < 128) {
+          wtab_x[k] = dw.a[min(degree_of(k), 16)];
+          wtab_y[k] = dw.b[min(degree_of(k), 16)];
+        }
+        wtab_c[k] = dw.c[min(degree_of(k), 32)];
+      }
+      named_bar_sync(1, kWorkers);
+    }
+    const float* wx = dw.on ? wtab_x : nullptr;
+    const float* wy = dw.on ? wtab_y : nullptr;
     auto convert = [&](int64_t u, int64_t iu) {
       const Unit cu = unit_of(u, t.ngroups);
       const int buf = static_cast<int>(iu & 1);
@@ -610,14 +637,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (wait_free) mbar_wait(&bars[B_XY_FREE], par);
         if (!t.raw_inplace) mbar_arrive(&bars[B_RAW_FREE]);
       } else if (t.raw_inplace) {
-        convert_input_regs(raw_x, t.din1, t.k1p, xh, xl, part_sh, ex_sh[buf], r, h, wait_free, &bars[B_XY_FREE], par);
+        convert_input_regs(raw_x, wx, t.din1, t.k1p, xh, xl, part_sh, ex_sh[buf], r, h, wait_free, &bars[B_XY_FREE],
+                           par);
         named_bar_sync(1, kWorkers);
-        convert_input_regs(raw_y, t.din2, t.k2p, yh, yl, part_sh, ey_sh[buf], r, h, false, &bars[B_XY_FREE], par);
+        convert_input_regs(raw_y, wy, t.din2, t.k2p, yh, yl, part_sh, ey_sh[buf], r, h, false, &bars[B_XY_FREE], par);
       } else {
         // both inputs are read before the raw buffer is handed back to the producer
-        convert_input(raw_x, t.din1, t.k1p, xh, xl, part_sh, ex_sh[buf], r, h, wait_free, &bars[B_XY_FREE], par);
+        convert_input(raw_x, wx, t.din1, t.k1p, xh, xl, part_sh, ex_sh[buf], r, h, wait_free, &bars[B_XY_FREE], par);
         named_bar_sync(1, kWorkers);
-        convert_input(raw_y, t.din2, t.k2p, yh, yl, part_sh, ey_sh[buf], r, h, false, &bars[B_XY_FREE], par);
+        convert_input(raw_y, wy, t.din2, t.k2p, yh, yl, part_sh, ey_sh[buf], r, h, false, &bars[B_XY_FREE], par);
         mbar_arrive(&bars[B_RAW_FREE]);
       }
       fence_proxy_async_smem();
@@ -696,11 +724,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (col0 + cb * 16 + cl < col_end) {
           float* op = op0 + cb * 16;
           const float* sp = sp0;
+          const float wc = dw.on ? wtab_c[col0 + cb * 16 + cl] : 1.f;  // fused output weights (weighted GTP)
           if (full) {
 #pragma unroll
-            for (int rr = 0; rr < 32; rr += 2, op += stride2, sp += 2 * kStageStride) *op = *sp;
+            for (int rr = 0; rr < 32; rr += 2, op += stride2, sp += 2 * kStageStride) *op = *sp * wc;
           } else {
-            for (int rr = 0; rr < left; rr += 2, op += stride2, sp += 2 * kStageStride) *op = *sp;
+            for (int rr = 0; rr < left; rr += 2, op += stride2, sp += 2 * kStageStride) *op = *sp * wc;
           }
         }
         __syncwarp();
@@ -743,7 +772,10 @@ int gtp_grid_tc_max_smem() {
   return optin - static_cast<int>(a.sharedSizeBytes) - 1024;  // slack for the 1 KB dynamic alignment
 }
 
-cudaError_t launch_gtp_grid_tc(const GridTcTables& t, const RowSpec& rs, int num_sms, cudaStream_t s) {
+cudaError_t launch_gtp_grid_tc(const GridTcTables& t, const RowSpec& rs, int num_sms, cudaStream_t s,
+                               const DegreeWeights* w) {
+  DegreeWeights dw{};
+  if (w) dw = *w;
   if (rs.rows <= 0) return cudaSuccess;
   static const bool prof = [] {
     const char* v = std::getenv("TPO_GRID_PROF");
@@ -774,7 +806,7 @@ cudaError_t launch_gtp_grid_tc(const GridTcTables& t, const RowSpec& rs, int num
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  e = cudaLaunchKernelEx(&cfg, kern, t, rs);
+  e = cudaLaunchKernelEx(&cfg, kern, t, rs, dw);
   if (prof && e == cudaSuccess) {
     std::vector<unsigned long long> h(kProfSlots * grid);
     cudaStreamSynchronize(s);

@@ -101,7 +101,14 @@ struct GridTcTables {
   alignas(64) CUtensorMap tm_s2;
   alignas(64) CUtensorMap tm_a;
 };
-cudaError_t launch_gtp_grid_tc(const GridTcTables& t, const RowSpec& rs, int num_sms, cudaStream_t s);
+// Per-degree weights fused into the grid kernel (weighted GTP, proj/src/gtp.cpp:206-215):
+// x[l,m] *= a[l], y[l,m] *= b[l] in the input conversion, out[l,m] *= c[l] in the epilogue.
+struct DegreeWeights {
+  int on;
+  float a[17], b[17], c[33];
+};
+cudaError_t launch_gtp_grid_tc(const GridTcTables& t, const RowSpec& rs, int num_sms, cudaStream_t s,
+                               const DegreeWeights* w = nullptr);
 int gtp_grid_tc_max_smem();
 
 // ---------------------------------------------------------------- GTP grid, SIMT separable

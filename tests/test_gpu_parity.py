@@ -463,3 +463,30 @@ def test_host_batch_api(tpo, orc):
         assert torch.equal(o, ref), kind
     # empty list and empty batch are fine
     tpo.run_host_batch([])
+
+
+@pytest.mark.parametrize("L,B,C", [(3, 700, None), (7, 300, None), (10, 150, None), (4, 9, 24)])
+def test_weighted_gtp_fused(tpo, orc, L, B, C):
+    # per-degree weights fused into the tcgen05 kernel (input conversion + epilogue): one
+    # launch, parity with the oracle and with the SIMT path (separate scaling passes)
+    import torch
+
+    x, y = _inputs(B, L, L, 770 + L, C=C, shared=C is not None)
+    rng = np.random.default_rng(L)
+    a, b, c = rng.standard_normal(L + 1), rng.standard_normal(L + 1), rng.standard_normal(2 * L + 1)
+    ctx = tpo.context()
+    xt, yt = torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda()
+    n0 = ctx.launches
+    out = tpo.weighted_gtp(xt, yt, a, b, c, L, L, 2 * L).cpu().numpy()
+    assert ctx.launches - n0 == 1 and ctx.last_grid_path == "tcgen05"
+    xs = x.reshape(-1, x.shape[-1]).astype(np.float64)
+    ys = (np.repeat(y, C, axis=0) if C is not None else y).reshape(-1, y.shape[-1]).astype(np.float64)
+    ref = np.stack([orc.weighted_gtp(orc.tower(L), xs[i], orc.tower(L), ys[i], a, b, c, 2 * L)
+                    for i in range(xs.shape[0])])
+    assert _normwise(out.reshape(ref.shape), ref) <= TOL
+    ctx.set_grid_path("simt")
+    try:
+        out_s = tpo.weighted_gtp(xt, yt, a, b, c, L, L, 2 * L).cpu().numpy()
+    finally:
+        ctx.set_grid_path("auto")
+    assert _normwise(out_s.reshape(ref.shape), ref) <= TOL
