@@ -86,7 +86,8 @@ void run_cgtp(tpo_ctx* ctx, int L1, int L2, const RowSpec& rs, cudaStream_t s) {
   const auto& t = ctx->impl.cgtp(L1, L2);
   // shared y per edge (config C4): per-edge dense GEMMs on tcgen05 when the shape allows
   const int kp = (t.din1 + 15) / 16 * 16, dout_pad = (t.dout + 15) / 16 * 16;
-  const bool aligned = (reinterpret_cast<uintptr_t>(rs.x) % 16 == 0) && (reinterpret_cast<uintptr_t>(rs.out) % 16 == 0);
+  const bool aligned = (reinterpret_cast<uintptr_t>(rs.x) % 16 == 0) && (reinterpret_cast<uintptr_t>(rs.out) % 16 == 0) &&
+                       (reinterpret_cast<uintptr_t>(rs.y) % 16 == 0) && t.din2 % 4 == 0;  // x / y rows by TMA
   static const bool edge_tc_on = [] {
     const char* v = std::getenv("TPO_CGTP_EDGE_TC");
     return !(v && *v == '0');

@@ -61,7 +61,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __shared__ __align__(8) uint64_t bars[6];
   __shared__ uint32_t tmem_sh;
   __shared__ int ex_sh[2][BM];
-  __shared__ float ys_sh[64];
+  __shared__ __align__(16) float ys_sh[2][64];  // the edge's y, prefetched with the x tile (by unit parity)
   __shared__ int ey_sh[2];
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -97,9 +97,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ===================================================== prep + MMA
     const int r = tid - 128;  // channel row of the unit
     const bool el = (warp == 4) && elect_one_sync();
+    // x tile and the edge's y row (din2 floats; 16 B multiple on this path) land on one barrier
+    const uint32_t ybytes = static_cast<uint32_t>(t.din2) * 4u;
     auto issue_x = [&](int64_t u, int b) {
-      mbar_arrive_expect_tx(&bars[b], xbytes);
+      mbar_arrive_expect_tx(&bars[b], xbytes + ybytes);
       bulk_g2s(raw + b * BM * t.din1, rs.x + u * BM * t.din1, xbytes, &bars[b]);
+      bulk_g2s(ys_sh[b], rs.y + (u / blocks_per_edge) * t.din2, ybytes, &bars[b]);
     };
     if (r == 0) {
       if (blockIdx.x < nunits) issue_x(blockIdx.x, 0);
@@ -111,18 +114,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       // buffers of parity b (X/M operands, row scales, Z) were last used by unit it - 2
       if (it >= 2) mbar_wait(&bars[4 + b], ((it >> 1) - 1) & 1);
       tc_fence_after();
-      const int64_t edge = u / blocks_per_edge;
-      if (r < t.din2) ys_sh[r] = __ldg(rs.y + edge * t.din2 + r);
-      named_bar_sync(1, 128);
+      // ---- x tile and y row landed (prefetched two units ahead)
+      mbar_wait(&bars[b], (it >> 1) & 1);
+      const float* ysb = ys_sh[b];
       if (warp == 4) {
         float ss = 0.f;
-        for (int k = lane; k < t.din2; k += 32) ss = fmaf(ys_sh[k], ys_sh[k], ss);
+        for (int k = lane; k < t.din2; k += 32) ss = fmaf(ysb[k], ysb[k], ss);
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
         if (lane == 0) ey_sh[b] = (ss > 0.f && ss < 3.0e38f) ? max(-120, min(120, ilogbf(ss) / 2 + 1)) : 0;
       }
       // ---- x row r: norm pass and split pass over shared memory (din1 % 4 == 0 on this path)
-      mbar_wait(&bars[b], (it >> 1) & 1);
       const float4* rx4 = reinterpret_cast<const float4*>(raw + b * BM * t.din1 + r * t.din1);
       float ss = 0.f;
       for (int k4 = 0; k4 < t.din1 / 4; ++k4) {
@@ -154,7 +156,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       ex_sh[b][r] = e;
       named_bar_sync(1, 128);  // raw buffer b consumed; ey known
-      if (r == 0 && u + 2 * gridDim.x < nunits) issue_x(u + 2 * gridDim.x, b);
       // ---- M_y^T (B operand, row o, K = i1): thread sums c_t y[i2_t] over the CG terms of its outputs
       const float ysc = pow2i(-ey_sh[b]);
       uint8_t* mh = mh_of(b);
@@ -169,7 +170,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int k = 0; k < nt; ++k) {
             const uint2 tw = __ldg(terms + k * 32);
             const int i1 = static_cast<int>(tw.x & 0xFFFFu), i2 = static_cast<int>(tw.x >> 16);
-            row[i1] += __uint_as_float(tw.y) * ys_sh[i2] * ysc;  // padding terms: coefficient 0
+            row[i1] += __uint_as_float(tw.y) * ysb[i2] * ysc;  // padding terms: coefficient 0
           }
         }
         for (int j0 = 0; j0 < kp; j0 += 8) {
@@ -190,6 +191,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       fence_proxy_async_smem();
       tc_fence_before();
       named_bar_sync(1, 128);
+      // raw x and y of buffer b are consumed (y by the M_y build above): prefetch unit u + 2
+      if (r == 0 && u + 2 * gridDim.x < nunits) issue_x(u + 2 * gridDim.x, b);
       // ---- D[b] = X . M_y (3xFP16), N split into <= 256-column MMAs
       if (warp == 4) {
         tc_fence_after();
