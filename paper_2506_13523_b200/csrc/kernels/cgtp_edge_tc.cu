@@ -27,7 +27,7 @@ constexpr int BM = 128;        // channels per unit == TMEM lanes
 constexpr int kThreads = 256;  // 8 warps: 2 per TMEM lane quarter
 constexpr int kBoxCols = 32;   // epilogue TMA store box: 128 rows x 32 fp32 (128 B rows, 128B swizzle)
 constexpr int kBoxBytes = BM * kBoxCols * 4;
-constexpr int kBoxBufs = 4;
+constexpr int kBoxBufs = 8;
 
 __device__ __forceinline__ float pow2i(int k) { return __int_as_float((127 + k) << 23); }
 __device__ __forceinline__ uint32_t pack_half2(float a, float b) {
