@@ -7,7 +7,7 @@ nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,driver_version --format=csv
 timeout -s KILL 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
   --log-file gpurun_out/$TAG/launches.csv python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-extras --no-graph \
   > gpurun_out/$TAG/bench_under_ncu.log 2>&1
-for L in ${GRID_LS:-10 6 1}; do
+for L in ${GRID_LS:-10 8 6 1}; do
   timeout -s KILL 300 ncu --set full --clock-control none --import-source on -k regex:gtp_grid -s 2 -c 1 \
     -o gpurun_out/$TAG/grid_L$L python tools/profile_kernel.py --kind gtp_grid --L $L > gpurun_out/$TAG/ncu_grid_L$L.log 2>&1
 done
