@@ -439,10 +439,10 @@ def side_measurements(tpo, dev, stream, flush, peaks):
             roof = max(byts / hbm, fl / tc_peak)
             bound = "tensor (dense S2-grid operators, 3xFP16)"
         elif kind == "gtp_fourier":
-            N = 4 * L + 1
-            fl = 2 * N * N * (2 * din + dout) * B
+            N = 4 * L + 2  # torus points per axis; antipodal pairs folded: N^2 / 2 points
+            fl = 2 * (N * N // 2) * (2 * din + dout) * B
             roof = max(byts / hbm, fl / tc_peak)
-            bound = "tensor (dense torus-grid operators, 3xFP16)"
+            bound = "tensor (dense torus operators on the N^2/2 antipodal-pair points, 3xFP16)"
         else:
             fl = 2 * 6378 * B  # 2 x reference sparse muls
             roof = max(byts / hbm, fl / fp32)

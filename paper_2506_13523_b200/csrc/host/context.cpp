@@ -461,16 +461,23 @@ const GridTcEntry& Context::grid_tc(int L1, int L2, int L3) {
 //   S[(a,b)][k] = Re sum_{(u,v,w) in enc_k} w w_N^(u a + v b),   w_N = exp(2 pi i / N)
 //   A[o][(a,b)] = Re sum_{(U,V,w) in dec_o} w w_N^-(U a + V b) / N^2
 const GridTcEntry& Context::fourier_tc(int L1, int L2, int L3) {
+  // Torus of N = 4L + 2 points per axis (the reference's n, proj/src/gtp.cpp:58): the
+  // product band 4L < N, so the cyclic convolution is exact.  The antipodal extension
+  // (proj/src/gtp.cpp:66-74) makes every torus function of a sphere input satisfy
+  // g(2 pi - theta, phi + pi) = g(theta, phi); with N even that pairs grid point
+  // (a, b) with (N - a, b + N/2) (no fixed points), and the pointwise product keeps the
+  // symmetry.  So both dense operators need one point per pair: S rows at the
+  // representatives b < N/2, A columns summed over each pair -- G = N^2 / 2.
   std::lock_guard<std::mutex> g(mu_);
   auto it = fourier_tc_.find({L1, L2, L3});
   if (it != fourier_tc_.end()) return it->second;
   const int L = std::max(L1, L2);
   const FourierTables& ft = fourier_tables(L);
-  const int N = 4 * L + 1;
+  const int N = 4 * L + 2, H = N / 2;
   const int Lz = 2 * L;
   const int L3e = std::min(L3, Lz);
   DenseOps ops;
-  ops.G = N * N;
+  ops.G = N * H;
   ops.din1 = (L1 + 1) * (L1 + 1);
   ops.din2 = (L2 + 1) * (L2 + 1);
   ops.dout_eff = (L3e + 1) * (L3e + 1);
@@ -479,13 +486,14 @@ const GridTcEntry& Context::fourier_tc(int L1, int L2, int L3) {
   std::vector<std::complex<double>> wn(N);
   for (int k = 0; k < N; ++k) wn[k] = std::polar(1.0, 2.0 * M_PI * k / N);
   auto modn = [N](long v) { return static_cast<int>(((v % N) + N) % N); };
-  auto build_s = [&](int din, std::vector<double>& S) {
+  auto build_s = [&](int din, std::vector<double>& S) {  // row a * H + b: torus point (a, b), b < N/2
     S.assign(static_cast<size_t>(ops.G) * din, 0.0);
     for (int k = 0; k < din; ++k)
       for (const FourierMode& e : ft.enc[k])
         for (int a = 0; a < N; ++a)
-          for (int b = 0; b < N; ++b)
-            S[static_cast<size_t>(a * N + b) * din + k] += (e.w * wn[modn(static_cast<long>(e.u) * a + static_cast<long>(e.v) * b)]).real();
+          for (int b = 0; b < H; ++b)
+            S[static_cast<size_t>(a * H + b) * din + k] +=
+                (e.w * wn[modn(static_cast<long>(e.u) * a + static_cast<long>(e.v) * b)]).real();
   };
   build_s(ops.din1, ops.s1);
   if (!ops.same_s) build_s(ops.din2, ops.s2);
@@ -494,9 +502,13 @@ const GridTcEntry& Context::fourier_tc(int L1, int L2, int L3) {
   for (int o = 0; o < ops.dout_eff; ++o)
     for (const FourierMode& e : ft.dec[o])
       for (int a = 0; a < N; ++a)
-        for (int b = 0; b < N; ++b)
-          ops.a[static_cast<size_t>(o) * ops.G + a * N + b] +=
-              (e.w * wn[modn(-(static_cast<long>(e.u) * a + static_cast<long>(e.v) * b))]).real() * inv;
+        for (int b = 0; b < H; ++b) {
+          const int a2 = modn(N - a), b2 = b + H;  // the paired point carries the same product value
+          const long ph1 = static_cast<long>(e.u) * a + static_cast<long>(e.v) * b;
+          const long ph2 = static_cast<long>(e.u) * a2 + static_cast<long>(e.v) * b2;
+          ops.a[static_cast<size_t>(o) * ops.G + a * H + b] +=
+              ((e.w * wn[modn(-ph1)]).real() + (e.w * wn[modn(-ph2)]).real()) * inv;
+        }
   return fourier_tc_.emplace(std::array<int, 3>{L1, L2, L3}, build_dense_tc(ops, "gtp_fourier")).first->second;
 }
 
