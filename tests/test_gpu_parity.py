@@ -323,10 +323,11 @@ def test_kats(tpo):
     assert tpo.cgtp(x, y, 0, 0).item() == pytest.approx(-6.0, rel=1e-6)
 
 
-def test_equivariance(tpo, orc):
-    # SO(3) equivariance of the GPU products (proj/src/verify.cpp:76-117 protocol)
-    rng = orc.Rng(20240901)
-    L = 3
+@pytest.mark.parametrize("L", [3, 6])
+def test_equivariance(tpo, orc, L):
+    # SO(3) equivariance of the GPU products (proj/src/verify.cpp:76-117 protocol); L = 6
+    # exercises the CGTP block kernel, the dt = 13 MTP kernel and the folded Fourier torus
+    rng = orc.Rng(20240901 + L)
     t = orc.tower(L)
     for kind in ("cgtp", "gtp_grid", "gtp_fourier", "mtp"):
         worst, scale = 0.0, 0.0
