@@ -1,0 +1,31 @@
+"""Small runs of every kernel path for compute-sanitizer (memcheck): ragged batches,
+shared y, weights, host batch API."""
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import numpy as np
+import torch
+
+import paper_2506_13523_b200 as tpo
+
+dev = torch.device("cuda:0")
+g = torch.Generator(device=dev)
+g.manual_seed(5)
+for kind, L, B in (("gtp_grid", 3, 300), ("gtp_grid", 7, 130), ("gtp_fourier", 4, 200), ("mtp", 6, 300),
+                   ("mtp", 2, 129), ("cgtp", 6, 140), ("cgtp", 3, 77)):
+    d = (L + 1) ** 2
+    x = torch.randn((B, d), generator=g, device=dev)
+    y = torch.randn((B, d), generator=g, device=dev)
+    tpo.run(kind, x, y, L, L, 0 if kind == "cgtp" else 2 * L)
+x = torch.randn((3, 128, 16), generator=g, device=dev)
+y = torch.randn((3, 16), generator=g, device=dev)
+tpo.cgtp(x, y, 3, 3)  # C4 edge kernel
+x = torch.randn((150, 36), generator=g, device=dev)
+y = torch.randn((150, 36), generator=g, device=dev)
+tpo.weighted_gtp(x, y, np.ones(6), np.ones(6), np.ones(11), 5, 5, 10)
+hx = torch.randn(500, 16).pin_memory(); hy = torch.randn(500, 16).pin_memory()
+ho = torch.empty(500, 49).pin_memory(); hm = torch.empty(500, 49).pin_memory()
+tpo.run_host_batch([("gtp_grid", hx, hy, ho, 3, 3, 6), ("mtp", hx, hy, hm, 3, 3, 6)])
+torch.cuda.synchronize()
+print("sanitize run done")
