@@ -13,6 +13,7 @@
 // registers.  The R x dt matmul row tasks keep one output row of Z in
 // registers and stream X / Y from shared memory.
 #include <algorithm>
+#include <cstdlib>
 
 #include "kernels.hpp"
 
@@ -22,7 +23,7 @@ namespace {
 constexpr int kThreads = 256;
 constexpr int kMaxDt = 33;  // lt <= 16
 
-template <int R>
+template <int R, int ZR>
 __global__ void __launch_bounds__(kThreads)
     mtp_kernel(const __grid_constant__ MtpDevTables t, const __grid_constant__ RowSpec rs) {
   extern __shared__ float sm[];
@@ -74,16 +75,22 @@ __global__ void __launch_bounds__(kThreads)
       for (int r = 0; r < R; ++r) dst[r * pc] = acc[r];
     }
     __syncthreads();
-    // ---- Z = X Y, classical cubic (proj/src/mtp.cpp:119-133): task = (row r, Z row i)
-    for (int task = tid; task < R * dt; task += kThreads) {
-      const int r = task / dt, i = task - r * dt;
-      const float* xr = X + r * pc + i * dt;
+    // ---- Z = X Y, classical cubic (proj/src/mtp.cpp:119-133): task = (row r, Z rows i0 .. i0+ZR-1);
+    // every Y element loaded from shared memory feeds ZR rows
+    const int ntr = (dt + ZR - 1) / ZR;
+    for (int task = tid; task < R * ntr; task += kThreads) {
+      const int r = task / ntr, i0 = (task - r * ntr) * ZR;
+      const float* xr = X + r * pc + i0 * dt;
       const float* yb = Y + r * pc;
-      float acc[kMaxDt];
+      float acc[ZR][kMaxDt];
 #pragma unroll
-      for (int j = 0; j < kMaxDt; ++j) acc[j] = 0.f;
+      for (int q = 0; q < ZR; ++q)
+#pragma unroll
+        for (int j = 0; j < kMaxDt; ++j) acc[q][j] = 0.f;
       for (int k = 0; k < dt; ++k) {
-        const float a = xr[k];
+        float a[ZR];
+#pragma unroll
+        for (int q = 0; q < ZR; ++q) a[q] = i0 + q < dt ? xr[q * dt + k] : 0.f;
         const float* yk = yb + k * dt;
         // 8-wide blocks guarded as a whole: no issue slots spent past dt
 #pragma unroll
@@ -91,14 +98,22 @@ __global__ void __launch_bounds__(kThreads)
           if (j0 < dt) {
 #pragma unroll
             for (int jj = 0; jj < 8; ++jj)
-              if (j0 + jj < kMaxDt && j0 + jj < dt) acc[j0 + jj] = fmaf(a, yk[j0 + jj], acc[j0 + jj]);
+              if (j0 + jj < kMaxDt && j0 + jj < dt) {
+                const float yv = yk[j0 + jj];
+#pragma unroll
+                for (int q = 0; q < ZR; ++q) acc[q][j0 + jj] = fmaf(a[q], yv, acc[q][j0 + jj]);
+              }
           }
         }
       }
-      float* zr = Z + r * pc + i * dt;
 #pragma unroll
-      for (int j = 0; j < kMaxDt; ++j)
-        if (j < dt) zr[j] = acc[j];
+      for (int q = 0; q < ZR; ++q) {
+        if (i0 + q >= dt) break;
+        float* zr = Z + r * pc + (i0 + q) * dt;
+#pragma unroll
+        for (int j = 0; j < kMaxDt; ++j)
+          if (j < dt) zr[j] = acc[q][j];
+      }
     }
     __syncthreads();
     // ---- extract (proj/src/mtp.cpp:60-97): out[o] = sum_e c_e Z[cell_e]; zero past the carrier band
@@ -122,19 +137,32 @@ __global__ void __launch_bounds__(kThreads)
   }
 }
 
-template <int R>
-cudaError_t launch_r(const MtpDevTables& t, const RowSpec& rs, int num_sms, cudaStream_t s) {
+template <int R, int ZR>
+cudaError_t launch_rz(const MtpDevTables& t, const RowSpec& rs, int num_sms, cudaStream_t s) {
   const int dt2 = t.dt * t.dt;
   const size_t smem = sizeof(float) * R * ((t.din1 | 1) + (t.din2 | 1) + 3 * (dt2 | 1));
-  cudaError_t e = cudaFuncSetAttribute(mtp_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  cudaError_t e = cudaFuncSetAttribute(mtp_kernel<R, ZR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return e;
   int occ = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, mtp_kernel<R>, kThreads, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, mtp_kernel<R, ZR>, kThreads, smem);
   const int64_t ntiles = (rs.rows + R - 1) / R;
   const int grid = static_cast<int>(std::min<int64_t>(ntiles, static_cast<int64_t>(num_sms) * std::max(occ, 1)));
-  mtp_kernel<R><<<grid, kThreads, smem, s>>>(t, rs);
+  mtp_kernel<R, ZR><<<grid, kThreads, smem, s>>>(t, rs);
   return cudaGetLastError();
+}
+
+// Z rows per matmul task: 2 measured fastest at every dt (fewer shared loads per FMA beats the
+// lost task parallelism; tools/mtp_simt_timing.py); TPO_MTP_ZR=1|3 for experiments
+template <int R>
+cudaError_t launch_r(const MtpDevTables& t, const RowSpec& rs, int num_sms, cudaStream_t s) {
+  static const int zr = [] {
+    const char* v = std::getenv("TPO_MTP_ZR");
+    return v ? std::atoi(v) : 2;
+  }();
+  if (zr == 1) return launch_rz<R, 1>(t, rs, num_sms, s);
+  if (zr == 3) return launch_rz<R, 3>(t, rs, num_sms, s);
+  return launch_rz<R, 2>(t, rs, num_sms, s);
 }
 
 }  // namespace
