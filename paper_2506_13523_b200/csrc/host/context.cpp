@@ -701,7 +701,7 @@ const CgtpTcTables* Context::cgtp_tc(int L1, int L2) {
       // K order k = m1 * n2p + m2 (n2p = n2 padded to 8; zero columns at the padding)
       const int n2p = pad_to(n2, 8), kw = n1 * n2p;
       const int kpad = pad_to(kw, 16), npad_all = pad_to(n, 16);
-      const int parts = (npad_all + 255) / 256;
+      const int parts = (npad_all + 191) / 192;  // accumulators of 192 columns (cgtp_tc.cu kDCols)
       const int np = pad_to((n + parts - 1) / parts, 16);
       for (int p = 0; p < parts; ++p) {
         CgtpTcUnit u{};
@@ -735,7 +735,7 @@ const CgtpTcTables* Context::cgtp_tc(int L1, int L2) {
     }
   // super-units: consecutive units packed into one 256-column accumulator
   for (size_t i = 0, col = 0; i < units.size(); ++i) {
-    if (col + units[i].n_pad > 256) {
+    if (col + units[i].n_pad > 192) {
       units[i - 1].dcol_last |= 1 << 16;
       col = 0;
     }
@@ -753,16 +753,12 @@ const CgtpTcTables* Context::cgtp_tc(int L1, int L2) {
   const int xy_bytes = 128 * t.xy_pitch * 4;
   const int budget = 186 * 1024 - xy_bytes;  // the kernel's static staging takes ~35 KB
   const char* as_env = std::getenv("TPO_CGTP_ASTAGES");
-  constexpr int kAStageBytes = 16384;  // two K-steps (cgtp_tc.cu kKps)
-  t.a_stages = as_env ? std::max(2, std::min(8, std::atoi(as_env))) : 4;
-  t.b_stages = std::min(8, (budget - t.a_stages * kAStageBytes) / t.b_stage_bytes);
-  while (t.b_stages < 4 && t.a_stages > 2) {
-    --t.a_stages;
-    t.b_stages = std::min(8, (budget - t.a_stages * kAStageBytes) / t.b_stage_bytes);
-  }
+  (void)as_env;
+  t.a_stages = 4;  // the P ring lives in TMEM (cgtp_tc.cu kAStagesTmem)
+  t.b_stages = std::min(8, budget / t.b_stage_bytes);
   if (t.b_stages < 2) return fail();
   t.off_a = 0;
-  t.off_b = t.a_stages * kAStageBytes;
+  t.off_b = 0;
   t.off_xy = t.off_b + t.b_stages * t.b_stage_bytes;
   t.smem_bytes = t.off_xy + xy_bytes;
   if (std::getenv("TPO_VERBOSE"))

@@ -36,8 +36,10 @@ constexpr int BM = 128;
 constexpr int kThreads = 576;  // 18 warps
 constexpr int kMaxStages = 8;
 constexpr int kStageStride = 33;  // epilogue staging row pitch (32-column blocks)
-constexpr int kKps = 2;                         // K-steps per A stage (4: fewer stages fit, slower at L = 10)
-constexpr int kAStage = 2 * BM * 16 * kKps * 2;  // hi + lo, 128 x (16 kKps) fp16 each
+constexpr int kKps = 2;      // K-steps per A stage
+constexpr int kDCols = 192;  // TMEM: two accumulators [0, 192), [192, 384) ...
+constexpr int kARing = 384;  // ... and the A ring [384, 512): stage sa, K-step j: hi at 32 sa + 16 j, lo + 8
+constexpr int kAStagesTmem = 4;
 // barriers: A full [8], A empty [8], B full [8], B empty [8], D full [2], D empty [2]
 constexpr int B_AF = 0, B_AE = 8, B_BF = 16, B_BE = 24, B_DF = 32, B_DE = 34, kBars = 36;
 
@@ -54,6 +56,11 @@ __device__ __forceinline__ void cp_async4(float* dst, const float* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+__device__ __forceinline__ void tmem_st4(uint32_t taddr, const uint32_t (&r)[4]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};" ::"r"(taddr), "r"(r[0]), "r"(r[1]),
+               "r"(r[2]), "r"(r[3])
+               : "memory");
+}
 __device__ __forceinline__ int norm_exp(float ss) {
   return (ss > 0.f && ss < 3.0e38f) ? max(-120, min(120, ilogbf(ss) / 2 + 1)) : 0;
 }
@@ -76,7 +83,6 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t ntiles = (rs.rows + BM - 1) / BM;
-  uint8_t* ring_a = smem + t.off_a;
   uint8_t* ring_b = smem + t.off_b;
   float* rowbuf = reinterpret_cast<float*>(smem + t.off_xy);  // [128][pitch]: y row | x_{l1} (odd pitch)
 
@@ -156,17 +162,17 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_wait(&bars[B_BF + sb], pb);
           tick(4, t0);
           tc_fence_after();
-          const uint32_t a0 = smem_u32(ring_a + sa * kAStage) + j * 2 * lbo_a, b0 = smem_u32(ring_b + sb * t.b_stage_bytes);
-          const uint64_t ah = make_sdesc(a0, lbo_a, 128), al = make_sdesc(a0 + kAStage / 2, lbo_a, 128);
+          const uint32_t ah = tmem + kARing + 32u * sa + 16u * j, al = ah + 8u;  // P in TMEM (TS mode)
+          const uint32_t b0 = smem_u32(ring_b + sb * t.b_stage_bytes);
           const uint64_t bh = make_sdesc(b0, lbo_b, 128), bl = make_sdesc(b0 + half_b, lbo_b, 128);
-          const uint32_t dc = tmem + 256u * d + dcol;
-          if (el) mma_f16_ss(dc, ah, bh, id, ks > 0 ? 1u : 0u);
-          if (el) mma_f16_ss(dc, ah, bl, id, 1u);
-          if (el) mma_f16_ss(dc, al, bh, id, 1u);
+          const uint32_t dc = tmem + static_cast<uint32_t>(kDCols) * d + dcol;
+          if (el) mma_f16_ts(dc, ah, bh, id, ks > 0 ? 1u : 0u);
+          if (el) mma_f16_ts(dc, ah, bl, id, 1u);
+          if (el) mma_f16_ts(dc, al, bh, id, 1u);
           if (el) tc_commit(&bars[B_BE + sb]);
           if (j == kKps - 1 || ks + 1 == un.ksteps) {
             if (el) tc_commit(&bars[B_AE + sa]);
-            if (++sa == t.a_stages) {
+            if (++sa == kAStagesTmem) {
               sa = 0;
               pa ^= 1;
             }
@@ -190,7 +196,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     // K order inside a block: k = m1 * n2p + m2 with n2p = 2 l2 + 1 padded to 8, so each
     // thread's 8-product chunk (chunk 2 ks + h of the block) is one x value times 8
     // consecutive y values (W has zero columns at the padding).
-    const int pt = tid - 64, r = pt & (BM - 1), h = pt >> 7;
+    // TMEM lane access: warp w reaches lanes 32 (w % 4) ..; two warps per quarter split the K-step
+    const int r = 32 * (warp & 3) + lane, h = (warp - 2) >> 2, pt = h * BM + r;
+    const uint32_t lbw = tmem + (static_cast<uint32_t>(32 * (warp & 3)) << 16);
     float* row = rowbuf + r * t.xy_pitch;  // y row (scaled) at [0, din2), x_{l1} (scaled) at [din2, din2 + 21)
     int sa = 0, pa = 0, na = 0, it = 0;    // A ring slot / phase / stages produced
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
@@ -254,9 +262,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         int c = h;
         for (int ks0 = 0; ks0 < un.ksteps; ks0 += kKps, c += 2 * kKps) {  // one A stage = kKps K-steps
           const long long t0 = now();
-          if (na++ >= t.a_stages) mbar_wait(&bars[B_AE + sa], pa ^ 1);
+          if (na++ >= kAStagesTmem) {
+            mbar_wait(&bars[B_AE + sa], pa ^ 1);
+            tc_fence_after();
+          }
           tick(8, t0);
-          uint8_t* st = ring_a + sa * kAStage;
 #pragma unroll
           for (int j = 0; j < kKps; ++j) {  // (tail sub-steps past the unit are built but never issued)
             const int cc = c + 2 * j;
@@ -272,15 +282,17 @@ __global__ void __launch_bounds__(kThreads, 1)
               hw[q] = *reinterpret_cast<const uint32_t*>(&hh);
               lw[q] = pack_half2(p0 - hf.x, p1 - hf.y);
             }
-            *reinterpret_cast<uint4*>(st + canon_off(r, 16 * j + 8 * h, BM)) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
-            *reinterpret_cast<uint4*>(st + kAStage / 2 + canon_off(r, 16 * j + 8 * h, BM)) =
-                make_uint4(lw[0], lw[1], lw[2], lw[3]);
+            // this thread's 8 products = 4 packed columns of the K-step's hi and lo blocks
+            const uint32_t col = kARing + 32u * sa + 16u * j + 4u * h;
+            tmem_st4(lbw + col, hw);
+            tmem_st4(lbw + col + 8u, lw);
           }
           const long long tf = now();
-          fence_proxy_async_smem();
+          tmem_wait_st();
+          tc_fence_before();
           mbar_arrive(&bars[B_AF + sa]);
           tick(11, tf);
-          if (++sa == t.a_stages) {
+          if (++sa == kAStagesTmem) {
             sa = 0;
             pa ^= 1;
           }
@@ -312,7 +324,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tick(10, t0);
         const int e_row = e_sh[it & 1][q * 32 + lane];
         const float s_lo = pow2i(e_row >> 1), s_hi = pow2i(e_row - (e_row >> 1));  // exact, split for range
-        const uint32_t dbase = lb + 256u * d;
+        const uint32_t dbase = lb + static_cast<uint32_t>(kDCols) * d;
         int uu = u0;
         // 32-column blocks (the last may be 16 wide), alternating between the quarter's two warps
         for (int c0 = 32 * eh; c0 < ncols; c0 += 64) {
