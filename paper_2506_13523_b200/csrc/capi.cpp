@@ -109,7 +109,7 @@ void run_cgtp(tpo_ctx* ctx, int L1, int L2, const RowSpec& rs, cudaStream_t s) {
   // larger degrees: per-(l1, l2) block GEMMs on tcgen05 (output-write bound)
   static const int tc_min_l = [] {
     const char* v = std::getenv("TPO_CGTP_TC_MINL");
-    return v ? std::atoi(v) : 5;  // measured: SIMT wins at L <= 3, even at L = 4
+    return v ? std::atoi(v) : 4;  // measured: SIMT wins at L <= 3 (L=4: 0.122 vs 0.147 ms)
   }();
   if (std::max(L1, L2) >= tc_min_l)
     if (const tpo_b200::CgtpTcTables* tc = ctx->impl.cgtp_tc(L1, L2)) {
