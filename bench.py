@@ -59,57 +59,108 @@ def load_peaks() -> dict:
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clocks + throttle reasons sampled during the timed region.
 
+    NVML is polled from a thread every ~1 ms (nvidia-smi's 20 ms cadence and
+    process start-up miss a few-ms region entirely); only samples taken while a
+    region is open (``with clk.region():``) are summarised.  Falls back to
+    ``nvidia-smi -lms 20`` when NVML is unavailable."""
+
+    REASONS = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+               ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+               ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+               ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"),
+               ("hw_power_brake", "nvmlClocksEventReasonHwPowerBrakeSlowdown"))
     FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
 
     def __init__(self, index: int):
         self.index = index
+        self.samples: list[tuple[float, set]] = []  # (sm MHz, reasons) inside open regions
+        self.max_mhz = None
+        self.source = None
+        self._open = False
+        self._stop = threading.Event()
+        self._t = None
         self.proc = None
-        self.lines: list[str] = []
 
     def __enter__(self):
         try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = float(pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM))
+            bits = [(n, getattr(pynvml, a)) for n, a in self.REASONS]
+
+            def poll():
+                while not self._stop.is_set():
+                    if self._open:
+                        sm = float(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM))
+                        r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                        self.samples.append((sm, {n for n, b in bits if r & b}))
+                    time.sleep(0.001)
+
+            self.source = "nvml (1 ms poll)"
+            self._t = threading.Thread(target=poll, daemon=True)
+            self._t.start()
+            return self
+        except Exception:
+            pass
+        try:  # fallback: nvidia-smi loop
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
                  "-lms", "20"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self._t = threading.Thread(target=self._read, daemon=True)
+            self.source = "nvidia-smi -lms 20"
+            self._t = threading.Thread(target=self._read_smi, daemon=True)
             self._t.start()
         except FileNotFoundError:
             self.proc = None
         return self
 
-    def _read(self):
+    def _read_smi(self):
+        names = [n for n, _ in self.REASONS[:4]]
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            parts = [p.strip() for p in line.split(",")]
+            if not self._open or len(parts) < 7:
+                continue
+            try:
+                sm = float(parts[0])
+                self.max_mhz = float(parts[1])
+            except ValueError:
+                continue
+            self.samples.append((sm, {n for n, v in zip(names, parts[3:7]) if v.lower() == "active"}))
+
+    class _Region:
+        def __init__(self, outer):
+            self.o = outer
+
+        def __enter__(self):
+            self.o._open = True
+
+        def __exit__(self, *exc):
+            self.o._open = False
+
+    def region(self):
+        return ClockSampler._Region(self)
 
     def __exit__(self, *exc):
+        self._stop.set()
         if self.proc:
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=2)
             except Exception:
                 self.proc.kill()
+        if self._t:
+            self._t.join(timeout=2)
 
     def summary(self) -> dict:
-        sm, mx, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            parts = [p.strip() for p in ln.split(",")]
-            if len(parts) < 7:
-                continue
-            try:
-                sm.append(float(parts[0]))
-                mx = float(parts[1])
-            except ValueError:
-                continue
-            for n, v in zip(names, parts[3:7]):
-                if v.lower() == "active":
-                    reasons.add(n)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
-                "reasons": sorted(reasons), "samples": len(sm)}
+        sm = [s for s, _ in self.samples]
+        reasons = set().union(*[r for _, r in self.samples]) if self.samples else set()
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(reasons), "samples": len(sm), "source": self.source}
 
 
 def dist_setup():
@@ -260,24 +311,26 @@ def main():
         wall0 = time.perf_counter()
         ev0 = torch.cuda.Event(enable_timing=True)
         ev1 = torch.cuda.Event(enable_timing=True)
-        for _ in range(args.steps):
-            flush.zero_()  # evict L2 (untimed)
-            ev0.record(stream)
-            graph.replay()
-            ev1.record(stream)
-            ev1.synchronize()
-            total_ms += ev0.elapsed_time(ev1)
-        torch.cuda.synchronize()
-        wall = time.perf_counter() - wall0
-        # per-L breakdown (outside the headline timing; same flush discipline)
-        for L in LS:
-            for _ in range(max(3, args.steps // 5)):
-                flush.zero_()
+        with clk.region():
+            for _ in range(args.steps):
+                flush.zero_()  # evict L2 (untimed)
                 ev0.record(stream)
-                graphs_L[L].replay()
+                graph.replay()
                 ev1.record(stream)
                 ev1.synchronize()
-                per_L[L] += ev0.elapsed_time(ev1) / max(3, args.steps // 5) * args.steps
+                total_ms += ev0.elapsed_time(ev1)
+            torch.cuda.synchronize()
+        wall = time.perf_counter() - wall0
+        # per-L breakdown (outside the headline timing; same flush discipline)
+        with clk.region():
+            for L in LS:
+                for _ in range(max(3, args.steps // 5)):
+                    flush.zero_()
+                    ev0.record(stream)
+                    graphs_L[L].replay()
+                    ev1.record(stream)
+                    ev1.synchronize()
+                    per_L[L] += ev0.elapsed_time(ev1) / max(3, args.steps // 5) * args.steps
     launches = launches_per_step * args.steps
     from paper_2506_13523_b200.dist import gather_checksums, max_over_ranks
 

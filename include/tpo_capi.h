@@ -95,6 +95,18 @@ int tpo_weighted_gtp_f32(tpo_ctx* ctx, int L1, int L2, int L3, const double* a,
                          const double* b, const double* c, const float* x, const float* y,
                          float* out, int64_t batch, int64_t channels, int y_shared, void* stream);
 
+/* Backward (vector-Jacobian products) of any kind: given grad_out
+ * [batch][channels][Dout], writes grad_x [batch][channels][(L1+1)^2] and
+ * grad_y [batch][channels][(L2+1)^2] (either may be NULL to skip it).  The
+ * reference has no backward (its paper benchmarks one);
+ * this is SURVEY.md 8(f) f4.  GTP kinds reuse the forward kernels through the
+ * symmetry of the real Gaunt coefficients, MTP through embed/extract adjoints
+ * (same l_tilde as the forward), CGTP through transposed CG term lists.
+ * y_shared != 0 is supported for grad_x only (grad_y must be NULL). */
+int tpo_backward_f32(tpo_ctx* ctx, int kind, int L1, int L2, int L3, int l_tilde, const float* x,
+                     const float* y, const float* grad_out, float* grad_x, float* grad_y,
+                     int64_t batch, int64_t channels, int y_shared, void* stream);
+
 /* Generic dispatch by kind (l_tilde only used by MTP). */
 int tpo_run_f32(tpo_ctx* ctx, int kind, int L1, int L2, int L3, int l_tilde, const float* x,
                 const float* y, float* out, int64_t batch, int64_t channels, int y_shared,

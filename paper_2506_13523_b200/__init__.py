@@ -8,6 +8,8 @@ Batched device API (torch tensors on an sm_100 device, fp32, contiguous):
     out = gtp_fourier(x, y, L1, L2, L3)            # tpo::gtp_fourier
     out = mtp(x, y, L1, L2, L3, l_tilde=-1)        # tpo::mtp
     out = weighted_gtp(x, y, a, b, c, L1, L2, L3)  # tpo::weighted_gtp
+    gx, gy = backward(kind, x, y, grad_out, L1, L2, L3)  # vector-Jacobian products
+    out = product(kind, x, y, L1, L2, L3)          # autograd-aware (torch.autograd.Function)
 
 x is [B, Din1] or [B, C, Din1]; y is [B, Din2] (shared across the C
 channels when x has a channel axis) or [B, C, Din2].  Results are
@@ -23,7 +25,7 @@ from ._lib import KINDS, Context, HostRequest, TpoError, check, context, lib
 
 __all__ = [
     "cgtp", "gtp_grid", "gtp_fourier", "mtp", "weighted_gtp", "run", "out_dim", "tower_dim",
-    "mtp_l_tilde", "Context", "TpoError", "context", "lib", "KINDS",
+    "mtp_l_tilde", "backward", "product", "Context", "TpoError", "context", "lib", "KINDS",
 ]
 
 
@@ -166,3 +168,61 @@ def weighted_gtp(x, y, a, b, c, L1: int, L2: int, L3: int):
     check(lib().tpo_weighted_gtp_f32(ctx.handle, L1, L2, L3, ptr(a), ptr(b), ptr(c), x.data_ptr(),
                                      y.data_ptr(), o.data_ptr(), B, Cc, ys, stream))
     return o
+
+
+def backward(kind: str, x, y, grad_out, L1: int, L2: int, L3: int = 0, l_tilde: int = -1,
+             need_x: bool = True, need_y: bool = True):
+    """Vector-Jacobian products of a product (tpo_backward_f32): returns
+    (grad_x, grad_y), each None when not requested.  grad_out has the forward
+    output's shape.  With a shared y ([B, Din2] beside x [B, C, Din1]) only
+    grad_x is available."""
+    import torch
+
+    x, y, o, B, C, ys, stream = _prep(x, y, L1, L2, kind, L3)
+    if not isinstance(grad_out, torch.Tensor) or grad_out.shape != o.shape or grad_out.dtype != torch.float32:
+        raise ValueError(f"grad_out must be a float32 tensor of shape {tuple(o.shape)}")
+    if grad_out.device != x.device:
+        raise ValueError("grad_out must be on the inputs' device")
+    if ys and need_y:
+        raise ValueError("backward: grad_y with a shared y is not supported")
+    g = grad_out.contiguous()
+    gx = torch.empty_like(x) if need_x else None
+    gy = torch.empty_like(y) if need_y else None
+    ctx = context(x.device.index)
+    check(lib().tpo_backward_f32(ctx.handle, KINDS[kind], L1, L2, L3, l_tilde, x.data_ptr(), y.data_ptr(),
+                                 g.data_ptr(), gx.data_ptr() if gx is not None else None,
+                                 gy.data_ptr() if gy is not None else None, B, C, ys, stream))
+    return gx, gy
+
+
+_Fn = None
+
+
+def _autograd_fn():
+    global _Fn
+    if _Fn is None:
+        import torch
+
+        class TensorProductFn(torch.autograd.Function):
+            @staticmethod
+            def forward(ctx, x, y, kind, L1, L2, L3, l_tilde):
+                ctx.save_for_backward(x, y)
+                ctx.cfg = (kind, L1, L2, L3, l_tilde)
+                return run(kind, x, y, L1, L2, L3, l_tilde)
+
+            @staticmethod
+            def backward(ctx, g):
+                x, y = ctx.saved_tensors
+                kind, L1, L2, L3, l_tilde = ctx.cfg
+                gx, gy = backward(kind, x, y, g, L1, L2, L3, l_tilde, ctx.needs_input_grad[0],
+                                  ctx.needs_input_grad[1])
+                return gx, gy, None, None, None, None, None
+
+        _Fn = TensorProductFn
+    return _Fn
+
+
+def product(kind: str, x, y, L1: int, L2: int, L3: int = 0, l_tilde: int = -1):
+    """Differentiable product (torch.autograd): the forward kernel of ``kind``
+    and tpo_backward_f32 for the gradients."""
+    return _autograd_fn().apply(x, y, kind, L1, L2, L3, l_tilde)

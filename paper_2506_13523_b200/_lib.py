@@ -67,6 +67,7 @@ def lib():
             "tpo_mtp_f32": (i, [p, i, i, i, i, p, p, p, i64, i64, i, p]),
             "tpo_weighted_gtp_f32": (i, [p, i, i, i, p, p, p, p, p, p, i64, i64, i, p]),
             "tpo_run_f32": (i, [p, i, i, i, i, i, p, p, p, i64, i64, i, p]),
+            "tpo_backward_f32": (i, [p, i, i, i, i, i, p, p, p, p, p, i64, i64, i, p]),
             "tpo_run_host_f32": (i, [p, i, i, i, i, i, p, p, p, i64, i64, i]),
             "tpo_run_host_batch_f32": (i, [p, p, i]),
             "tpo_set_gtp_grid_path": (i, [p, i]),
@@ -86,7 +87,7 @@ EXPORTED = [
     "tpo_last_error", "tpo_version", "tpo_ctx_create", "tpo_ctx_destroy", "tpo_ctx_launches",
     "tpo_tower_dim", "tpo_out_dim", "tpo_mtp_l_tilde", "tpo_cgtp_mimo_f32", "tpo_gtp_grid_f32",
     "tpo_gtp_fourier_f32", "tpo_mtp_f32", "tpo_weighted_gtp_f32", "tpo_run_f32", "tpo_run_host_f32",
-    "tpo_run_host_batch_f32",
+    "tpo_run_host_batch_f32", "tpo_backward_f32",
     "tpo_set_gtp_grid_path", "tpo_last_gtp_grid_path", "tpo_cg_real", "tpo_fourier_table",
 ]
 

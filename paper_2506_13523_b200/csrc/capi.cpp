@@ -325,6 +325,86 @@ int tpo_weighted_gtp_f32(tpo_ctx* ctx, int L1, int L2, int L3, const double* a, 
   });
 }
 
+// Vector-Jacobian products (backward) of the four products; the reference has
+// none (its paper benchmarks backward).
+// Every product is bilinear, out_c = sum_ab W_abc x_a y_b, so
+// grad_x_a = sum_bc W_abc y_b g_c and grad_y_b = sum_ac W_abc x_a g_c:
+//  * GTP (grid / Fourier): W = real Gaunt coefficients, symmetric in (a, b, c),
+//    hence grad_x = gtp(g, y; L3, L2 -> L1) and grad_y = gtp(g, x; L3, L1 -> L2)
+//    -- the forward kernels on a grid of band L3 + L2 (exact quadrature);
+//  * MTP: extract is the adjoint of embed and embed(v)^T = embed(P v) with
+//    P = (-1)^l per degree, hence grad_x = mtp(g, P y) and grad_y = mtp(P x, g)
+//    (carrier l~ of the forward; degree-parity pass on the other input);
+//  * CGTP: transposed real-CG term lists on the sparse SIMT kernel
+//    (Context::cgtp_bwd), windows of grad_out columns accumulated.
+// grad_x / grad_y may be null (not computed).  With a shared y (one per batch
+// entry across channels) grad_y would be a channel reduction: not supported.
+int tpo_backward_f32(tpo_ctx* ctx, int kind, int L1, int L2, int L3, int l_tilde, const float* x, const float* y,
+                     const float* grad_out, float* grad_x, float* grad_y, int64_t batch, int64_t channels,
+                     int y_shared, void* stream) {
+  return guarded([&] {
+    check_args(ctx, L1, L2, x, y, grad_out, batch, channels);
+    if (y_shared && grad_y) throw InvalidArgument("backward: grad_y with a shared y (channel reduction) is not supported");
+    const cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const int64_t rows = batch * channels;
+    ctx->impl.activate();
+    Context& c = ctx->impl;
+    switch (kind) {
+      case TPO_KIND_CGTP: {
+        if (rows == 0) return;
+        if (grad_x)
+          for (const auto& t : c.cgtp_bwd(L1, L2, 0))
+            launched(ctx, tpo_b200::launch_cgtp(t, rows_of(grad_out, y, grad_x, batch, channels, y_shared), c.num_sms(), s),
+                     "cgtp backward kernel");
+        if (grad_y)
+          for (const auto& t : c.cgtp_bwd(L1, L2, 1))
+            launched(ctx, tpo_b200::launch_cgtp(t, rows_of(grad_out, x, grad_y, batch, channels, 0), c.num_sms(), s),
+                     "cgtp backward kernel");
+        return;
+      }
+      case TPO_KIND_GTP_GRID:
+      case TPO_KIND_GTP_FOURIER: {
+        check_L3(L3, "gtp backward");
+        if (L3 > kMaxL) throw InvalidArgument("gtp backward: L3 above the supported input maximum");
+        if (grad_x) run_kind(ctx, TPO_KIND_GTP_GRID, L3, L2, L1, -1, grad_out, y, grad_x, batch, channels, y_shared, s);
+        if (grad_y) run_kind(ctx, TPO_KIND_GTP_GRID, L3, L1, L2, -1, grad_out, x, grad_y, batch, channels, 0, s);
+        return;
+      }
+      case TPO_KIND_MTP: {
+        check_L3(L3, "mtp backward");
+        if (L3 > kMaxL) throw InvalidArgument("mtp backward: L3 above the supported input maximum");
+        const int lmin = min_lt(L1, L2, L3);
+        if (l_tilde >= 0 && l_tilde < lmin) throw InvalidArgument("mtp: l_tilde below the minimal carrier degree");
+        const int lt = l_tilde >= 0 ? l_tilde : lmin;
+        if (rows == 0) return;
+        auto parity = [&](int L) {
+          std::vector<double> w(L + 1);
+          for (int l = 0; l <= L; ++l) w[l] = (l & 1) ? -1.0 : 1.0;
+          return c.degree_weights(w);
+        };
+        if (grad_x) {
+          const int64_t yrows = y_shared ? batch : rows;
+          float* py = nullptr;
+          tpo_b200::cuda_check(cudaMallocAsync(reinterpret_cast<void**>(&py), std::max<int64_t>(yrows, 1) * (L2 + 1) * (L2 + 1) * sizeof(float), s), "malloc");
+          launched(ctx, tpo_b200::launch_scale_degrees(y, py, yrows, L2, parity(L2), s), "parity");
+          run_kind(ctx, TPO_KIND_MTP, L3, L2, L1, lt, grad_out, py, grad_x, batch, channels, y_shared, s);
+          cudaFreeAsync(py, s);
+        }
+        if (grad_y) {
+          float* px = nullptr;
+          tpo_b200::cuda_check(cudaMallocAsync(reinterpret_cast<void**>(&px), rows * (L1 + 1) * (L1 + 1) * sizeof(float), s), "malloc");
+          launched(ctx, tpo_b200::launch_scale_degrees(x, px, rows, L1, parity(L1), s), "parity");
+          run_kind(ctx, TPO_KIND_MTP, L1, L3, L2, lt, px, grad_out, grad_y, batch, channels, 0, s);
+          cudaFreeAsync(px, s);
+        }
+        return;
+      }
+      default:
+        throw InvalidArgument("backward: unknown kind");
+    }
+  });
+}
+
 namespace {
 void cuda_check_s(cudaError_t e, const char* what) { tpo_b200::cuda_check(e, what); }
 }  // namespace

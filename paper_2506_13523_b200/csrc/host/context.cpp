@@ -113,12 +113,13 @@ float* Context::scratch(int slot, size_t floats) {
 // ------------------------------------------------------------------ CGTP
 // Output layout = reference path order (x degree, y degree, l3 ascending),
 // proj/src/cgtp.cpp:152-163; term lists from the real CG nonzeros.
-const CgtpTables& Context::cgtp(int L1, int L2) {
-  std::lock_guard<std::mutex> g(mu_);
-  auto it = cgtp_.find({L1, L2});
-  if (it != cgtp_.end()) return it->second;
-  const int din1 = (L1 + 1) * (L1 + 1), din2 = (L2 + 1) * (L2 + 1);
-  std::vector<std::vector<std::pair<uint32_t, float>>> per_out;
+namespace {
+using TermList = std::vector<std::vector<std::pair<uint32_t, float>>>;  // per output: {i1 | i2 << 16, coef}
+
+// CGTP term lists of every path, in the reference's output order
+// (proj/src/cgtp.cpp:152-163): per_out[o] = {(i1, i2, c)} over the real-CG nonzeros
+TermList cgtp_terms(int L1, int L2) {
+  TermList per_out;
   for (int l1 = 0; l1 <= L1; ++l1)
     for (int l2 = 0; l2 <= L2; ++l2)
       for (int l3 = std::abs(l1 - l2); l3 <= l1 + l2; ++l3) {
@@ -129,6 +130,13 @@ const CgtpTables& Context::cgtp(int L1, int L2) {
           per_out[off + e.m3 + l3].push_back({i1 | (i2 << 16), static_cast<float>(e.v)});
         }
       }
+  return per_out;
+}
+}  // namespace
+
+// Pack per-output term lists warp-major (kernels.hpp: CgtpTables) and upload.
+CgtpTables Context::pack_cgtp(const std::vector<std::vector<std::pair<uint32_t, float>>>& per_out, int din1,
+                              int din2) {
   const int dout = static_cast<int>(per_out.size());
   const int nchunks = (dout + kCgtpChunk - 1) / kCgtpChunk;
   const int nwarps = nchunks * kCgtpChunk / 32;
@@ -159,10 +167,58 @@ const CgtpTables& Context::cgtp(int L1, int L2) {
   t.din2 = din2;
   t.dout = dout;
   t.nchunks = nchunks;
+  t.x_stride = din1;
+  t.x_off = 0;
+  t.accumulate = 0;
   t.terms = upload(terms);
   t.warp_off = upload(off);
   t.warp_nt = upload(nt);
+  return t;
+}
+
+// Output layout = reference path order (x degree, y degree, l3 ascending),
+// proj/src/cgtp.cpp:152-163; term lists from the real CG nonzeros.
+const CgtpTables& Context::cgtp(int L1, int L2) {
+  std::lock_guard<std::mutex> g(mu_);
+  auto it = cgtp_.find({L1, L2});
+  if (it != cgtp_.end()) return it->second;
+  const CgtpTables t = pack_cgtp(cgtp_terms(L1, L2), (L1 + 1) * (L1 + 1), (L2 + 1) * (L2 + 1));
   return cgtp_.emplace(std::array<int, 2>{L1, L2}, t).first->second;
+}
+
+// CGTP backward (vector-Jacobian product) on the same SIMT kernel.  With
+// out[o] = sum_t c_t x[i1_t] y[i2_t]:
+//   grad_x[a] = sum_{t: i1_t = a} c_t g[o_t] y[i2_t],  grad_y[b] = sum_{t: i2_t = b} c_t g[o_t] x[i1_t].
+// The kernel's first operand is a window of grad_out columns [o0, o0 + w)
+// (x_off / x_stride), its second the other input (so a per-edge shared y
+// keeps working for grad_x); windows accumulate into the result.
+const std::vector<CgtpTables>& Context::cgtp_bwd(int L1, int L2, int wrt) {
+  std::lock_guard<std::mutex> g(mu_);
+  auto it = cgtp_bwd_.find({L1, L2, wrt});
+  if (it != cgtp_bwd_.end()) return it->second;
+  const int din1 = (L1 + 1) * (L1 + 1), din2 = (L2 + 1) * (L2 + 1);
+  const int dres = wrt == 0 ? din1 : din2, dother = wrt == 0 ? din2 : din1;
+  const TermList fwd = cgtp_terms(L1, L2);
+  const int dout = static_cast<int>(fwd.size());
+  // window width: shared tile (w + dother) * 36 floats stays <= ~95 KB (two blocks per SM)
+  const int wmax = std::max(64, 660 - dother) / 4 * 4;
+  std::vector<CgtpTables> tabs;
+  for (int o0 = 0; o0 < dout; o0 += wmax) {
+    const int w = std::min(wmax, dout - o0);
+    TermList per_res(dres);
+    for (int o = o0; o < o0 + w; ++o)
+      for (const auto& tm : fwd[o]) {
+        const uint32_t i1 = tm.first & 0xFFFFu, i2 = tm.first >> 16;
+        const uint32_t res = wrt == 0 ? i1 : i2, oth = wrt == 0 ? i2 : i1;
+        per_res[res].push_back({static_cast<uint32_t>(o - o0) | (oth << 16), tm.second});
+      }
+    CgtpTables t = pack_cgtp(per_res, w, dother);
+    t.x_stride = dout;
+    t.x_off = o0;
+    t.accumulate = o0 > 0 ? 1 : 0;
+    tabs.push_back(t);
+  }
+  return cgtp_bwd_.emplace(std::array<int, 3>{L1, L2, wrt}, std::move(tabs)).first->second;
 }
 
 // ------------------------------------------------------------------ GTP grid (tcgen05)

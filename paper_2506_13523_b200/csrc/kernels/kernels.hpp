@@ -29,6 +29,10 @@ struct RowSpec {
 constexpr int kCgtpChunk = 256;
 struct CgtpTables {
   int din1, din2, dout, nchunks;
+  // x rows are read as x[r * x_stride + x_off + i1] (forward: x_stride = din1, x_off = 0; the
+  // backward tables sweep windows of grad_out columns); accumulate: out += instead of out =
+  int64_t x_stride;
+  int x_off, accumulate;
   const uint2* terms;
   const int* warp_off;  // [nchunks * kCgtpChunk / 32]
   const int* warp_nt;   // [nchunks * kCgtpChunk / 32]

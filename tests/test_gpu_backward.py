@@ -1,0 +1,140 @@
+"""GPU parity of the backward pass (tpo_backward_f32).
+
+The reference has no backward; the oracle here is the definition itself:
+every product is bilinear, so the vector-Jacobian product for row b is
+grad_x = J_x(y_b)^T g_b with J_x(y_b)[a] = T(e_a, y_b), evaluated by the fp64
+oracle on basis vectors (no use of the Gaunt / embed identities the kernels
+rely on).  Same normwise 1e-5 contract as the forward.  At full sizes the
+check is size-independent: <g, T(dx, y)> = <grad_x, dx> (bilinearity).
+"""
+import numpy as np
+import pytest
+
+TOL = 1e-5
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def tpo():
+    import torch
+
+    assert torch.cuda.is_available()
+    import paper_2506_13523_b200 as m
+
+    return m
+
+
+def _dout(kind, L):
+    return (L + 1) ** 4 if kind == "cgtp" else (2 * L + 1) ** 2
+
+
+def _ref_vjp(orc, kind, L, x, y, g):
+    """fp64 (grad_x, grad_y) per row from oracle Jacobians on basis vectors."""
+    B, D = x.shape
+    eye = np.eye(D)[:, None]
+    gx = np.empty((B, D)); gy = np.empty((B, D))
+    for b in range(B):
+        Jx = orc.batch_mimo(kind, L, eye, np.repeat(y[b][None, None], D, 0))[:, 0]  # [D][Dout]
+        Jy = orc.batch_mimo(kind, L, np.repeat(x[b][None, None], D, 0), eye)[:, 0]
+        gx[b] = Jx @ g[b]
+        gy[b] = Jy @ g[b]
+    return gx, gy
+
+
+def _normwise(out, ref):
+    scale = np.maximum(np.abs(ref).max(axis=1), 1e-300)
+    return float((np.abs(out - ref).max(axis=1) / scale).max())
+
+
+def _run(tpo, kind, L, B, seed, L3=None, lt=-1):
+    import torch
+
+    L3 = 2 * L if L3 is None else L3
+    rng = np.random.default_rng(seed)
+    D = (L + 1) ** 2
+    x = rng.standard_normal((B, D)).astype(np.float32)
+    y = rng.standard_normal((B, D)).astype(np.float32)
+    g = rng.standard_normal((B, _dout(kind, L))).astype(np.float32)
+    gx, gy = tpo.backward(kind, torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda(),
+                          torch.from_numpy(g).cuda(), L, L, L3, lt)
+    torch.cuda.synchronize()
+    return x, y, g, gx.cpu().numpy().astype(np.float64), gy.cpu().numpy().astype(np.float64)
+
+
+@pytest.mark.parametrize("kind,L", [("cgtp", 1), ("cgtp", 2), ("cgtp", 3), ("cgtp", 5), ("cgtp", 6),
+                                    ("gtp_grid", 1), ("gtp_grid", 3), ("gtp_grid", 5), ("gtp_grid", 6),
+                                    ("gtp_grid", 10), ("gtp_fourier", 2), ("gtp_fourier", 6),
+                                    ("mtp", 1), ("mtp", 3), ("mtp", 6), ("mtp", 8)])
+def test_backward_vs_oracle(tpo, orc, kind, L):
+    B = 6 if L >= 6 else 24
+    x, y, g, gx, gy = _run(tpo, kind, L, B, 900 + L)
+    rx, ry = _ref_vjp(orc, kind, L, x.astype(np.float64), y.astype(np.float64), g.astype(np.float64))
+    ex, ey = _normwise(gx, rx), _normwise(gy, ry)
+    assert ex <= TOL and ey <= TOL, (kind, L, ex, ey)
+
+
+def test_backward_mtp_l_tilde_override(tpo, orc):
+    """Larger carrier (l~ = 4 at L = 2): the VJP uses the forward's carrier."""
+    L, lt = 2, 4
+    x, y, g, gx, gy = _run(tpo, "mtp", L, 4, 77, lt=lt)
+    t, t3 = orc.tower(L), orc.tower(2 * L)
+    D = (L + 1) ** 2
+    for b in range(4):
+        Jx = np.stack([orc.mtp(t, np.eye(D)[a], t, y[b].astype(np.float64), 2 * L, lt_override=lt) for a in range(D)])
+        Jy = np.stack([orc.mtp(t, x[b].astype(np.float64), t, np.eye(D)[a], 2 * L, lt_override=lt) for a in range(D)])
+        assert _normwise(gx[b][None], (Jx @ g[b])[None]) <= TOL
+        assert _normwise(gy[b][None], (Jy @ g[b])[None]) <= TOL
+    del t3
+
+
+@pytest.mark.parametrize("kind,L", [("cgtp", 3), ("cgtp", 5), ("gtp_grid", 4), ("mtp", 4)])
+def test_backward_shared_y_channels(tpo, orc, kind, L):
+    """Channel-wise form (x [B][C][D], y [B][D] shared): grad_x per (b, c)."""
+    import torch
+
+    B, C = 3, 64
+    rng = np.random.default_rng(31 + L)
+    D = (L + 1) ** 2
+    x = rng.standard_normal((B, C, D)).astype(np.float32)
+    y = rng.standard_normal((B, D)).astype(np.float32)
+    g = rng.standard_normal((B, C, _dout(kind, L))).astype(np.float32)
+    gx, gy = tpo.backward(kind, torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda(), torch.from_numpy(g).cuda(),
+                          L, L, 2 * L, need_y=False)
+    assert gy is None
+    gx = gx.cpu().numpy().astype(np.float64)
+    eye = np.eye(D)[:, None]
+    for b in range(B):
+        Jx = orc.batch_mimo(kind, L, eye, np.repeat(y[b].astype(np.float64)[None, None], D, 0))[:, 0]
+        ref = g[b].astype(np.float64) @ Jx.T  # [C][D]
+        assert _normwise(gx[b], ref) <= TOL, (kind, L, b)
+    with pytest.raises(ValueError):
+        tpo.backward(kind, torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda(), torch.from_numpy(g).cuda(),
+                     L, L, 2 * L)
+
+
+@pytest.mark.parametrize("kind,L", [("gtp_grid", 10), ("gtp_fourier", 6), ("mtp", 6), ("cgtp", 4)])
+def test_backward_bilinearity_full_batch(tpo, kind, L):
+    """Size-independent check at the BASELINE batch: <g, T(dx, y)> = <grad_x, dx>
+    and <g, T(x, dy)> = <grad_y, dy> per row, through the autograd wrapper."""
+    import torch
+
+    B = 65536 if kind != "cgtp" else 8192
+    gen = torch.Generator(device="cuda").manual_seed(5)
+    D = (L + 1) ** 2
+    x = torch.randn(B, D, device="cuda", generator=gen, requires_grad=True)
+    y = torch.randn(B, D, device="cuda", generator=gen, requires_grad=True)
+    out = tpo.product(kind, x, y, L, L, 2 * L)
+    g = torch.randn(out.shape, device="cuda", generator=gen)
+    out.backward(g)
+    dx = torch.randn(B, D, device="cuda", generator=gen)
+    dy = torch.randn(B, D, device="cuda", generator=gen)
+    with torch.no_grad():
+        lhs_x = (g.double() * tpo.run(kind, dx, y.detach(), L, L, 2 * L).double()).sum(1)
+        rhs_x = (x.grad.double() * dx.double()).sum(1)
+        lhs_y = (g.double() * tpo.run(kind, x.detach(), dy, L, L, 2 * L).double()).sum(1)
+        rhs_y = (y.grad.double() * dy.double()).sum(1)
+    for lhs, rhs in ((lhs_x, rhs_x), (lhs_y, rhs_y)):
+        scale = (g.double().abs().sum(1) * 1.0).clamp_min(1.0)
+        err = ((lhs - rhs).abs() / scale).max().item()
+        assert err < 1e-4, (kind, L, err)
