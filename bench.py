@@ -513,6 +513,29 @@ def side_measurements(tpo, dev, stream, flush, peaks):
                                   "channel_tp_per_s": round(B * C / ms * 1e3, 1),
                                   "gbs": round(byts / ms / 1e6, 1), "roofline_frac": round(byts / hbm / (ms / 1e3), 4),
                                   "bound": "HBM (139,328 B per edge)"}
+    # general CGTP at L=6 (per-(l1, l2) block GEMMs on tcgen05): output-write bound
+    L, B = 6, 65536
+    din, dout = (L + 1) ** 2, (L + 1) ** 4
+    x = torch.randn((B, din), generator=g, device=dev)
+    y = torch.randn((B, din), generator=g, device=dev)
+    o = torch.empty((B, dout), device=dev)
+    ms = timeit(lambda: tpo.cgtp(x, y, L, L, out=o))
+    byts = 4 * (2 * din + dout) * B
+    res[f"cgtp_L{L}_B{B}"] = {"ms": round(ms, 4), "tp_per_s": round(B / ms * 1e3, 1), "gbs": round(byts / ms / 1e6, 1),
+                              "roofline_frac": round(byts / hbm / (ms / 1e3), 4), "bound": "HBM"}
+    del o
+    # backward (tpo_backward_f32: grad_x and grad_y) of each kind at L=6, batch 65536
+    bwd = {}
+    for kind in ("gtp_grid", "gtp_fourier", "mtp", "cgtp"):
+        dout = (L + 1) ** 4 if kind == "cgtp" else (2 * L + 1) ** 2
+        go = torch.randn((B, dout), generator=g, device=dev)
+        ms = timeit(lambda: tpo.backward(kind, x, y, go, L, L, 2 * L))
+        byts = 4 * (4 * din + dout) * B  # read x, y, grad_out; write grad_x, grad_y
+        bwd[f"{kind}_L{L}_B{B}"] = {"ms": round(ms, 4), "tp_per_s": round(B / ms * 1e3, 1),
+                                    "gbs": round(byts / ms / 1e6, 1),
+                                    "hbm_frac": round(byts / hbm / (ms / 1e3), 4)}
+        del go
+    res["backward"] = bwd
     return res
 
 

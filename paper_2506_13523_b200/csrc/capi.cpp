@@ -325,6 +325,64 @@ int tpo_weighted_gtp_f32(tpo_ctx* ctx, int L1, int L2, int L3, const double* a, 
   });
 }
 
+namespace {
+// grad (tower 0..Lr) = Gaunt contraction of grad_out (tower 0..L3) with the
+// other input (tower 0..Lo), on the tcgen05 grid kernel: grad_out's degrees
+// (those <= Lr + Lo; higher ones meet no Gaunt triangle) are cut into groups of
+// <= 128 columns (the kernel's K limit), each group one launch on its smallest
+// exact grid (Context::grid_tc_part), partial results summed.  Shapes the
+// kernel cannot take go to the forward path with swapped operands (SIMT).
+void gtp_vjp(tpo_ctx* ctx, int Lr, int Lo, int L3, const float* g, const float* other, float* res, int64_t batch,
+             int64_t channels, int shared, cudaStream_t s) {
+  Context& c = ctx->impl;
+  const int64_t rows = batch * channels;
+  const int Lg = std::min(L3, Lr + Lo);
+  std::vector<std::pair<int, int>> groups;
+  for (int a = 0; a <= Lg;) {
+    int b = a;
+    while (b + 1 <= Lg && (b + 2) * (b + 2) - a * a <= 128) ++b;
+    groups.push_back({a, b});
+    a = b + 1;
+  }
+  bool tc = c.grid_path != 2;
+  for (const auto& gr : groups)
+    if (!c.grid_tc_part(gr.first, gr.second, Lo, Lr).fits) tc = false;
+  if (!tc || groups.empty()) {
+    run_kind(ctx, TPO_KIND_GTP_GRID, L3, Lo, Lr, -1, g, other, res, batch, channels, shared, s);
+    return;
+  }
+  const int64_t dg = static_cast<int64_t>(L3 + 1) * (L3 + 1), dr = static_cast<int64_t>(Lr + 1) * (Lr + 1);
+  const bool direct = groups.size() == 1 && Lg == L3;  // grad_out rows are the operand as they are
+  float* win = nullptr;
+  float* part = nullptr;
+  if (!direct) {
+    int wmax = 0;
+    for (const auto& gr : groups) wmax = std::max(wmax, (gr.second + 1) * (gr.second + 1) - gr.first * gr.first);
+    tpo_b200::cuda_check(cudaMallocAsync(reinterpret_cast<void**>(&win), rows * wmax * sizeof(float), s), "malloc");
+    if (groups.size() > 1)
+      tpo_b200::cuda_check(cudaMallocAsync(reinterpret_cast<void**>(&part), rows * dr * sizeof(float), s), "malloc");
+  }
+  for (size_t i = 0; i < groups.size(); ++i) {
+    const int a = groups[i].first, b = groups[i].second;
+    const int64_t w = static_cast<int64_t>(b + 1) * (b + 1) - static_cast<int64_t>(a) * a;
+    const float* op = g;
+    if (!direct) {  // columns a^2 .. (b+1)^2 - 1 of every grad_out row, packed
+      tpo_b200::cuda_check(cudaMemcpy2DAsync(win, w * sizeof(float), g + static_cast<int64_t>(a) * a, dg * sizeof(float),
+                                             w * sizeof(float), rows, cudaMemcpyDeviceToDevice, s),
+                           "gather grad_out columns");
+      op = win;
+    }
+    float* dst = i == 0 ? res : part;
+    launched(ctx, tpo_b200::launch_gtp_grid_tc(c.grid_tc_part(a, b, Lo, Lr).t, rows_of(op, other, dst, batch, channels, shared),
+                                               c.num_sms(), s),
+             "gtp_grid tcgen05 kernel (backward)");
+    if (i > 0) launched(ctx, tpo_b200::launch_accumulate(part, res, rows * dr, s), "accumulate");
+  }
+  if (win) cudaFreeAsync(win, s);
+  if (part) cudaFreeAsync(part, s);
+}
+}  // namespace
+
 // Vector-Jacobian products (backward) of the four products; the reference has
 // none (its paper benchmarks backward).
 // Every product is bilinear, out_c = sum_ab W_abc x_a y_b, so
@@ -366,8 +424,9 @@ int tpo_backward_f32(tpo_ctx* ctx, int kind, int L1, int L2, int L3, int l_tilde
       case TPO_KIND_GTP_FOURIER: {
         check_L3(L3, "gtp backward");
         if (L3 > kMaxL) throw InvalidArgument("gtp backward: L3 above the supported input maximum");
-        if (grad_x) run_kind(ctx, TPO_KIND_GTP_GRID, L3, L2, L1, -1, grad_out, y, grad_x, batch, channels, y_shared, s);
-        if (grad_y) run_kind(ctx, TPO_KIND_GTP_GRID, L3, L1, L2, -1, grad_out, x, grad_y, batch, channels, 0, s);
+        if (rows == 0) return;
+        if (grad_x) gtp_vjp(ctx, L1, L2, L3, grad_out, y, grad_x, batch, channels, y_shared, s);
+        if (grad_y) gtp_vjp(ctx, L2, L1, L3, grad_out, x, grad_y, batch, channels, 0, s);
         return;
       }
       case TPO_KIND_MTP: {

@@ -63,6 +63,13 @@ Context::Context(int device) : device_(device) {
     throw CudaFailure("device is sm_" + std::to_string(prop.major) + std::to_string(prop.minor) +
                       "; this library is built for sm_100a (B200) only");
   num_sms_ = prop.multiProcessorCount;
+  {  // stream-ordered temporaries (backward / weighted passes) stay mapped between calls
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+      uint64_t keep = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+  }
   cuda_check(cudaStreamCreateWithFlags(&host_stream_, cudaStreamNonBlocking), "cudaStreamCreate");
   cuda_check(cudaStreamCreateWithFlags(&h2d_stream_, cudaStreamNonBlocking), "cudaStreamCreate");
   cuda_check(cudaStreamCreateWithFlags(&d2h_stream_, cudaStreamNonBlocking), "cudaStreamCreate");
@@ -506,6 +513,48 @@ const GridTcEntry& Context::grid_tc(int L1, int L2, int L3) {
     for (int gi = 0; gi < ops.G; ++gi)
       ops.a[static_cast<size_t>(o) * ops.G + gi] = gr.weights[gi / gr.n_phi] * phi_scale * s_val(gi, o);
   return grid_tc_.emplace(std::array<int, 3>{L1, L2, L3}, build_dense_tc(ops, "gtp_grid")).first->second;
+}
+
+// Backward operator set of the grid GTP (tpo_backward_f32): input 1 = degrees
+// [a, b] of grad_out (its columns a^2 .. (b+1)^2 - 1), input 2 = the tower
+// 0..L2 of the other input, output tower 0..Lo.  By the symmetry of the real
+// Gaunt coefficients grad = sum_j w_j Y_o(j) G(j) F(j) with G the synthesis of
+// those grad_out degrees: the integrand has degree <= Lo + L2 + b, so the
+// smallest product grid that integrates it exactly has band
+// ceil((Lo + L2 + b) / 2) (GL exact to 2 band + 1 in cos(theta), n_phi = 2 band + 1
+// points exact to frequency 2 band) -- the forward's grid when b = Lo + L2.
+const GridTcEntry& Context::grid_tc_part(int a, int b, int L2, int Lo) {
+  std::lock_guard<std::mutex> g(mu_);
+  const std::array<int, 4> key{a, b, L2, Lo};
+  auto it = grid_tc_part_.find(key);
+  if (it != grid_tc_part_.end()) return it->second;
+  const int band = std::max({(Lo + L2 + b + 1) / 2, Lo, L2, b});
+  const S2Grid& gr = s2_grid(band);
+  DenseOps ops;
+  ops.G = gr.n_theta * gr.n_phi;
+  ops.din1 = (b + 1) * (b + 1) - a * a;
+  ops.din2 = (L2 + 1) * (L2 + 1);
+  ops.dout_eff = (Lo + 1) * (Lo + 1);
+  ops.dout_total = ops.dout_eff;
+  ops.same_s = false;
+  const double phi_scale = 2.0 * M_PI / gr.n_phi;
+  auto s_val = [&](int gidx, int k) -> double {
+    const int j = gidx / gr.n_phi, kk = gidx % gr.n_phi;
+    const int l = static_cast<int>(std::sqrt(static_cast<double>(k)) + 1e-9);
+    const int m = k - l * l - l;
+    return gr.lambda(l, std::abs(m), j) * gr.csm(m, kk);
+  };
+  ops.s1.resize(static_cast<size_t>(ops.G) * ops.din1);
+  for (int gi = 0; gi < ops.G; ++gi)
+    for (int k = 0; k < ops.din1; ++k) ops.s1[static_cast<size_t>(gi) * ops.din1 + k] = s_val(gi, a * a + k);
+  ops.s2.resize(static_cast<size_t>(ops.G) * ops.din2);
+  for (int gi = 0; gi < ops.G; ++gi)
+    for (int k = 0; k < ops.din2; ++k) ops.s2[static_cast<size_t>(gi) * ops.din2 + k] = s_val(gi, k);
+  ops.a.resize(static_cast<size_t>(ops.dout_eff) * ops.G);
+  for (int o = 0; o < ops.dout_eff; ++o)
+    for (int gi = 0; gi < ops.G; ++gi)
+      ops.a[static_cast<size_t>(o) * ops.G + gi] = gr.weights[gi / gr.n_phi] * phi_scale * s_val(gi, o);
+  return grid_tc_part_.emplace(key, build_dense_tc(ops, "gtp_grid backward")).first->second;
 }
 
 // Fourier GTP on the tensor cores.  The reference convolves the two torus

@@ -53,6 +53,8 @@ class Context {
   const std::vector<CgtpTables>& cgtp_bwd(int L1, int L2, int wrt);
   const CgtpTcTables* cgtp_tc(int L1, int L2);  // nullptr: shape not on the tcgen05 block path
   const GridTcEntry& grid_tc(int L1, int L2, int L3);
+  // backward: grad_out degrees [a, b] x tower L2 -> tower Lo, smallest exact grid
+  const GridTcEntry& grid_tc_part(int a, int b, int L2, int Lo);
   const GridTcEntry& fourier_tc(int L1, int L2, int L3);  // Fourier GTP as torus-grid dense operators
   const GridSimtTables& grid_simt(int L1, int L2, int L3);
   const FourierDevTables& fourier(int L1, int L2, int L3);
@@ -92,6 +94,7 @@ class Context {
   CgtpTables pack_cgtp(const std::vector<std::vector<std::pair<uint32_t, float>>>& per_out, int din1, int din2);
   std::map<std::array<int, 2>, std::pair<bool, CgtpTcTables>> cgtp_tc_;
   std::map<std::array<int, 3>, GridTcEntry> grid_tc_;
+  std::map<std::array<int, 4>, GridTcEntry> grid_tc_part_;
   std::map<std::array<int, 3>, GridTcEntry> fourier_tc_;
   GridTcEntry build_dense_tc(const struct DenseOps& ops, const char* label);
   std::map<std::array<int, 3>, GridSimtTables> grid_simt_;

@@ -124,4 +124,35 @@ cudaError_t launch_scale_degrees(const float* in, float* out, int64_t rows, int 
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------- out += in (backward partial sums)
+namespace {
+__global__ void accumulate_kernel(const float4* __restrict__ in, float4* __restrict__ out, int64_t n4) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n4;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const float4 a = __ldg(in + i);
+    float4 b = out[i];
+    b.x += a.x; b.y += a.y; b.z += a.z; b.w += a.w;
+    out[i] = b;
+  }
+}
+__global__ void accumulate_tail_kernel(const float* __restrict__ in, float* __restrict__ out, int64_t n) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i < n) out[i] += in[i];
+}
+}  // namespace
+
+cudaError_t launch_accumulate(const float* in, float* out, int64_t n, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  const bool vec = (reinterpret_cast<uintptr_t>(in) % 16 == 0) && (reinterpret_cast<uintptr_t>(out) % 16 == 0);
+  const int64_t n4 = vec ? n / 4 : 0;
+  if (n4 > 0) {
+    const int grid = static_cast<int>(std::min<int64_t>((n4 + 255) / 256, 148 * 16));
+    accumulate_kernel<<<grid, 256, 0, s>>>(reinterpret_cast<const float4*>(in), reinterpret_cast<float4*>(out), n4);
+  }
+  const int64_t rem = n - 4 * n4;
+  if (rem > 0)
+    accumulate_tail_kernel<<<static_cast<int>((rem + 255) / 256), 256, 0, s>>>(in + 4 * n4, out + 4 * n4, rem);
+  return cudaGetLastError();
+}
+
 }  // namespace tpo_b200

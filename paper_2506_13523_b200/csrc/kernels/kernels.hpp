@@ -190,5 +190,7 @@ cudaError_t launch_mtp_tc(const MtpTcTables& t, const RowSpec& rs, int num_sms, 
 // x[r][(l,m)] *= w[l] (per-degree scaling, proj/src/gtp.cpp:34-44)
 cudaError_t launch_scale_degrees(const float* in, float* out, int64_t rows, int L, const float* w,
                                  cudaStream_t s);
+// out[i] += in[i], i < n (backward partial sums)
+cudaError_t launch_accumulate(const float* in, float* out, int64_t n, cudaStream_t s);
 
 }  // namespace tpo_b200

@@ -113,13 +113,14 @@ def test_backward_shared_y_channels(tpo, orc, kind, L):
                      L, L, 2 * L)
 
 
-@pytest.mark.parametrize("kind,L", [("gtp_grid", 10), ("gtp_fourier", 6), ("mtp", 6), ("cgtp", 4)])
+@pytest.mark.parametrize("kind,L", [("gtp_grid", 10), ("gtp_fourier", 6), ("mtp", 6), ("cgtp", 4),
+                                    ("gtp_grid", 16), ("gtp_fourier", 16), ("mtp", 16), ("cgtp", 8)])
 def test_backward_bilinearity_full_batch(tpo, kind, L):
     """Size-independent check at the BASELINE batch: <g, T(dx, y)> = <grad_x, dx>
     and <g, T(x, dy)> = <grad_y, dy> per row, through the autograd wrapper."""
     import torch
 
-    B = 65536 if kind != "cgtp" else 8192
+    B = 65536 if kind != "cgtp" and L <= 10 else 4096
     gen = torch.Generator(device="cuda").manual_seed(5)
     D = (L + 1) ** 2
     x = torch.randn(B, D, device="cuda", generator=gen, requires_grad=True)
@@ -138,3 +139,17 @@ def test_backward_bilinearity_full_batch(tpo, kind, L):
         scale = (g.double().abs().sum(1) * 1.0).clamp_min(1.0)
         err = ((lhs - rhs).abs() / scale).max().item()
         assert err < 1e-4, (kind, L, err)
+
+
+@pytest.mark.parametrize("L", [2, 7])
+def test_backward_gtp_simt_path(tpo, orc, L):
+    """The SIMT fallback (grid_path 'simt': forward kernel with swapped operands)
+    gives the same VJP as the tcgen05 degree-group path."""
+    ctx = tpo.context()
+    ctx.set_grid_path("simt")
+    try:
+        x, y, g, gx, gy = _run(tpo, "gtp_grid", L, 4, 600 + L)
+    finally:
+        ctx.set_grid_path("auto")
+    rx, ry = _ref_vjp(orc, "gtp_grid", L, x.astype(np.float64), y.astype(np.float64), g.astype(np.float64))
+    assert _normwise(gx, rx) <= TOL and _normwise(gy, ry) <= TOL
