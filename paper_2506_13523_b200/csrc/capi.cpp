@@ -393,8 +393,8 @@ void gtp_vjp(tpo_ctx* ctx, int Lr, int Lo, int L3, const float* g, const float* 
 //  * MTP: extract is the adjoint of embed and embed(v)^T = embed(P v) with
 //    P = (-1)^l per degree, hence grad_x = mtp(g, P y) and grad_y = mtp(P x, g)
 //    (carrier l~ of the forward; degree-parity pass on the other input);
-//  * CGTP: transposed real-CG term lists on the sparse SIMT kernel
-//    (Context::cgtp_bwd), windows of grad_out columns accumulated.
+//  * CGTP: transposed real-CG term lists (Context::cgtp_bwd, cgtp_bwd.cu),
+//    grad_out swept in shared-memory windows, sums kept in registers.
 // grad_x / grad_y may be null (not computed).  With a shared y (one per batch
 // entry across channels) grad_y would be a channel reduction: not supported.
 int tpo_backward_f32(tpo_ctx* ctx, int kind, int L1, int L2, int L3, int l_tilde, const float* x, const float* y,
@@ -411,13 +411,13 @@ int tpo_backward_f32(tpo_ctx* ctx, int kind, int L1, int L2, int L3, int l_tilde
       case TPO_KIND_CGTP: {
         if (rows == 0) return;
         if (grad_x)
-          for (const auto& t : c.cgtp_bwd(L1, L2, 0))
-            launched(ctx, tpo_b200::launch_cgtp(t, rows_of(grad_out, y, grad_x, batch, channels, y_shared), c.num_sms(), s),
-                     "cgtp backward kernel");
+          launched(ctx, tpo_b200::launch_cgtp_bwd(c.cgtp_bwd(L1, L2, 0), rows_of(grad_out, y, grad_x, batch, channels, y_shared),
+                                                  c.num_sms(), s),
+                   "cgtp backward kernel");
         if (grad_y)
-          for (const auto& t : c.cgtp_bwd(L1, L2, 1))
-            launched(ctx, tpo_b200::launch_cgtp(t, rows_of(grad_out, x, grad_y, batch, channels, 0), c.num_sms(), s),
-                     "cgtp backward kernel");
+          launched(ctx, tpo_b200::launch_cgtp_bwd(c.cgtp_bwd(L1, L2, 1), rows_of(grad_out, x, grad_y, batch, channels, 0),
+                                                  c.num_sms(), s),
+                   "cgtp backward kernel");
         return;
       }
       case TPO_KIND_GTP_GRID:

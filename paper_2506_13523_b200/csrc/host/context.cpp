@@ -174,9 +174,6 @@ CgtpTables Context::pack_cgtp(const std::vector<std::vector<std::pair<uint32_t, 
   t.din2 = din2;
   t.dout = dout;
   t.nchunks = nchunks;
-  t.x_stride = din1;
-  t.x_off = 0;
-  t.accumulate = 0;
   t.terms = upload(terms);
   t.warp_off = upload(off);
   t.warp_nt = upload(nt);
@@ -193,13 +190,10 @@ const CgtpTables& Context::cgtp(int L1, int L2) {
   return cgtp_.emplace(std::array<int, 2>{L1, L2}, t).first->second;
 }
 
-// CGTP backward (vector-Jacobian product) on the same SIMT kernel.  With
-// out[o] = sum_t c_t x[i1_t] y[i2_t]:
+// CGTP backward tables (cgtp_bwd.cu).  With out[o] = sum_t c_t x[i1_t] y[i2_t]:
 //   grad_x[a] = sum_{t: i1_t = a} c_t g[o_t] y[i2_t],  grad_y[b] = sum_{t: i2_t = b} c_t g[o_t] x[i1_t].
-// The kernel's first operand is a window of grad_out columns [o0, o0 + w)
-// (x_off / x_stride), its second the other input (so a per-edge shared y
-// keeps working for grad_x); windows accumulate into the result.
-const std::vector<CgtpTables>& Context::cgtp_bwd(int L1, int L2, int wrt) {
+// Terms are grouped by (virtual output, grad_out window) and packed warp-major.
+const CgtpBwdTables& Context::cgtp_bwd(int L1, int L2, int wrt) {
   std::lock_guard<std::mutex> g(mu_);
   auto it = cgtp_bwd_.find({L1, L2, wrt});
   if (it != cgtp_bwd_.end()) return it->second;
@@ -207,25 +201,61 @@ const std::vector<CgtpTables>& Context::cgtp_bwd(int L1, int L2, int wrt) {
   const int dres = wrt == 0 ? din1 : din2, dother = wrt == 0 ? din2 : din1;
   const TermList fwd = cgtp_terms(L1, L2);
   const int dout = static_cast<int>(fwd.size());
-  // window width: shared tile (w + dother) * 36 floats stays <= ~95 KB (two blocks per SM)
-  const int wmax = std::max(64, 660 - dother) / 4 * 4;
-  std::vector<CgtpTables> tabs;
-  for (int o0 = 0; o0 < dout; o0 += wmax) {
-    const int w = std::min(wmax, dout - o0);
-    TermList per_res(dres);
-    for (int o = o0; o < o0 + w; ++o)
-      for (const auto& tm : fwd[o]) {
-        const uint32_t i1 = tm.first & 0xFFFFu, i2 = tm.first >> 16;
-        const uint32_t res = wrt == 0 ? i1 : i2, oth = wrt == 0 ? i2 : i1;
-        per_res[res].push_back({static_cast<uint32_t>(o - o0) | (oth << 16), tm.second});
+  CgtpBwdTables t{};
+  // window: up to 256 columns (tile 36 KB; measured 256 vs 480: L=4 0.66 vs 0.82 ms, L=8 15.7 vs 20.3 ms)
+  const char* w_s = std::getenv("TPO_CGTP_BWD_W");  // A/B experiments only
+  t.dwin = std::min(dout, w_s ? std::max(16, std::atoi(w_s)) : 256);
+  t.nwin = (dout + t.dwin - 1) / t.dwin;
+  t.dother = dother;
+  t.dres = dres;
+  const char* split_s = std::getenv("TPO_CGTP_BWD_SPLIT");  // A/B experiments only
+  const int smax = std::max(1, kCgtpChunk / dres);
+  t.nsplit = split_s ? std::max(1, std::min(std::atoi(split_s), smax)) : smax;
+  const int nvirt = t.nsplit * dres;
+  t.nchunks = (nvirt + kCgtpChunk - 1) / kCgtpChunk;
+  t.g_stride = dout;
+  // per (virtual output, window): {(o - w * dwin) | i_other << 16, c}
+  std::vector<std::vector<std::vector<std::pair<uint32_t, float>>>> lists(
+      nvirt, std::vector<std::vector<std::pair<uint32_t, float>>>(t.nwin));
+  std::vector<int> count(dres, 0);
+  for (int o = 0; o < dout; ++o)
+    for (const auto& tm : fwd[o]) {
+      const uint32_t i1 = tm.first & 0xFFFFu, i2 = tm.first >> 16;
+      const int a = static_cast<int>(wrt == 0 ? i1 : i2);
+      const uint32_t oth = wrt == 0 ? i2 : i1;
+      const int v = (count[a]++ % t.nsplit) * dres + a;
+      const int w = o / t.dwin;
+      lists[v][w].push_back({static_cast<uint32_t>(o - w * t.dwin) | (oth << 16), tm.second});
+    }
+  const int nwarps = kCgtpChunk / 32;
+  std::vector<int> off(static_cast<size_t>(t.nchunks) * t.nwin * nwarps), nt(off.size());
+  std::vector<uint2> terms;
+  for (int q = 0; q < t.nchunks; ++q)
+    for (int w = 0; w < t.nwin; ++w)
+      for (int wp = 0; wp < nwarps; ++wp) {
+        const size_t idx = (static_cast<size_t>(q) * t.nwin + w) * nwarps + wp;
+        int tmax = 0;
+        for (int l = 0; l < 32; ++l) {
+          const int v = q * kCgtpChunk + wp * 32 + l;
+          if (v < nvirt) tmax = std::max<int>(tmax, static_cast<int>(lists[v][w].size()));
+        }
+        off[idx] = static_cast<int>(terms.size());
+        nt[idx] = tmax;
+        terms.resize(terms.size() + static_cast<size_t>(tmax) * 32, make_uint2(0u, 0u));  // padding: coef 0
+        for (int l = 0; l < 32; ++l) {
+          const int v = q * kCgtpChunk + wp * 32 + l;
+          if (v >= nvirt) continue;
+          for (size_t k = 0; k < lists[v][w].size(); ++k) {
+            uint32_t cb;
+            std::memcpy(&cb, &lists[v][w][k].second, 4);
+            terms[off[idx] + k * 32 + l] = make_uint2(lists[v][w][k].first, cb);
+          }
+        }
       }
-    CgtpTables t = pack_cgtp(per_res, w, dother);
-    t.x_stride = dout;
-    t.x_off = o0;
-    t.accumulate = o0 > 0 ? 1 : 0;
-    tabs.push_back(t);
-  }
-  return cgtp_bwd_.emplace(std::array<int, 3>{L1, L2, wrt}, std::move(tabs)).first->second;
+  t.terms = upload(terms);
+  t.warp_off = upload(off);
+  t.warp_nt = upload(nt);
+  return cgtp_bwd_.emplace(std::array<int, 3>{L1, L2, wrt}, t).first->second;
 }
 
 // ------------------------------------------------------------------ GTP grid (tcgen05)

@@ -49,8 +49,8 @@ class Context {
   void activate() const;
 
   const CgtpTables& cgtp(int L1, int L2);
-  // backward term tables (wrt 0: grad_x, 1: grad_y), one per window of grad_out columns
-  const std::vector<CgtpTables>& cgtp_bwd(int L1, int L2, int wrt);
+  // backward term tables (wrt 0: grad_x, 1: grad_y), cgtp_bwd.cu
+  const CgtpBwdTables& cgtp_bwd(int L1, int L2, int wrt);
   const CgtpTcTables* cgtp_tc(int L1, int L2);  // nullptr: shape not on the tcgen05 block path
   const GridTcEntry& grid_tc(int L1, int L2, int L3);
   // backward: grad_out degrees [a, b] x tower L2 -> tower Lo, smallest exact grid
@@ -90,7 +90,7 @@ class Context {
   std::mutex mu_;
   std::vector<void*> allocs_;
   std::map<std::array<int, 2>, CgtpTables> cgtp_;
-  std::map<std::array<int, 3>, std::vector<CgtpTables>> cgtp_bwd_;
+  std::map<std::array<int, 3>, CgtpBwdTables> cgtp_bwd_;
   CgtpTables pack_cgtp(const std::vector<std::vector<std::pair<uint32_t, float>>>& per_out, int din1, int din2);
   std::map<std::array<int, 2>, std::pair<bool, CgtpTcTables>> cgtp_tc_;
   std::map<std::array<int, 3>, GridTcEntry> grid_tc_;

@@ -55,7 +55,8 @@ __global__ void __launch_bounds__(kCgtpChunk)
       const int e = tid + q * kCgtpChunk;
       const int r = e & (kRows - 1), k = e >> 5;
       const int64_t g = row0 + r;
-      px[q] = (k < t.din1 && tile < ntiles && g < rs.rows) ? __ldg(rs.x + g * t.x_stride + t.x_off + k) : 0.f;
+      px[q] = (k < t.din1 && tile < ntiles && g < rs.rows) ? __ldg(rs.x + g * t.din1 + k) : 0.f;
+
     }
   };
   int b = 0;
@@ -78,7 +79,7 @@ __global__ void __launch_bounds__(kCgtpChunk)
       __syncthreads();  // single buffer: previous tile's readers are done
       for (int i = tid; i < kRows * t.din1; i += kCgtpChunk) {  // coalesced rows
         const int r = i / t.din1, k = i - r * t.din1;
-        xs[k * kPitch + r] = r < nr ? __ldg(rs.x + (row0 + r) * t.x_stride + t.x_off + k) : 0.f;
+        xs[k * kPitch + r] = r < nr ? __ldg(rs.x + row0 * t.din1 + i) : 0.f;
       }
       if (!kEdgeTile)
         for (int i = tid; i < kRows * t.din2; i += kCgtpChunk) {
@@ -131,11 +132,7 @@ __global__ void __launch_bounds__(kCgtpChunk)
         float* op = rs.out + row0 * t.dout + o;
 #pragma unroll
         for (int r = 0; r < kRows; ++r)
-          if (r < nr) {
-            const float v = (r & 1) ? acc[r >> 1].y : acc[r >> 1].x;
-            float* d = op + static_cast<int64_t>(r) * t.dout;
-            *d = t.accumulate ? *d + v : v;
-          }
+          if (r < nr) op[static_cast<int64_t>(r) * t.dout] = (r & 1) ? acc[r >> 1].y : acc[r >> 1].x;
       }
     }
   }

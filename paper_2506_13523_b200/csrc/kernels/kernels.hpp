@@ -29,15 +29,28 @@ struct RowSpec {
 constexpr int kCgtpChunk = 256;
 struct CgtpTables {
   int din1, din2, dout, nchunks;
-  // x rows are read as x[r * x_stride + x_off + i1] (forward: x_stride = din1, x_off = 0; the
-  // backward tables sweep windows of grad_out columns); accumulate: out += instead of out =
-  int64_t x_stride;
-  int x_off, accumulate;
   const uint2* terms;
   const int* warp_off;  // [nchunks * kCgtpChunk / 32]
   const int* warp_nt;   // [nchunks * kCgtpChunk / 32]
 };
 cudaError_t launch_cgtp(const CgtpTables& t, const RowSpec& rs, int num_sms, cudaStream_t s);
+
+// CGTP backward (cgtp_bwd.cu): grad[a] = sum_t c_t g[o_t] v[i_t] over the
+// transposed term lists (a = coefficient of the input the gradient is for,
+// v = the other input, g = grad_out).  A block owns 32 rows and sweeps grad_out
+// in windows of dwin columns staged in shared memory, accumulating in
+// registers; the term list of output a is dealt over nsplit virtual outputs
+// p * dres + a (nsplit * dres <= kCgtpChunk) reduced through shared memory.
+//   term t of virtual output v, window w: terms[warp_off[(q * nwin + w) * 8 + (v % 256) / 32] + t * 32 + v % 32],
+//   q = v / 256, t < warp_nt[same index]; term.x = (o - w * dwin) | i << 16.
+struct CgtpBwdTables {
+  int dwin, nwin, dother, dres, nsplit, nchunks;
+  int64_t g_stride;  // grad_out row length (forward Dout)
+  const uint2* terms;
+  const int* warp_off;
+  const int* warp_nt;
+};
+cudaError_t launch_cgtp_bwd(const CgtpBwdTables& t, const RowSpec& rs, int num_sms, cudaStream_t s);
 
 // Shared-y CGTP (one y per edge, channels a multiple of 128) as per-edge dense
 // GEMMs on tcgen05: out[c] = x[c] . M_y (cgtp_edge_tc.cu).  tm_out: 2-D TMA
