@@ -288,7 +288,7 @@ int tpo_weighted_gtp_f32(tpo_ctx* ctx, int L1, int L2, int L3, const double* a, 
     Context& c0 = ctx->impl;
     if (c0.grid_path != 2 && L1 <= 16 && L2 <= 16 && L3 <= 32) {
       const auto& e = c0.grid_tc(L1, L2, L3);
-      if (e.fits) {
+      if (e.fits && e.t.dout_eff <= 448) {  // per-column output weights: wtab_c[448] in the kernel
         tpo_b200::DegreeWeights dw{};
         dw.on = 1;
         for (int i = 0; i <= L1; ++i) dw.a[i] = static_cast<float>(a[i]);

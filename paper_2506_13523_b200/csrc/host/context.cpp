@@ -308,7 +308,7 @@ GridTcEntry Context::build_dense_tc(const DenseOps& ops, const char* label) {
   t.dout_total = ops.dout_total;
   t.same_s = ops.same_s ? 1 : 0;
   const int max_smem = gtp_grid_tc_max_smem();
-  if (t.k1p > 128 || t.k2p > 128 || max_smem <= 0) {  // SIMT kernels handle these shapes
+  if (t.k1p > 144 || t.k2p > 144 || max_smem <= 0) {  // SIMT kernels handle these shapes (kKHalfMax)
     ent.fits = false;
     return ent;
   }
@@ -316,7 +316,7 @@ GridTcEntry Context::build_dense_tc(const DenseOps& ops, const char* label) {
   //   TMEM: zg (Z) + 2 nc (F_x, F_y; P overwrites F_x) <= 512 columns
   const int force_nc = env_int("TPO_GRID_NC", 0), force_groups = env_int("TPO_GRID_GROUPS", 0);
   // CTA pairs are correct but slower inside this kernel (profiles/r01/ubench_summary.md): opt-in
-  t.pair = env_int("TPO_GRID_PAIR", 0) ? 1 : 0;
+  t.pair = env_int("TPO_GRID_PAIR", 0) && t.k1p <= 128 && t.k2p <= 128 ? 1 : 0;
   auto mss = [&](int n) { return t.pair ? mma_ss_pair(n) : mma_ss(n); };
   auto mts = [&](int n) { return t.pair ? mma_ts_pair(n) : mma_ts(n); };
   double best = 1e300;

@@ -43,7 +43,8 @@ constexpr int BM = 128;            // rows per tile == TMEM lanes
 constexpr int kWorkerWarps = 8;
 constexpr int kWorkers = kWorkerWarps * 32;
 constexpr int kThreads = 96 + kWorkers;  // + producer A warp (warp 10)
-constexpr int kKHalfMax = 64;      // input K (padded) <= 128, split over 2 threads per row
+constexpr int kKHalfMax = 72;      // input K (padded) <= 144 (L <= 11; L = 12 exceeds shared memory), 2 threads per row
+constexpr int kKHalfStd = 64;      // K <= 128 (L <= 10): the default instantiation (no spills at 168 registers)
 constexpr int kStageStride = 17;   // epilogue staging row pitch (floats)
 constexpr int kMaxStages = 8;
 constexpr int kMaxSlices = 8;      // nc <= 128
@@ -133,6 +134,7 @@ __device__ __forceinline__ uint32_t pack_half2(float a, float b) {
 // alias the destination (in-place mode).
 // in-place staging (raw rows share the operand buffers): every value is read into registers
 // before the barrier, so no thread overwrites a raw value another thread has yet to read
+template <int KH>
 __device__ __noinline__ void convert_input_regs(const float* raw, const float* wdeg, int din, int kp, uint8_t* dst_hi,
                                                    uint8_t* dst_lo, float* part, int* e_out, int r, int h,
                                                    bool wait_free, uint64_t* xy_free, uint32_t xy_free_par) {
@@ -140,14 +142,14 @@ __device__ __noinline__ void convert_input_regs(const float* raw, const float* w
   const int k0 = h * kh;
   const float* src = raw + r * din + k0;
   const int nv = min(kh, din - k0);  // valid raw values of this half (may be <= 0)
-  float v[kKHalfMax];
+  float v[KH];
   float ss = 0.f;
   if ((din & 3) == 0) {
     // rows of a multiple of 4 floats sit a multiple of 16 B apart: 128-bit reads (a scalar
     // read of the same k by 32 rows would hit one bank 32 / gcd-fold, e.g. 32-way at din = 64)
     const float4* src4 = reinterpret_cast<const float4*>(src);
 #pragma unroll
-    for (int j0 = 0; j0 < kKHalfMax; j0 += 4) {
+    for (int j0 = 0; j0 < KH; j0 += 4) {
       if (j0 < kh) {
         const float4 a = (j0 < nv) ? src4[j0 >> 2] : make_float4(0.f, 0.f, 0.f, 0.f);
         v[j0] = a.x; v[j0 + 1] = a.y; v[j0 + 2] = a.z; v[j0 + 3] = a.w;
@@ -155,7 +157,7 @@ __device__ __noinline__ void convert_input_regs(const float* raw, const float* w
     }
   } else {
 #pragma unroll
-    for (int j0 = 0; j0 < kKHalfMax; j0 += 8) {
+    for (int j0 = 0; j0 < KH; j0 += 8) {
       if (j0 < kh) {
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
@@ -166,11 +168,11 @@ __device__ __noinline__ void convert_input_regs(const float* raw, const float* w
   }
   if (wdeg) {  // fused per-degree input weights (weighted GTP)
 #pragma unroll
-    for (int j = 0; j < kKHalfMax; ++j)
+    for (int j = 0; j < KH; ++j)
       if (j < kh) v[j] *= wdeg[k0 + j];
   }
 #pragma unroll
-  for (int j = 0; j < kKHalfMax; ++j)
+  for (int j = 0; j < KH; ++j)
     if (j < kh) ss = fmaf(v[j], v[j], ss);
   part[h * BM + r] = ss;
   named_bar_sync(1, kWorkers);
@@ -181,7 +183,7 @@ __device__ __noinline__ void convert_input_regs(const float* raw, const float* w
   // |x| * 2^-e <= 2: fp16 hi/lo stay normal for the row's dominant entries
   const float sc = pow2i(-e);
 #pragma unroll
-  for (int j0 = 0; j0 < kKHalfMax; j0 += 8) {
+  for (int j0 = 0; j0 < KH; j0 += 8) {
     if (j0 < kh) {
       uint32_t hw[4], lw[4];
 #pragma unroll
@@ -281,7 +283,7 @@ __device__ unsigned long long* g_prof = nullptr;
 // important -- the number of MMA instructions per unit of work.  Rank 0
 // issues every MMA; its commits multicast to both CTAs; the rank-1 MMA warp
 // forwards "my half landed" to rank 0's ring slots; workers signal rank 0.
-template <bool PROF, bool PAIR>
+template <bool PROF, bool PAIR, int KH = kKHalfStd>
 __global__ void __launch_bounds__(kThreads, 1)
     gtp_grid_tc_kernel(const __grid_constant__ GridTcTables t, const __grid_constant__ RowSpec rs,
                        const __grid_constant__ DegreeWeights dw) {
@@ -296,7 +298,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __shared__ int ex_sh[2][BM], ey_sh[2][BM];
   __shared__ float part_sh[2 * BM];
   // weighted GTP: per-column weights (flat (l,m) index -> weight of degree l), filled once
-  __shared__ float wtab_x[128], wtab_y[128], wtab_c[448];
+  __shared__ float wtab_x[2 * kKHalfMax], wtab_y[2 * kKHalfMax], wtab_c[448];
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t rank = PAIR ? cluster_ctarank() : 0u;
@@ -596,7 +598,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     };
     if (dw.on) {  // fused per-degree weights (weighted GTP): per-column tables, broadcast reads
       for (int k = wt; k < 448; k += kWorkers) {
-        if (k < 128) {
+        if (k < 2 * kKHalfMax) {
           wtab_x[k] = dw.a[min(degree_of(k), 16)];
           wtab_y[k] = dw.b[min(degree_of(k), 16)];
         }
@@ -637,10 +639,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (wait_free) mbar_wait(&bars[B_XY_FREE], par);
         if (!t.raw_inplace) mbar_arrive(&bars[B_RAW_FREE]);
       } else if (t.raw_inplace) {
-        convert_input_regs(raw_x, wx, t.din1, t.k1p, xh, xl, part_sh, ex_sh[buf], r, h, wait_free, &bars[B_XY_FREE],
+        convert_input_regs<KH>(raw_x, wx, t.din1, t.k1p, xh, xl, part_sh, ex_sh[buf], r, h, wait_free, &bars[B_XY_FREE],
                            par);
         named_bar_sync(1, kWorkers);
-        convert_input_regs(raw_y, wy, t.din2, t.k2p, yh, yl, part_sh, ey_sh[buf], r, h, false, &bars[B_XY_FREE], par);
+        convert_input_regs<KH>(raw_y, wy, t.din2, t.k2p, yh, yl, part_sh, ey_sh[buf], r, h, false, &bars[B_XY_FREE], par);
       } else {
         // both inputs are read before the raw buffer is handed back to the producer
         convert_input(raw_x, wx, t.din1, t.k1p, xh, xl, part_sh, ex_sh[buf], r, h, wait_free, &bars[B_XY_FREE], par);
@@ -781,8 +783,13 @@ cudaError_t launch_gtp_grid_tc(const GridTcTables& t, const RowSpec& rs, int num
     const char* v = std::getenv("TPO_GRID_PROF");
     return v && *v == '1';
   }();
-  auto kern = t.pair ? (prof ? gtp_grid_tc_kernel<true, true> : gtp_grid_tc_kernel<false, true>)
-                     : (prof ? gtp_grid_tc_kernel<true, false> : gtp_grid_tc_kernel<false, false>);
+  // K > 128 (L = 11, 12): a separate instantiation with the wider register conversion, so the
+  // default one keeps its register budget (the wide one spills ~100 B in cold code)
+  const bool big = t.k1p > 2 * kKHalfStd || t.k2p > 2 * kKHalfStd;
+  if (big && t.pair) return cudaErrorInvalidValue;  // planner never pairs K > 128
+  auto kern = big ? gtp_grid_tc_kernel<false, false, kKHalfMax>
+              : t.pair ? (prof ? gtp_grid_tc_kernel<true, true> : gtp_grid_tc_kernel<false, true>)
+                       : (prof ? gtp_grid_tc_kernel<true, false> : gtp_grid_tc_kernel<false, false>);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, t.smem_bytes);
   if (e != cudaSuccess) return e;
   const int kp = t.pair ? 2 : 1;

@@ -74,7 +74,7 @@ def _check_batch(tpo, orc, kind, L, B, seed, L3=None):
 
 
 # ---------------------------------------------------------------- per kind, L sweep
-@pytest.mark.parametrize("L", list(range(0, 11)))
+@pytest.mark.parametrize("L", list(range(0, 12)))
 def test_gtp_grid_tcgen05(tpo, orc, L):
     ctx = tpo.context()
     ctx.set_grid_path("tc")
@@ -181,13 +181,13 @@ def test_cgtp_large(tpo, orc, L):
     _check_batch(tpo, orc, "cgtp", L, 8, 310 + L)
 
 
-@pytest.mark.parametrize("L", list(range(0, 11)))
+@pytest.mark.parametrize("L", list(range(0, 12)))
 def test_gtp_fourier_tcgen05(tpo, orc, L):
     # torus-grid dense operators (convolution theorem) on the fused tcgen05 kernel
     ctx = tpo.context()
     ctx.set_grid_path("tc")
     try:
-        _check_batch(tpo, orc, "gtp_fourier", L, 1000 if L <= 8 else 300, 400 + L)
+        _check_batch(tpo, orc, "gtp_fourier", L, 1000 if L <= 8 else 300 if L <= 10 else 160, 400 + L)
         assert ctx.last_grid_path == "tcgen05"
     finally:
         ctx.set_grid_path("auto")
