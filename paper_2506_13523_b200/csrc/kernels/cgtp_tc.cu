@@ -40,6 +40,7 @@ constexpr int kKps = 2;      // K-steps per A stage
 constexpr int kDCols = 192;  // TMEM: two accumulators [0, 192), [192, 384) ...
 constexpr int kARing = 384;  // ... and the A ring [384, 512): stage sa, K-step j: hi at 32 sa + 16 j, lo + 8
 constexpr int kAStagesTmem = 4;
+constexpr int kXSeg = 33;  // staged x_{l1} segment: 2 l1 + 1 <= 33 (l1 <= 16)
 // barriers: A full [8], A empty [8], B full [8], B empty [8], D full [2], D empty [2]
 constexpr int B_AF = 0, B_AE = 8, B_BF = 16, B_BE = 24, B_DF = 32, B_DE = 34, kBars = 36;
 
@@ -199,7 +200,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // TMEM lane access: warp w reaches lanes 32 (w % 4) ..; two warps per quarter split the K-step
     const int r = 32 * (warp & 3) + lane, h = (warp - 2) >> 2, pt = h * BM + r;
     const uint32_t lbw = tmem + (static_cast<uint32_t>(32 * (warp & 3)) << 16);
-    float* row = rowbuf + r * t.xy_pitch;  // y row (scaled) at [0, din2), x_{l1} (scaled) at [din2, din2 + 21)
+    float* row = rowbuf + r * t.xy_pitch;  // y row (scaled) at [0, din2), x_{l1} (scaled) at [din2, din2 + kXSeg)
     int sa = 0, pa = 0, na = 0, it = 0;    // A ring slot / phase / stages produced
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
       const int64_t g = tile * BM + r;
@@ -250,15 +251,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (un.l1 != cur_l1) {  // restage x_{l1} (both halves are past the previous block)
           named_bar_sync(1, 2 * BM);
           if (h == 0)
-            for (int j = 0; j < 21; ++j)  // zeros past n1: y reads may run into this segment (times 0 in W)
+            for (int j = 0; j < kXSeg; ++j)  // zeros past n1: y reads may run into this segment (times 0 in W)
               row[t.din2 + j] = (ok && j < n1) ? __ldg(xr + un.l1 * un.l1 + j) * sx : 0.f;
           named_bar_sync(1, 2 * BM);
           cur_l1 = un.l1;
         }
         const float* xs = row + t.din2;
         const float* ys = row + un.l2 * un.l2;
-        // chunk c (8 products: x index c / cpr, y offset 8 (c % cpr)); cpr <= 3 for l2 <= 10
-        const int cdiv = cpr == 1 ? 0 : (cpr == 2 ? 1 : 2);
+        // chunk c (8 products: x index c / cpr, y offset 8 (c % cpr)); cpr <= 3 for l2 <= 11
+        const int cdiv = cpr == 1 ? 0 : (cpr == 2 ? 1 : (cpr == 3 ? 2 : 3));
         int c = h;
         for (int ks0 = 0; ks0 < un.ksteps; ks0 += kKps, c += 2 * kKps) {  // one A stage = kKps K-steps
           const long long t0 = now();
@@ -270,7 +271,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int j = 0; j < kKps; ++j) {  // (tail sub-steps past the unit are built but never issued)
             const int cc = c + 2 * j;
-            const int m1 = cdiv == 0 ? cc : (cdiv == 1 ? cc >> 1 : (cc * 0xAAAB) >> 17);
+            const int m1 = cdiv == 0 ? cc : (cdiv == 1 ? cc >> 1 : (cdiv == 2 ? (cc * 0xAAAB) >> 17 : cc / cpr));
             const float xv = m1 < n1 ? xs[m1] : 0.f;
             const float* yp = ys + 8 * (cc - m1 * cpr);
             uint32_t hw[4], lw[4];

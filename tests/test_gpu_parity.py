@@ -122,7 +122,8 @@ def test_cgtp_edge_tiles(tpo, orc, C):
     assert _normwise(out, ref) <= TOL
 
 
-@pytest.mark.parametrize("L,B", [(4, 5000), (5, 148 * 128 * 2 + 77), (6, 148 * 128 + 5), (7, 700), (8, 300), (10, 200)])
+@pytest.mark.parametrize("L,B", [(4, 5000), (5, 148 * 128 * 2 + 77), (6, 148 * 128 + 5), (7, 700), (8, 300), (10, 200),
+                                 (11, 150), (12, 40)])
 def test_cgtp_tensor_cores(tpo, orc, L, B):
     # per-(l1, l2) block GEMMs on tcgen05: several tiles per CTA, ragged tail, rows of
     # very different magnitude (per-row power-of-two scaling)
