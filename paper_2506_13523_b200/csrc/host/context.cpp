@@ -308,7 +308,7 @@ GridTcEntry Context::build_dense_tc(const DenseOps& ops, const char* label) {
   t.dout_total = ops.dout_total;
   t.same_s = ops.same_s ? 1 : 0;
   const int max_smem = gtp_grid_tc_max_smem();
-  if (t.k1p > 144 || t.k2p > 144 || max_smem <= 0) {  // SIMT kernels handle these shapes (kKHalfMax)
+  if (t.k1p > 176 || t.k2p > 176 || max_smem <= 0) {  // SIMT kernels handle these shapes (kKHalfMax)
     ent.fits = false;
     return ent;
   }
@@ -334,6 +334,9 @@ GridTcEntry Context::build_dense_tc(const DenseOps& ops, const char* label) {
       const int nch = (G + cand - 1) / cand;
       const int nc = pad_to((G + nch - 1) / nch, 16);  // rebalance padding over chunks
       const int np = parts_for(zg);
+      // in-place operands + two stages of each ring + epilogue staging must fit (K > 128 is tight)
+      if (static_cast<int>(512u * (t.k1p + t.k2p) + 2u * 64u * (nc + zg / np) + 8u * 32u * 17u * 4u) > max_smem)
+        continue;
       // + ~60 cycles per ring stage for the mbarrier wait when a stage's MMAs lack slack
       const double g1 = 3.0 * ((t.k1p + t.k2p) / 16) * mss(nc) +
                         ((t.k1p + t.k2p) / 16) * std::max(0.0, 60.0 - 3.0 * (mss(nc) - 45.0)) / (t.same_s ? 2 : 1);

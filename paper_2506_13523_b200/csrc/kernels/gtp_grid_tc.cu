@@ -43,7 +43,7 @@ constexpr int BM = 128;            // rows per tile == TMEM lanes
 constexpr int kWorkerWarps = 8;
 constexpr int kWorkers = kWorkerWarps * 32;
 constexpr int kThreads = 96 + kWorkers;  // + producer A warp (warp 10)
-constexpr int kKHalfMax = 72;      // input K (padded) <= 144 (L <= 11; L = 12 exceeds shared memory), 2 threads per row
+constexpr int kKHalfMax = 88;      // input K (padded) <= 176 (L <= 12), split over 2 threads per row
 constexpr int kKHalfStd = 64;      // K <= 128 (L <= 10): the default instantiation (no spills at 168 registers)
 constexpr int kStageStride = 17;   // epilogue staging row pitch (floats)
 constexpr int kMaxStages = 8;

@@ -74,7 +74,7 @@ def _check_batch(tpo, orc, kind, L, B, seed, L3=None):
 
 
 # ---------------------------------------------------------------- per kind, L sweep
-@pytest.mark.parametrize("L", list(range(0, 12)))
+@pytest.mark.parametrize("L", list(range(0, 13)))
 def test_gtp_grid_tcgen05(tpo, orc, L):
     ctx = tpo.context()
     ctx.set_grid_path("tc")
@@ -182,7 +182,7 @@ def test_cgtp_large(tpo, orc, L):
     _check_batch(tpo, orc, "cgtp", L, 8, 310 + L)
 
 
-@pytest.mark.parametrize("L", list(range(0, 12)))
+@pytest.mark.parametrize("L", list(range(0, 13)))
 def test_gtp_fourier_tcgen05(tpo, orc, L):
     # torus-grid dense operators (convolution theorem) on the fused tcgen05 kernel
     ctx = tpo.context()
