@@ -337,10 +337,14 @@ void gtp_vjp(tpo_ctx* ctx, int Lr, int Lo, int L3, const float* g, const float* 
   Context& c = ctx->impl;
   const int64_t rows = batch * channels;
   const int Lg = std::min(L3, Lr + Lo);
+  static const int kmax = [] {  // columns per group (the kernel takes K <= 176)
+    const char* v = std::getenv("TPO_GTP_BWD_K");
+    return v ? std::max(16, std::min(176, std::atoi(v))) : 176;  // 176 vs 128: L=6 0.170 vs 0.357 ms
+  }();
   std::vector<std::pair<int, int>> groups;
   for (int a = 0; a <= Lg;) {
     int b = a;
-    while (b + 1 <= Lg && (b + 2) * (b + 2) - a * a <= 128) ++b;
+    while (b + 1 <= Lg && (b + 2) * (b + 2) - a * a <= kmax) ++b;
     groups.push_back({a, b});
     a = b + 1;
   }
@@ -367,9 +371,7 @@ void gtp_vjp(tpo_ctx* ctx, int Lr, int Lo, int L3, const float* g, const float* 
     const int64_t w = static_cast<int64_t>(b + 1) * (b + 1) - static_cast<int64_t>(a) * a;
     const float* op = g;
     if (!direct) {  // columns a^2 .. (b+1)^2 - 1 of every grad_out row, packed
-      tpo_b200::cuda_check(cudaMemcpy2DAsync(win, w * sizeof(float), g + static_cast<int64_t>(a) * a, dg * sizeof(float),
-                                             w * sizeof(float), rows, cudaMemcpyDeviceToDevice, s),
-                           "gather grad_out columns");
+      launched(ctx, tpo_b200::launch_gather_cols(g, dg, a * a, static_cast<int>(w), win, rows, s), "gather grad_out columns");
       op = win;
     }
     float* dst = i == 0 ? res : part;
@@ -380,6 +382,69 @@ void gtp_vjp(tpo_ctx* ctx, int Lr, int Lo, int L3, const float* g, const float* 
   }
   if (win) cudaFreeAsync(win, s);
   if (part) cudaFreeAsync(part, s);
+}
+}  // namespace
+
+namespace {
+// MTP backward on the tcgen05 MTP kernel.  With P = (-1)^l per degree,
+// grad_x = mtp(g, P y) and grad_y = mtp(P x, g) = P mtp(P g, x); the signs are
+// folded into the embed / extract operators (Context::mtp_tc flags) and
+// grad_out enters as input 1, cut by degree into groups of <= 64 columns (the
+// kernel's K limit); degrees of grad_out above 2 l~ meet zero outputs and are
+// skipped.  Returns false (nothing launched) when a shape does not fit.
+bool mtp_vjp_tc(tpo_ctx* ctx, int L1, int L2, int L3, int lt, const float* x, const float* y, const float* g,
+                float* gx, float* gy, int64_t batch, int64_t channels, int shared, cudaStream_t s) {
+  Context& c = ctx->impl;
+  const int64_t rows = batch * channels;
+  const int Lg = std::min(L3, 2 * lt);
+  std::vector<std::pair<int, int>> groups;
+  for (int a = 0; a <= Lg;) {
+    int b = a;
+    while (b + 1 <= Lg && (b + 2) * (b + 2) - a * a <= 64) ++b;
+    groups.push_back({a, b});
+    a = b + 1;
+  }
+  // (input-2 degree, output degree, flags) per requested gradient
+  struct Job { const float* other; int Lo, Lr, flags; float* res; int shared; };
+  std::vector<Job> jobs;
+  if (gx) jobs.push_back({y, L2, L1, 2, gx, shared});
+  if (gy) jobs.push_back({x, L1, L2, 1 | 4, gy, 0});
+  for (const Job& j : jobs)
+    for (const auto& gr : groups)
+      if (!c.mtp_tc(gr.second, j.Lo, j.Lr, lt, gr.first, j.flags)) return false;
+  const int64_t dg = static_cast<int64_t>(L3 + 1) * (L3 + 1);
+  const bool direct = groups.size() == 1 && Lg == L3;
+  float* win = nullptr;
+  float* part = nullptr;
+  int64_t dr_max = 0;
+  for (const Job& j : jobs) dr_max = std::max<int64_t>(dr_max, static_cast<int64_t>(j.Lr + 1) * (j.Lr + 1));
+  if (!direct) {
+    int wmax = 0;
+    for (const auto& gr : groups) wmax = std::max(wmax, (gr.second + 1) * (gr.second + 1) - gr.first * gr.first);
+    tpo_b200::cuda_check(cudaMallocAsync(reinterpret_cast<void**>(&win), rows * wmax * sizeof(float), s), "malloc");
+    if (groups.size() > 1)
+      tpo_b200::cuda_check(cudaMallocAsync(reinterpret_cast<void**>(&part), rows * dr_max * sizeof(float), s), "malloc");
+  }
+  for (size_t i = 0; i < groups.size(); ++i) {
+    const int a = groups[i].first, b = groups[i].second;
+    const int64_t w = static_cast<int64_t>(b + 1) * (b + 1) - static_cast<int64_t>(a) * a;
+    const float* op = g;
+    if (!direct) {  // columns a^2 .. (b+1)^2 - 1 of every grad_out row, packed
+      launched(ctx, tpo_b200::launch_gather_cols(g, dg, a * a, static_cast<int>(w), win, rows, s), "gather grad_out columns");
+      op = win;
+    }
+    for (const Job& j : jobs) {
+      const int64_t dr = static_cast<int64_t>(j.Lr + 1) * (j.Lr + 1);
+      float* dst = i == 0 ? j.res : part;
+      launched(ctx, tpo_b200::launch_mtp_tc(*c.mtp_tc(b, j.Lo, j.Lr, lt, a, j.flags),
+                                            rows_of(op, j.other, dst, batch, channels, j.shared), c.num_sms(), s),
+               "mtp tcgen05 kernel (backward)");
+      if (i > 0) launched(ctx, tpo_b200::launch_accumulate(part, j.res, rows * dr, s), "accumulate");
+    }
+  }
+  if (win) cudaFreeAsync(win, s);
+  if (part) cudaFreeAsync(part, s);
+  return true;
 }
 }  // namespace
 
@@ -436,6 +501,7 @@ int tpo_backward_f32(tpo_ctx* ctx, int kind, int L1, int L2, int L3, int l_tilde
         if (l_tilde >= 0 && l_tilde < lmin) throw InvalidArgument("mtp: l_tilde below the minimal carrier degree");
         const int lt = l_tilde >= 0 ? l_tilde : lmin;
         if (rows == 0) return;
+        if (mtp_vjp_tc(ctx, L1, L2, L3, lt, x, y, grad_out, grad_x, grad_y, batch, channels, y_shared, s)) return;
         auto parity = [&](int L) {
           std::vector<double> w(L + 1);
           for (int l = 0; l <= L; ++l) w[l] = (l & 1) ? -1.0 : 1.0;

@@ -911,12 +911,16 @@ const CgtpTcTables* Context::cgtp_tc(int L1, int L2) {
 // Dense embed / extract operators in the TMEM orders of mtp_tc.cu
 // (kernels.hpp, MtpTcTables), same CG tables as Context::mtp
 // (proj/src/mtp.cpp:20-97).
-const MtpTcTables* Context::mtp_tc(int L1, int L2, int L3, int lt) {
+// a1 > 0: input 1 holds only degrees a1..L1 (columns (l, m) - a1^2; backward
+// windows of grad_out).  flags: 1 = (-1)^l on input 1, 2 = on input 2, 4 = on
+// the output (the carrier-transpose identities of the MTP backward, capi.cpp).
+const MtpTcTables* Context::mtp_tc(int L1, int L2, int L3, int lt, int a1, int flags) {
   std::lock_guard<std::mutex> g(mu_);
-  auto it = mtp_tc_.find({L1, L2, L3, lt});
+  const std::array<int, 6> key{L1, L2, L3, lt, a1, flags};
+  auto it = mtp_tc_.find(key);
   if (it != mtp_tc_.end()) return it->second.first ? &it->second.second : nullptr;
   auto fail = [&]() -> const MtpTcTables* {
-    mtp_tc_.emplace(std::array<int, 4>{L1, L2, L3, lt}, std::make_pair(false, MtpTcTables{}));
+    mtp_tc_.emplace(key, std::make_pair(false, MtpTcTables{}));
     return nullptr;
   };
   const char* env = std::getenv("TPO_MTP_TC");
@@ -924,7 +928,7 @@ const MtpTcTables* Context::mtp_tc(int L1, int L2, int L3, int lt) {
   if ((env && env[0] == '0') || dt > 13) return fail();
   MtpTcTables t{};
   t.dt = dt;
-  t.din1 = (L1 + 1) * (L1 + 1);
+  t.din1 = (L1 + 1) * (L1 + 1) - a1 * a1;
   t.din2 = (L2 + 1) * (L2 + 1);
   const int L3e = std::min(L3, 2 * lt);
   t.dout_eff = (L3e + 1) * (L3e + 1);
@@ -957,16 +961,17 @@ const MtpTcTables* Context::mtp_tc(int L1, int L2, int L3, int lt) {
   auto xpos = [&](int i, int k) { return k * dt + i; };
   auto ypos = [&](int k, int j) { return k * dt + j; };
   auto zpos = [&](int i, int j) { return i < i1 ? i * dt + j : size0 + (i - i1) * dt + j; };
+  auto sgn = [&](int bit, int l) { return ((flags & bit) && (l & 1)) ? -1.0 : 1.0; };
   for (int l = 0; l <= std::max(L1, L2); ++l)  // proj/src/mtp.cpp:20-39
     for (const CGEntry& e : real_cg(lt, lt, l)) {
       const int a = e.m1 + lt, b = e.m2 + lt, in = flat(l, e.m3);
-      if (l <= L1) e1[static_cast<size_t>(xpos(a, b)) * t.k1 + in] += e.v;
-      if (l <= L2) e2[static_cast<size_t>(ypos(a, b)) * t.k2 + in] += e.v;
+      if (l >= a1 && l <= L1) e1[static_cast<size_t>(xpos(a, b)) * t.k1 + in - a1 * a1] += sgn(1, l) * e.v;
+      if (l <= L2) e2[static_cast<size_t>(ypos(a, b)) * t.k2 + in] += sgn(2, l) * e.v;
     }
   std::vector<double> ex(static_cast<size_t>(t.n2) * t.kz, 0.0);
   for (int l3 = 0; l3 <= L3e; ++l3)  // proj/src/mtp.cpp:60-97
     for (const CGEntry& e : real_cg(lt, lt, l3))
-      ex[static_cast<size_t>(flat(l3, e.m3)) * t.kz + zpos(e.m1 + lt, e.m2 + lt)] += e.v;
+      ex[static_cast<size_t>(flat(l3, e.m3)) * t.kz + zpos(e.m1 + lt, e.m2 + lt)] += sgn(4, l3) * e.v;
   // per K-step [hi | lo][rows x 16] canonical
   auto tile = [&](const std::vector<double>& m, int rows, int kdim) {
     const int nks = kdim / 16;
@@ -1008,7 +1013,7 @@ const MtpTcTables* Context::mtp_tc(int L1, int L2, int L3, int lt) {
     std::fprintf(stderr, "[tpo] mtp tcgen05 dt=%d n1=%d n2=%d k=(%d,%d) kz=%d zcols=(%d,%d,%d,%d) y0=%d stages=%d smem=%d\n",
                  dt, t.n1, t.n2, t.k1, t.k2, t.kz, t.zgrp_col[0], t.zgrp_col[1], t.zgrp_col[2], t.zgrp_col[3],
                  t.y0_reuse, t.stages, t.smem_bytes);
-  return &mtp_tc_.emplace(std::array<int, 4>{L1, L2, L3, lt}, std::make_pair(true, t)).first->second.second;
+  return &mtp_tc_.emplace(key, std::make_pair(true, t)).first->second.second;
 }
 
 const float* Context::degree_weights(const std::vector<double>& w) {

@@ -59,7 +59,8 @@ class Context {
   const GridSimtTables& grid_simt(int L1, int L2, int L3);
   const FourierDevTables& fourier(int L1, int L2, int L3);
   const MtpDevTables& mtp(int L1, int L2, int L3, int lt);
-  const MtpTcTables* mtp_tc(int L1, int L2, int L3, int lt);  // nullptr: shape not on the tcgen05 path
+  // nullptr: shape not on the tcgen05 path; a1 / flags: backward variants (context.cpp)
+  const MtpTcTables* mtp_tc(int L1, int L2, int L3, int lt, int a1 = 0, int flags = 0);
   const float* degree_weights(const std::vector<double>& w);  // small per-call device array
 
   // scratch for host entry points / weighted products (grown on demand)
@@ -100,7 +101,7 @@ class Context {
   std::map<std::array<int, 3>, GridSimtTables> grid_simt_;
   std::map<std::array<int, 3>, FourierDevTables> fourier_;
   std::map<std::array<int, 4>, MtpDevTables> mtp_;
-  std::map<std::array<int, 4>, std::pair<bool, MtpTcTables>> mtp_tc_;
+  std::map<std::array<int, 6>, std::pair<bool, MtpTcTables>> mtp_tc_;
   std::map<std::vector<double>, const float*> weights_;
   std::array<void*, 12> scratch_{};
   std::array<size_t, 12> scratch_cap_{};

@@ -155,4 +155,25 @@ cudaError_t launch_accumulate(const float* in, float* out, int64_t n, cudaStream
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------- column window gather (backward)
+namespace {
+__global__ void gather_cols_kernel(const float* __restrict__ src, int64_t stride, int col0, int w,
+                                   float* __restrict__ dst, int64_t n) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = i / w;
+    dst[i] = __ldg(src + r * stride + col0 + (i - r * w));
+  }
+}
+}  // namespace
+
+cudaError_t launch_gather_cols(const float* src, int64_t stride, int col0, int w, float* dst, int64_t rows,
+                               cudaStream_t s) {
+  const int64_t n = rows * w;
+  if (n <= 0) return cudaSuccess;
+  const int grid = static_cast<int>(std::min<int64_t>((n + 255) / 256, 148 * 16));
+  gather_cols_kernel<<<grid, 256, 0, s>>>(src, stride, col0, w, dst, n);
+  return cudaGetLastError();
+}
+
 }  // namespace tpo_b200

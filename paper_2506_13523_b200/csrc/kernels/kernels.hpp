@@ -205,5 +205,8 @@ cudaError_t launch_scale_degrees(const float* in, float* out, int64_t rows, int 
                                  cudaStream_t s);
 // out[i] += in[i], i < n (backward partial sums)
 cudaError_t launch_accumulate(const float* in, float* out, int64_t n, cudaStream_t s);
+// dst[r][k] = src[r * stride + col0 + k], k < w (backward: a window of grad_out columns, packed)
+cudaError_t launch_gather_cols(const float* src, int64_t stride, int col0, int w, float* dst, int64_t rows,
+                               cudaStream_t s);
 
 }  // namespace tpo_b200
