@@ -819,9 +819,13 @@ const CgtpTcTables* Context::cgtp_tc(int L1, int L2) {
     return nullptr;
   };
   const char* env = std::getenv("TPO_CGTP_TC");
-  // L <= 12: at L = 15 the 3xFP16 split of blocks with K = (2l+1)^2 ~ 900 reaches 1.09e-5 normwise
-  // on rows of mixed magnitude (tests/test_gpu_parity.py), past the 1e-5 contract; SIMT beyond
-  if ((env && env[0] == '0') || L1 > 12 || L2 > 12) return fail();
+  // L <= 14: at L = 15 the 3xFP16 block path reaches 1.1-1.4e-5 normwise on rows of mixed
+  // magnitude (tools/cgtp_tc_accuracy.py), past the 1e-5 contract; SIMT beyond
+  static const int max_l = [] {
+    const char* v = std::getenv("TPO_CGTP_TC_MAXL");  // A/B and accuracy experiments only
+    return v ? std::atoi(v) : 14;  // tools/cgtp_tc_accuracy.py: L=12-14 <= 7.2e-6, L=15 1.1-1.4e-5
+  }();
+  if ((env && env[0] == '0') || L1 > std::min(max_l, 16) || L2 > std::min(max_l, 16)) return fail();
   CgtpTcTables t{};
   t.din1 = (L1 + 1) * (L1 + 1);
   t.din2 = (L2 + 1) * (L2 + 1);

@@ -123,7 +123,7 @@ def test_cgtp_edge_tiles(tpo, orc, C):
 
 
 @pytest.mark.parametrize("L,B", [(4, 5000), (5, 148 * 128 * 2 + 77), (6, 148 * 128 + 5), (7, 700), (8, 300), (10, 200),
-                                 (11, 150), (12, 40)])
+                                 (11, 150), (12, 40), (13, 24), (14, 16)])
 def test_cgtp_tensor_cores(tpo, orc, L, B):
     # per-(l1, l2) block GEMMs on tcgen05: several tiles per CTA, ragged tail, rows of
     # very different magnitude (per-row power-of-two scaling)
