@@ -27,5 +27,25 @@ tpo.weighted_gtp(x, y, np.ones(6), np.ones(6), np.ones(11), 5, 5, 10)
 hx = torch.randn(500, 16).pin_memory(); hy = torch.randn(500, 16).pin_memory()
 ho = torch.empty(500, 49).pin_memory(); hm = torch.empty(500, 49).pin_memory()
 tpo.run_host_batch([("gtp_grid", hx, hy, ho, 3, 3, 6), ("mtp", hx, hy, hm, 3, 3, 6)])
+# K > 128 grid / Fourier instantiation (L = 11, 12), CGTP blocks at L = 13
+for kind, L, B in (("gtp_grid", 11, 130), ("gtp_fourier", 12, 70), ("cgtp", 13, 9)):
+    d = (L + 1) ** 2
+    x = torch.randn((B, d), generator=g, device=dev)
+    y = torch.randn((B, d), generator=g, device=dev)
+    tpo.run(kind, x, y, L, L, 0 if kind == "cgtp" else 2 * L)
+# backward of every kind: degree groups + gather + accumulate (grid L=7, MTP L=6), CGTP kernel,
+# shared-y grad_x
+for kind, L, B in (("gtp_grid", 7, 130), ("gtp_grid", 3, 77), ("mtp", 6, 150), ("mtp", 2, 40),
+                   ("cgtp", 6, 70), ("cgtp", 2, 33)):
+    d = (L + 1) ** 2
+    dout = (L + 1) ** 4 if kind == "cgtp" else (2 * L + 1) ** 2
+    x = torch.randn((B, d), generator=g, device=dev)
+    y = torch.randn((B, d), generator=g, device=dev)
+    go = torch.randn((B, dout), generator=g, device=dev)
+    tpo.backward(kind, x, y, go, L, L, 2 * L)
+x = torch.randn((3, 64, 16), generator=g, device=dev)
+y = torch.randn((3, 16), generator=g, device=dev)
+go = torch.randn((3, 64, 256), generator=g, device=dev)
+tpo.backward("cgtp", x, y, go, 3, 3, 6, need_y=False)
 torch.cuda.synchronize()
 print("sanitize run done")
