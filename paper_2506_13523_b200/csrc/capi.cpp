@@ -119,6 +119,76 @@ void run_cgtp(tpo_ctx* ctx, int L1, int L2, const RowSpec& rs, cudaStream_t s) {
   launched(ctx, tpo_b200::launch_cgtp(t, rs, ctx->impl.num_sms(), s), "cgtp kernel");
 }
 
+// Inputs wider than the tcgen05 kernel's K limit (L > 12): the product is bilinear,
+// so it is the sum over (x degree group, y degree group) of launches on the same
+// operators restricted to those columns (Context::dense_split_tc), input windows
+// packed by a gather kernel, partial outputs accumulated.  Returns false when a
+// part does not fit either.
+// L <= 14: at L = 16 the summed 3xFP16 parts reach 1.02e-5 (grid) / 1.08e-5 (Fourier) normwise,
+// past the 1e-5 contract, and gain little over SIMT (70 vs 81 ms per 2^19 shard)
+constexpr int kMaxSplitL = 14;
+bool run_dense_split(tpo_ctx* ctx, int fourier, int L1, int L2, int L3, const RowSpec& rs, cudaStream_t s) {
+  Context& c = ctx->impl;
+  static const int kmax = [] {
+    const char* v = std::getenv("TPO_GTP_SPLIT_K");
+    return v ? std::max(16, std::min(176, std::atoi(v))) : 128;  // 128 vs 176: L=13 24.0 vs 36.6 ms
+  }();
+  auto groups_of = [](int L) {
+    std::vector<std::pair<int, int>> gs;
+    for (int a = 0; a <= L;) {
+      int b = a;
+      while (b + 1 <= L && (b + 2) * (b + 2) - a * a <= kmax) ++b;
+      gs.push_back({a, b});
+      a = b + 1;
+    }
+    return gs;
+  };
+  const auto g1 = groups_of(L1), g2 = groups_of(L2);
+  for (const auto& u : g1)
+    for (const auto& v : g2)
+      if (!c.dense_split_tc(fourier, L1, L2, L3, u.first, u.second, v.first, v.second).fits) return false;
+  const int64_t rows = rs.rows, yrows = rs.y_shared ? rows / rs.channels : rows;
+  const int64_t d1 = static_cast<int64_t>(L1 + 1) * (L1 + 1), d2 = static_cast<int64_t>(L2 + 1) * (L2 + 1);
+  const int64_t dout = static_cast<int64_t>(L3 + 1) * (L3 + 1);
+  auto width = [](const std::pair<int, int>& r) { return (r.second + 1) * (r.second + 1) - r.first * r.first; };
+  int w1 = 0, w2 = 0;
+  for (const auto& u : g1) w1 = std::max(w1, width(u));
+  for (const auto& v : g2) w2 = std::max(w2, width(v));
+  float *xw = nullptr, *yw = nullptr, *part = nullptr;
+  if (g1.size() > 1) tpo_b200::cuda_check(cudaMallocAsync(reinterpret_cast<void**>(&xw), rows * w1 * sizeof(float), s), "malloc");
+  if (g2.size() > 1) tpo_b200::cuda_check(cudaMallocAsync(reinterpret_cast<void**>(&yw), yrows * w2 * sizeof(float), s), "malloc");
+  tpo_b200::cuda_check(cudaMallocAsync(reinterpret_cast<void**>(&part), rows * dout * sizeof(float), s), "malloc");
+  bool first = true;
+  for (const auto& u : g1) {
+    const float* xp = rs.x;
+    if (g1.size() > 1) {
+      launched(ctx, tpo_b200::launch_gather_cols(rs.x, d1, u.first * u.first, width(u), xw, rows, s), "gather x columns");
+      xp = xw;
+    }
+    for (const auto& v : g2) {
+      const float* yp = rs.y;
+      if (g2.size() > 1) {
+        launched(ctx, tpo_b200::launch_gather_cols(rs.y, d2, v.first * v.first, width(v), yw, yrows, s), "gather y columns");
+        yp = yw;
+      }
+      RowSpec r = rs;
+      r.x = xp;
+      r.y = yp;
+      r.out = first ? rs.out : part;
+      launched(ctx, tpo_b200::launch_gtp_grid_tc(c.dense_split_tc(fourier, L1, L2, L3, u.first, u.second, v.first, v.second).t,
+                                                 r, c.num_sms(), s),
+               "gtp tcgen05 kernel (degree groups)");
+      if (!first) launched(ctx, tpo_b200::launch_accumulate(part, rs.out, rows * dout, s), "accumulate");
+      first = false;
+    }
+  }
+  if (xw) cudaFreeAsync(xw, s);
+  if (yw) cudaFreeAsync(yw, s);
+  cudaFreeAsync(part, s);
+  c.last_grid_path = 1;
+  return true;
+}
+
 void run_grid(tpo_ctx* ctx, int L1, int L2, int L3, const RowSpec& rs, cudaStream_t s) {
   Context& c = ctx->impl;
   if (c.grid_path != 2) {
@@ -128,6 +198,7 @@ void run_grid(tpo_ctx* ctx, int L1, int L2, int L3, const RowSpec& rs, cudaStrea
       launched(ctx, tpo_b200::launch_gtp_grid_tc(e.t, rs, c.num_sms(), s), "gtp_grid tcgen05 kernel");
       return;
     }
+    if (std::max(L1, L2) > 12 && std::max(L1, L2) <= kMaxSplitL && run_dense_split(ctx, 0, L1, L2, L3, rs, s)) return;
     if (c.grid_path == 1) throw InvalidArgument("gtp_grid: shape does not fit the tcgen05 tiling");
   }
   c.last_grid_path = 2;
@@ -146,6 +217,7 @@ void run_fourier(tpo_ctx* ctx, int L1, int L2, int L3, const RowSpec& rs, cudaSt
       launched(ctx, tpo_b200::launch_gtp_grid_tc(e.t, rs, c.num_sms(), s), "gtp_fourier tcgen05 kernel");
       return;
     }
+    if (std::max(L1, L2) > 12 && std::max(L1, L2) <= kMaxSplitL && run_dense_split(ctx, 1, L1, L2, L3, rs, s)) return;
     if (c.grid_path == 1) throw InvalidArgument("gtp_fourier: shape does not fit the tcgen05 tiling");
   }
   c.last_grid_path = 2;

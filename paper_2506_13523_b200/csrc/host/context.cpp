@@ -511,10 +511,8 @@ GridTcEntry Context::build_dense_tc(const DenseOps& ops, const char* label) {
   return ent;
 }
 
-const GridTcEntry& Context::grid_tc(int L1, int L2, int L3) {
-  std::lock_guard<std::mutex> g(mu_);
-  auto it = grid_tc_.find({L1, L2, L3});
-  if (it != grid_tc_.end()) return it->second;
+namespace {
+DenseOps make_grid_ops(int L1, int L2, int L3) {
   // dense operators on the reference's product grid (proj/src/sphere.cpp:105-195, gtp.cpp:228-260)
   const int band = L1 + L2;
   const int L3e = std::min(L3, band);
@@ -545,7 +543,45 @@ const GridTcEntry& Context::grid_tc(int L1, int L2, int L3) {
   for (int o = 0; o < ops.dout_eff; ++o)  // quadrature weight w_j * 2 pi / n_phi
     for (int gi = 0; gi < ops.G; ++gi)
       ops.a[static_cast<size_t>(o) * ops.G + gi] = gr.weights[gi / gr.n_phi] * phi_scale * s_val(gi, o);
-  return grid_tc_.emplace(std::array<int, 3>{L1, L2, L3}, build_dense_tc(ops, "gtp_grid")).first->second;
+  return ops;
+}
+}  // namespace
+
+const GridTcEntry& Context::grid_tc(int L1, int L2, int L3) {
+  std::lock_guard<std::mutex> g(mu_);
+  auto it = grid_tc_.find({L1, L2, L3});
+  if (it != grid_tc_.end()) return it->second;
+  return grid_tc_.emplace(std::array<int, 3>{L1, L2, L3}, build_dense_tc(make_grid_ops(L1, L2, L3), "gtp_grid")).first->second;
+}
+
+namespace {
+DenseOps make_fourier_ops(int L1, int L2, int L3);
+}  // namespace
+
+// Forward GTP (grid or Fourier) with inputs wider than the kernel's K limit: the
+// product is bilinear, so it is the sum over degree groups (x degrees [a1, b1],
+// y degrees [a2, b2]) of the same operators restricted to those columns.
+const GridTcEntry& Context::dense_split_tc(int fourier, int L1, int L2, int L3, int a1, int b1, int a2, int b2) {
+  std::lock_guard<std::mutex> g(mu_);
+  const std::array<int, 8> key{fourier, L1, L2, L3, a1, b1, a2, b2};
+  auto it = dense_split_.find(key);
+  if (it != dense_split_.end()) return it->second;
+  DenseOps full = fourier ? make_fourier_ops(L1, L2, L3) : make_grid_ops(L1, L2, L3);
+  if (full.same_s) full.s2 = full.s1;
+  auto cols = [&](const std::vector<double>& S, int din, int a, int b) {
+    const int c0 = a * a, w = (b + 1) * (b + 1) - c0;
+    std::vector<double> out(static_cast<size_t>(full.G) * w);
+    for (int gi = 0; gi < full.G; ++gi)
+      for (int k = 0; k < w; ++k) out[static_cast<size_t>(gi) * w + k] = S[static_cast<size_t>(gi) * din + c0 + k];
+    return out;
+  };
+  DenseOps ops = full;
+  ops.s1 = cols(full.s1, full.din1, a1, b1);
+  ops.s2 = cols(full.s2, full.din2, a2, b2);
+  ops.din1 = (b1 + 1) * (b1 + 1) - a1 * a1;
+  ops.din2 = (b2 + 1) * (b2 + 1) - a2 * a2;
+  ops.same_s = false;
+  return dense_split_.emplace(key, build_dense_tc(ops, fourier ? "gtp_fourier split" : "gtp_grid split")).first->second;
 }
 
 // Backward operator set of the grid GTP (tpo_backward_f32): input 1 = degrees
@@ -598,7 +634,8 @@ const GridTcEntry& Context::grid_tc_part(int a, int b, int L2, int Lo) {
 // two real dense operators (the torus functions of real inputs are real):
 //   S[(a,b)][k] = Re sum_{(u,v,w) in enc_k} w w_N^(u a + v b),   w_N = exp(2 pi i / N)
 //   A[o][(a,b)] = Re sum_{(U,V,w) in dec_o} w w_N^-(U a + V b) / N^2
-const GridTcEntry& Context::fourier_tc(int L1, int L2, int L3) {
+namespace {
+DenseOps make_fourier_ops(int L1, int L2, int L3) {
   // Torus of N = 4L + 2 points per axis (the reference's n, proj/src/gtp.cpp:58): the
   // product band 4L < N, so the cyclic convolution is exact.  The antipodal extension
   // (proj/src/gtp.cpp:66-74) makes every torus function of a sphere input satisfy
@@ -606,9 +643,6 @@ const GridTcEntry& Context::fourier_tc(int L1, int L2, int L3) {
   // (a, b) with (N - a, b + N/2) (no fixed points), and the pointwise product keeps the
   // symmetry.  So both dense operators need one point per pair: S rows at the
   // representatives b < N/2, A columns summed over each pair -- G = N^2 / 2.
-  std::lock_guard<std::mutex> g(mu_);
-  auto it = fourier_tc_.find({L1, L2, L3});
-  if (it != fourier_tc_.end()) return it->second;
   const int L = std::max(L1, L2);
   const FourierTables& ft = fourier_tables(L);
   const int N = 4 * L + 2, H = N / 2;
@@ -647,7 +681,15 @@ const GridTcEntry& Context::fourier_tc(int L1, int L2, int L3) {
           ops.a[static_cast<size_t>(o) * ops.G + a * H + b] +=
               ((e.w * wn[modn(-ph1)]).real() + (e.w * wn[modn(-ph2)]).real()) * inv;
         }
-  return fourier_tc_.emplace(std::array<int, 3>{L1, L2, L3}, build_dense_tc(ops, "gtp_fourier")).first->second;
+  return ops;
+}
+}  // namespace
+
+const GridTcEntry& Context::fourier_tc(int L1, int L2, int L3) {
+  std::lock_guard<std::mutex> g(mu_);
+  auto it = fourier_tc_.find({L1, L2, L3});
+  if (it != fourier_tc_.end()) return it->second;
+  return fourier_tc_.emplace(std::array<int, 3>{L1, L2, L3}, build_dense_tc(make_fourier_ops(L1, L2, L3), "gtp_fourier")).first->second;
 }
 
 // ------------------------------------------------------------------ GTP grid (SIMT separable)

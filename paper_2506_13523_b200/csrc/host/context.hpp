@@ -53,6 +53,8 @@ class Context {
   const CgtpBwdTables& cgtp_bwd(int L1, int L2, int wrt);
   const CgtpTcTables* cgtp_tc(int L1, int L2);  // nullptr: shape not on the tcgen05 block path
   const GridTcEntry& grid_tc(int L1, int L2, int L3);
+  // forward with inputs past the K limit: x degrees [a1, b1] x y degrees [a2, b2] of the full operators
+  const GridTcEntry& dense_split_tc(int fourier, int L1, int L2, int L3, int a1, int b1, int a2, int b2);
   // backward: grad_out degrees [a, b] x tower L2 -> tower Lo, smallest exact grid
   const GridTcEntry& grid_tc_part(int a, int b, int L2, int Lo);
   const GridTcEntry& fourier_tc(int L1, int L2, int L3);  // Fourier GTP as torus-grid dense operators
@@ -96,6 +98,7 @@ class Context {
   std::map<std::array<int, 2>, std::pair<bool, CgtpTcTables>> cgtp_tc_;
   std::map<std::array<int, 3>, GridTcEntry> grid_tc_;
   std::map<std::array<int, 4>, GridTcEntry> grid_tc_part_;
+  std::map<std::array<int, 8>, GridTcEntry> dense_split_;
   std::map<std::array<int, 3>, GridTcEntry> fourier_tc_;
   GridTcEntry build_dense_tc(const struct DenseOps& ops, const char* label);
   std::map<std::array<int, 3>, GridSimtTables> grid_simt_;

@@ -492,3 +492,16 @@ def test_weighted_gtp_fused(tpo, orc, L, B, C):
     finally:
         ctx.set_grid_path("auto")
     assert _normwise(out_s.reshape(ref.shape), ref) <= TOL
+
+
+@pytest.mark.parametrize("kind,L,B", [("gtp_grid", 13, 200), ("gtp_grid", 14, 60), ("gtp_fourier", 13, 40),
+                                      ("gtp_fourier", 14, 16)])
+def test_gtp_tcgen05_degree_groups(tpo, orc, kind, L, B):
+    # inputs past the kernel's K limit (L = 13, 14): sum of launches over (x, y) degree groups
+    ctx = tpo.context()
+    ctx.set_grid_path("tc")
+    try:
+        _check_batch(tpo, orc, kind, L, B, 700 + L)
+        assert ctx.last_grid_path == "tcgen05"
+    finally:
+        ctx.set_grid_path("auto")

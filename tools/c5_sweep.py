@@ -48,7 +48,7 @@ def main():
             dout = (L + 1) ** 4 if kind == "cgtp" else (2 * L + 1) ** 2
             L3 = 0 if kind == "cgtp" else 2 * L
             B = min(SHARD, max(4096, int(4e9 // (4 * dout)) // 128 * 128))
-            slow = (kind in ("gtp_grid", "gtp_fourier") and L >= 13) or kind == "mtp" and L >= 7
+            slow = kind == "mtp" and L >= 7
             if slow:  # SIMT paths: a 16384-row sample keeps the sweep within minutes
                 B = min(B, 16384)
             g = torch.Generator(device=dev); g.manual_seed(L)
