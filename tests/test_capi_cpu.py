@@ -52,6 +52,25 @@ def test_no_silent_cpu_path():
     x = torch.zeros((2, 9)); y = torch.zeros((2, 9))
     with pytest.raises(ValueError):
         tpo.gtp_grid(x, y, 2, 2, 4)  # CPU tensors are rejected, never computed on host
+    with pytest.raises(ValueError):  # the backward too
+        tpo.backward("gtp_grid", x, y, torch.zeros((2, 25)), 2, 2, 4)
+
+
+def test_backward_abi_argument_errors():
+    """tpo_backward_f32 validates before touching a device: null context / bad
+    kind / shared-y grad_y map to TPO_EINVAL with a message."""
+    import ctypes
+
+    import paper_2506_13523_b200 as tpo
+
+    L = tpo.lib()
+    rc = L.tpo_backward_f32(None, 1, 2, 2, 4, -1, None, None, None, None, None, 0, 1, 0, None)
+    assert rc == 1 and b"null context" in L.tpo_last_error()
+    fake = ctypes.c_void_p(1)  # never dereferenced: the argument checks run first
+    buf = (ctypes.c_float * 64)()
+    p = ctypes.cast(buf, ctypes.c_void_p)
+    rc = L.tpo_backward_f32(fake, 1, 2, 2, 4, -1, p, p, p, p, p, 1, 2, 1, None)
+    assert rc == 1 and b"shared y" in L.tpo_last_error()
 
 
 def test_context_first_call_does_not_deadlock():
