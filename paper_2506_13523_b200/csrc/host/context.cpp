@@ -228,6 +228,8 @@ const CgtpBwdTables& Context::cgtp_bwd(int L1, int L2, int wrt) {
       lists[v][w].push_back({static_cast<uint32_t>(o - w * t.dwin) | (oth << 16), tm.second});
     }
   const int nwarps = kCgtpChunk / 32;
+  const char* ord_s = std::getenv("TPO_CGTP_BWD_ORDER");  // A/B experiments only
+  const bool order_on = !(ord_s && *ord_s == '0');
   std::vector<int> off(static_cast<size_t>(t.nchunks) * t.nwin * nwarps), nt(off.size());
   std::vector<uint2> terms;
   for (int q = 0; q < t.nchunks; ++q)
@@ -242,15 +244,41 @@ const CgtpBwdTables& Context::cgtp_bwd(int L1, int L2, int wrt) {
         off[idx] = static_cast<int>(terms.size());
         nt[idx] = tmax;
         terms.resize(terms.size() + static_cast<size_t>(tmax) * 32, make_uint2(0u, 0u));  // padding: coef 0
+        // step k of the 8 lanes of a quarter warp issue one LDS.128 each into the grad_out tile
+        // (row io) and the other input (row iv): rows 4 banks apart, so lanes whose rows agree
+        // mod 8 (and differ) conflict.  Greedy per step: each lane takes, among the next 16 of
+        // its terms, the one adding the fewest conflicts (same row = broadcast, free)
+        std::vector<std::vector<std::pair<uint32_t, float>>> rest(32);
         for (int l = 0; l < 32; ++l) {
           const int v = q * kCgtpChunk + wp * 32 + l;
-          if (v >= nvirt) continue;
-          for (size_t k = 0; k < lists[v][w].size(); ++k) {
-            uint32_t cb;
-            std::memcpy(&cb, &lists[v][w][k].second, 4);
-            terms[off[idx] + k * 32 + l] = make_uint2(lists[v][w][k].first, cb);
-          }
+          if (v < nvirt) rest[l] = lists[v][w];
         }
+        for (int k = 0; k < tmax; ++k)
+          for (int qq = 0; qq < 4; ++qq) {
+            int cio[8] = {}, civ[8] = {};
+            std::vector<uint32_t> rio, riv;
+            for (int l = qq * 8; l < qq * 8 + 8; ++l) {
+              auto& r = rest[l];
+              if (r.empty()) continue;
+              size_t best = 0;
+              int bc = 1 << 30;
+              for (size_t c = 0; c < std::min<size_t>(order_on ? 16 : 1, r.size()); ++c) {
+                const uint32_t io = r[c].first & 0xFFFFu, iv = r[c].first >> 16;
+                const bool sio = std::find(rio.begin(), rio.end(), io) != rio.end();
+                const bool siv = std::find(riv.begin(), riv.end(), iv) != riv.end();
+                const int cost = (sio ? 0 : cio[io & 7]) + (siv ? 0 : civ[iv & 7]);
+                if (cost < bc) { bc = cost; best = c; }
+              }
+              const auto tm = r[best];
+              r.erase(r.begin() + static_cast<long>(best));
+              const uint32_t io = tm.first & 0xFFFFu, iv = tm.first >> 16;
+              if (std::find(rio.begin(), rio.end(), io) == rio.end()) { rio.push_back(io); ++cio[io & 7]; }
+              if (std::find(riv.begin(), riv.end(), iv) == riv.end()) { riv.push_back(iv); ++civ[iv & 7]; }
+              uint32_t cb;
+              std::memcpy(&cb, &tm.second, 4);
+              terms[off[idx] + static_cast<size_t>(k) * 32 + l] = make_uint2(tm.first, cb);
+            }
+          }
       }
   t.terms = upload(terms);
   t.warp_off = upload(off);
