@@ -505,3 +505,50 @@ def test_gtp_tcgen05_degree_groups(tpo, orc, kind, L, B):
         assert ctx.last_grid_path == "tcgen05"
     finally:
         ctx.set_grid_path("auto")
+
+
+def test_equivariance_report(tpo, orc):
+    """SO(3) equivariance error, reported (north star): 20 Haar rotations per kind and L,
+    max|T(Dx, Dy) - D T(x, y)| / max|T(x, y)| on the GPU outputs (fp32), written to
+    gpurun_out/equivariance.json when run on a GPU box.  Also O(3) where the product has a
+    definite parity: under inversion (x -> (-1)^l x) GTP outputs pick up (-1)^l3 and CGTP paths
+    (-1)^(l1 + l2); the MTP mixes parities across paths (its Sum w * paths includes odd
+    l1 + l2 + l3), so only its SO(3) error is reported."""
+    import json
+    from pathlib import Path
+
+    rep = {}
+    for L in (3, 6, 10):
+        rng = orc.Rng(777 + L)
+        t = orc.tower(L)
+        par_in = np.concatenate([np.full(2 * l + 1, (-1.0) ** l) for l in t])
+        for kind in ("cgtp", "gtp_grid", "gtp_fourier", "mtp"):
+            if kind == "cgtp":
+                out_ls = [l3 for l1 in t for l2 in t for l3 in range(abs(l1 - l2), l1 + l2 + 1)]
+                par_out = np.concatenate([np.full(2 * l3 + 1, (-1.0) ** (l1 + l2)) for l1 in t for l2 in t
+                                          for l3 in range(abs(l1 - l2), l1 + l2 + 1)])
+            else:
+                out_ls = orc.tower(2 * L)
+                par_out = np.concatenate([np.full(2 * l + 1, (-1.0) ** l) for l in out_ls])
+            xs, ys, rots = [], [], []
+            for _ in range(20):
+                x, y = rng.tower(L), rng.tower(L)
+                R = rng.rotation()
+                xs += [x, orc.rotate(t, x, R), par_in * x]
+                ys += [y, orc.rotate(t, y, R), par_in * y]
+                rots.append(R)
+            out = _gpu(tpo, kind, np.stack(xs).astype(np.float32), np.stack(ys).astype(np.float32), L, L, 2 * L)
+            so3, o3 = 0.0, 0.0
+            for i, R in enumerate(rots):
+                base, rot, inv = out[3 * i], out[3 * i + 1], out[3 * i + 2]
+                scale = np.abs(base).max()
+                so3 = max(so3, np.abs(rot - orc.rotate(out_ls, base, R)).max() / scale)
+                o3 = max(o3, np.abs(inv - par_out * base).max() / scale)
+            if kind == "mtp":
+                o3 = None
+            rep[f"{kind}_L{L}"] = {"so3_rel_err": so3, "inversion_rel_err": o3, "rotations": 20}
+            assert so3 < 1e-5 and (o3 is None or o3 < 1e-5), (kind, L, so3, o3)
+    out_dir = Path(__file__).resolve().parents[1] / "gpurun_out"
+    if out_dir.exists():
+        (out_dir / "equivariance.json").write_text(json.dumps(rep, indent=1))
+    print(json.dumps(rep))
