@@ -63,10 +63,11 @@ Context::Context(int device) : device_(device) {
     throw CudaFailure("device is sm_" + std::to_string(prop.major) + std::to_string(prop.minor) +
                       "; this library is built for sm_100a (B200) only");
   num_sms_ = prop.multiProcessorCount;
-  {  // stream-ordered temporaries (backward / weighted passes) stay mapped between calls
+  {  // stream-ordered temporaries (backward / weighted / degree-group passes) stay mapped between
+     // calls up to 4 GiB (re-mapping them per call cost ~1.3 ms); larger pools shrink at syncs
     cudaMemPool_t pool;
     if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
-      uint64_t keep = UINT64_MAX;
+      uint64_t keep = 4ull << 30;
       cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
     }
   }
