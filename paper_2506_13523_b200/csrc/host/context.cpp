@@ -336,7 +336,7 @@ GridTcEntry Context::build_dense_tc(const DenseOps& ops, const char* label) {
   t.dout_eff = ops.dout_eff;
   t.dout_total = ops.dout_total;
   t.same_s = ops.same_s ? 1 : 0;
-  const int max_smem = gtp_grid_tc_max_smem();
+  const int max_smem = gtp_grid_tc_max_smem(t.k1p > 128 || t.k2p > 128);
   if (t.k1p > 176 || t.k2p > 176 || max_smem <= 0) {  // SIMT kernels handle these shapes (kKHalfMax)
     ent.fits = false;
     return ent;

@@ -298,7 +298,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __shared__ int ex_sh[2][BM], ey_sh[2][BM];
   __shared__ float part_sh[2 * BM];
   // weighted GTP: per-column weights (flat (l,m) index -> weight of degree l), filled once
-  __shared__ float wtab_x[2 * kKHalfMax], wtab_y[2 * kKHalfMax], wtab_c[448];
+  __shared__ float wtab_x[2 * KH], wtab_y[2 * KH], wtab_c[448];
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t rank = PAIR ? cluster_ctarank() : 0u;
@@ -598,7 +598,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     };
     if (dw.on) {  // fused per-degree weights (weighted GTP): per-column tables, broadcast reads
       for (int k = wt; k < 448; k += kWorkers) {
-        if (k < 2 * kKHalfMax) {
+        if (k < 2 * KH) {
           wtab_x[k] = dw.a[min(degree_of(k), 16)];
           wtab_y[k] = dw.b[min(degree_of(k), 16)];
         }
@@ -765,9 +765,11 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 }  // namespace
 
-int gtp_grid_tc_max_smem() {
+int gtp_grid_tc_max_smem(bool big_k) {
   cudaFuncAttributes a{};
-  if (cudaFuncGetAttributes(&a, gtp_grid_tc_kernel<false, true>) != cudaSuccess) return 0;
+  if (cudaFuncGetAttributes(&a, big_k ? gtp_grid_tc_kernel<false, false, kKHalfMax> : gtp_grid_tc_kernel<false, true>) !=
+      cudaSuccess)
+    return 0;
   int dev = 0, optin = 0;
   cudaGetDevice(&dev);
   if (cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess) return 0;

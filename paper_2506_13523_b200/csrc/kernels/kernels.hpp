@@ -126,7 +126,7 @@ struct DegreeWeights {
 };
 cudaError_t launch_gtp_grid_tc(const GridTcTables& t, const RowSpec& rs, int num_sms, cudaStream_t s,
                                const DegreeWeights* w = nullptr);
-int gtp_grid_tc_max_smem();
+int gtp_grid_tc_max_smem(bool big_k = false);  // big_k: the K > 128 instantiation
 
 // ---------------------------------------------------------------- GTP grid, SIMT separable
 struct GridSimtTables {
