@@ -103,7 +103,14 @@ void* Context::dev_alloc(size_t bytes) {
 template <class T>
 T* Context::upload(const std::vector<T>& v) {
   void* p = dev_alloc(v.size() * sizeof(T));
-  if (!v.empty()) cuda_check(cudaMemcpy(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice), "upload");
+  if (!v.empty()) {
+    cuda_check(cudaMemcpy(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice), "upload");
+    // a pageable H2D cudaMemcpy may return once the data is staged, before the DMA lands, and
+    // the kernels run on non-blocking streams that do not order after the legacy stream: wait
+    // for the copy here (tables are built once per shape; an intermittent parity failure on
+    // the first call of a new shape was traced to this)
+    cuda_check(cudaStreamSynchronize(cudaStreamLegacy), "upload sync");
+  }
   return static_cast<T*>(p);
 }
 
