@@ -61,7 +61,7 @@ def load_peaks() -> dict:
 class ClockSampler:
     """SM clocks + throttle reasons sampled during the timed region.
 
-    NVML is polled from a thread every ~1 ms (nvidia-smi's 20 ms cadence and
+    NVML is polled from a thread every ~0.2 ms (nvidia-smi's 20 ms cadence and
     process start-up miss a few-ms region entirely); only samples taken while a
     region is open (``with clk.region():``) are summarised.  Falls back to
     ``nvidia-smi -lms 20`` when NVML is unavailable."""
@@ -100,9 +100,9 @@ class ClockSampler:
                         sm = float(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM))
                         r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
                         self.samples.append((sm, {n for n, b in bits if r & b}))
-                    time.sleep(0.001)
+                    time.sleep(0.0002)
 
-            self.source = "nvml (1 ms poll)"
+            self.source = "nvml (0.2 ms poll)"
             self._t = threading.Thread(target=poll, daemon=True)
             self._t.start()
             return self
