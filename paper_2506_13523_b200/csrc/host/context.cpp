@@ -400,12 +400,40 @@ GridTcEntry Context::build_dense_tc(const DenseOps& ops, const char* label) {
   t.nparts = parts_for(t.zg);
   t.zp = t.zg / t.nparts;
   t.safe_war = env_int("TPO_GRID_SAFE_WAR", 1);
+  {
+    // GEMM-2 accumulation segments of <= ~20 K-steps (60 MMAs): tcgen05 accumulates in fp32 with
+    // truncation once per MMA (a per-MMA round-toward-zero model reproduces the measured 1.04e-5 at
+    // L = 12 to three digits; tools/precision_model.py), so one accumulator over the whole grid
+    // (77 K-steps at L = 12) costs ~1e-5 normwise; segments added in fp32 keep it ~3-4e-6
+    const int seg_slices = std::max(1, env_int("TPO_GRID_SEG_SLICES", 20));
+    const int total = t.nchunks * t.nslices;
+    const int nseg = (total + seg_slices - 1) / seg_slices;
+    t.seg_chunks = std::max(1, (t.nchunks + nseg - 1) / nseg);
+  }
+  t.seg_red = env_int("TPO_GRID_SEG_RED", 1);
+  t.split_roles = env_int("TPO_GRID_SPLIT_ROLES", 1);
+  // input scale: |F(g)| <= ||x||_2 ||S row g||_2, so ||x|| < 2^in_shift keeps P = F_x F_y < 2^14
+  {
+    auto row_norm_max = [&](const std::vector<double>& S, int din) {
+      double m = 0.0;
+      for (int gi = 0; gi < G; ++gi) {
+        double ss = 0.0;
+        for (int k = 0; k < din; ++k) ss += S[static_cast<size_t>(gi) * din + k] * S[static_cast<size_t>(gi) * din + k];
+        m = std::max(m, std::sqrt(ss));
+      }
+      return m;
+    };
+    const double n1 = row_norm_max(ops.s1, t.din1), n2 = ops.same_s ? n1 : row_norm_max(ops.s2, t.din2);
+    t.in_shift = std::max(0, std::min(12, static_cast<int>(std::floor((14.0 - std::log2(std::max(n1 * n2, 1e-30))) / 2))));
+  }
   t.dbg = env_int("TPO_GRID_DBG", 0);
 
   // ---- shared memory: X/Y operands, optional separate raw staging, B ring, epilogue staging
   const uint32_t xy = 512u * (t.k1p + t.k2p);
   const uint32_t raw = static_cast<uint32_t>(pad_to(512 * (t.din1 + t.din2), 1024));
-  const uint32_t epi = 8u * 32u * 17u * 4u;
+  // epilogue staging per worker warp: 32 x 17 floats, plus 512 floats of read-back slots when
+  // GEMM 2 runs in several accumulation segments
+  const uint32_t epi = 8u * 32u * 17u * 4u + (t.seg_chunks < t.nchunks && !t.seg_red ? 8u * 512u * 4u : 0u);
   const int force_inplace = env_int("TPO_GRID_INPLACE", -1), force_stages = env_int("TPO_GRID_STAGES", 0);
   // two B-operand rings; prefer the separate raw staging buffer, then depth
   const int kp = t.pair ? 2 : 1;  // each CTA of a pair streams one row half of every slice
@@ -453,14 +481,14 @@ GridTcEntry Context::build_dense_tc(const DenseOps& ops, const char* label) {
   if (env_int("TPO_GRID_VERBOSE", 0))
     std::fprintf(stderr,
                  "[tpo] %s tcgen05 G=%d din=(%d,%d) dout=%d nc=%d chunks=%d groups=%d zg=%d parts=%d s_stages=%d "
-                 "a_stages=%d inplace=%d pair=%d smem=%d\n",
+                 "a_stages=%d inplace=%d pair=%d smem=%d seg_chunks=%d\n",
                  label, G, t.din1, t.din2, t.dout_eff, nc, t.nchunks, t.ngroups, t.zg, t.nparts, s_st, a_st, inplace,
-                 t.pair, t.smem_bytes);
+                 t.pair, t.smem_bytes, t.seg_chunks);
 
   // ---- operators -> fp16 hi / lo slices in the UMMA canonical layout
   double amax = 0.0;
   for (double v : ops.a) amax = std::max(amax, std::abs(v));
-  t.a_shift = amax > 0 ? -(std::ilogb(amax) + 1) : 0;
+  t.a_shift = amax > 0 ? 12 - (std::ilogb(amax) + 1) : 0;  // max |A| 2^a_shift in [2^11, 2^12)
   const double a_scale = std::ldexp(1.0, t.a_shift);
 
   // S slices: [chunk][kstep][hi | lo][nc x 16 canonical]
@@ -945,7 +973,7 @@ const CgtpTcTables* Context::cgtp_tc(int L1, int L2) {
               const int k = ks * 16 + kk, m1 = k / n2p, m2 = k % n2p;
               if (k >= kw || m2 >= n2) continue;
               uint16_t hv, lv;
-              split_half(W[static_cast<size_t>(p * np + r) * n + m1 * n2 + m2], hv, lv);
+              split_half(std::ldexp(W[static_cast<size_t>(p * np + r) * n + m1 * n2 + m2], kTabShift), hv, lv);
               const uint32_t o = sm100::canon_off(r, kk, u.n_pad) / 2;
               hi[o] = hv;
               lo[o] = lv;
@@ -1053,7 +1081,7 @@ const MtpTcTables* Context::mtp_tc(int L1, int L2, int L3, int lt, int a1, int f
   std::vector<double> ex(static_cast<size_t>(t.n2) * t.kz, 0.0);
   for (int l3 = 0; l3 <= L3e; ++l3)  // proj/src/mtp.cpp:60-97
     for (const CGEntry& e : real_cg(lt, lt, l3))
-      ex[static_cast<size_t>(flat(l3, e.m3)) * t.kz + zpos(e.m1 + lt, e.m2 + lt)] += sgn(4, l3) * e.v;
+      ex[static_cast<size_t>(flat(l3, e.m3)) * t.kz + zpos(e.m1 + lt, e.m2 + lt)] += sgn(4, l3) * std::ldexp(e.v, kTabShift);
   // per K-step [hi | lo][rows x 16] canonical
   auto tile = [&](const std::vector<double>& m, int rows, int kdim) {
     const int nks = kdim / 16;

@@ -29,11 +29,6 @@ constexpr int kBoxCols = 32;   // epilogue TMA store box: 128 rows x 32 fp32 (12
 constexpr int kBoxBytes = BM * kBoxCols * 4;
 constexpr int kBoxBufs = 8;
 
-__device__ __forceinline__ float pow2i(int k) { return __int_as_float((127 + k) << 23); }
-__device__ __forceinline__ uint32_t pack_half2(float a, float b) {
-  const __half2 h = __floats2half2_rn(a, b);
-  return *reinterpret_cast<const uint32_t*>(&h);
-}
 
 __device__ __forceinline__ void tma_store_2d(const void* tmap, const void* src, int c0, int c1) {
   asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
@@ -118,20 +113,20 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(&bars[b], (it >> 1) & 1);
       const float* ysb = ys_sh[b];
       if (warp == 4) {
-        float ss = 0.f;
-        for (int k = lane; k < t.din2; k += 32) ss = fmaf(ysb[k], ysb[k], ss);
+        float mx = 0.f;
+        for (int k = lane; k < t.din2; k += 32) mx = fmaxf(mx, fabsf(ysb[k]));
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
-        if (lane == 0) ey_sh[b] = (ss > 0.f && ss < 3.0e38f) ? max(-120, min(120, ilogbf(ss) / 2 + 1)) : 0;
+        for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        if (lane == 0) ey_sh[b] = row_scale_exp(mx, 1) - kInShift;  // max|y| < 2^7: |M_y| < 2^7 sum|c|
       }
       // ---- x row r: norm pass and split pass over shared memory (din1 % 4 == 0 on this path)
       const float4* rx4 = reinterpret_cast<const float4*>(raw + b * BM * t.din1 + r * t.din1);
-      float ss = 0.f;
+      float mx = 0.f;
       for (int k4 = 0; k4 < t.din1 / 4; ++k4) {
         const float4 a = rx4[k4];
-        ss = fmaf(a.x, a.x, fmaf(a.y, a.y, fmaf(a.z, a.z, fmaf(a.w, a.w, ss))));
+        mx = fmaxf(fmaxf(mx, fabsf(a.x)), fmaxf(fabsf(a.y), fmaxf(fabsf(a.z), fabsf(a.w))));
       }
-      const int e = (ss > 0.f && ss < 3.0e38f) ? max(-120, min(120, ilogbf(ss) / 2 + 1)) : 0;
+      const int e = row_scale_exp(mx, 1) - kInShift;
       const float sc = pow2i(-e);
       uint8_t* xh = xh_of(b);
       uint8_t* xl = xh + BM * kp * 2;

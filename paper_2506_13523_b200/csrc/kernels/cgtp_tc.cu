@@ -44,26 +44,10 @@ constexpr int kXSeg = 33;  // staged x_{l1} segment: 2 l1 + 1 <= 33 (l1 <= 16)
 // barriers: A full [8], A empty [8], B full [8], B empty [8], D full [2], D empty [2]
 constexpr int B_AF = 0, B_AE = 8, B_BF = 16, B_BE = 24, B_DF = 32, B_DE = 34, kBars = 36;
 
-__device__ __forceinline__ float pow2i(int k) { return __int_as_float((127 + k) << 23); }
-__device__ __forceinline__ float mul_pow2(float v, int k) {
-  const int k1 = k >> 1;
-  return (v * pow2i(k1)) * pow2i(k - k1);
-}
-__device__ __forceinline__ uint32_t pack_half2(float a, float b) {
-  const __half2 h = __floats2half2_rn(a, b);
-  return *reinterpret_cast<const uint32_t*>(&h);
-}
-__device__ __forceinline__ void cp_async4(float* dst, const float* src) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 __device__ __forceinline__ void tmem_st4(uint32_t taddr, const uint32_t (&r)[4]) {
   asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};" ::"r"(taddr), "r"(r[0]), "r"(r[1]),
                "r"(r[2]), "r"(r[3])
                : "memory");
-}
-__device__ __forceinline__ int norm_exp(float ss) {
-  return (ss > 0.f && ss < 3.0e38f) ? max(-120, min(120, ilogbf(ss) / 2 + 1)) : 0;
 }
 
 // optional in-kernel cycle accounting (env TPO_CGTP_PROF=1), kProfSlots per CTA:
@@ -216,32 +200,32 @@ __global__ void __launch_bounds__(kThreads, 1)
         } else {
           for (int k = 0; k < t.din2; ++k) row[k] = 0.f;
         }
-        float s0 = 0.f, s1 = 0.f;
+        float m0 = 0.f, m1 = 0.f;
         int k = 0;
         for (; k + 2 <= t.din2; k += 2) {
-          s0 = fmaf(row[k], row[k], s0);
-          s1 = fmaf(row[k + 1], row[k + 1], s1);
+          m0 = fmaxf(m0, fabsf(row[k]));
+          m1 = fmaxf(m1, fabsf(row[k + 1]));
         }
-        if (k < t.din2) s0 = fmaf(row[k], row[k], s0);
-        const int ey = norm_exp(s0 + s1);
+        if (k < t.din2) m0 = fmaxf(m0, fabsf(row[k]));
+        const int ey = row_scale_exp(fmaxf(m0, m1), 1) - kInShift;  // max|y| 2^-ey in [2^6, 2^7)
         const float sy = pow2i(-ey);
         for (k = 0; k < t.din2; ++k) row[k] *= sy;
         ey_sh[r] = ey;
       } else {  // x row norm (its degree segments are staged per l1 below)
-        float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+        float m0 = 0.f, m1 = 0.f, m2 = 0.f, m3 = 0.f;
         if (ok) {
           int k = 0;
           for (; k + 4 <= t.din1; k += 4) {
-            const float a0 = __ldg(xr + k), a1 = __ldg(xr + k + 1), a2 = __ldg(xr + k + 2), a3 = __ldg(xr + k + 3);
-            s0 = fmaf(a0, a0, s0); s1 = fmaf(a1, a1, s1); s2 = fmaf(a2, a2, s2); s3 = fmaf(a3, a3, s3);
+            m0 = fmaxf(m0, fabsf(__ldg(xr + k))); m1 = fmaxf(m1, fabsf(__ldg(xr + k + 1)));
+            m2 = fmaxf(m2, fabsf(__ldg(xr + k + 2))); m3 = fmaxf(m3, fabsf(__ldg(xr + k + 3)));
           }
-          for (; k < t.din1; ++k) s0 = fmaf(__ldg(xr + k), __ldg(xr + k), s0);
+          for (; k < t.din1; ++k) m0 = fmaxf(m0, fabsf(__ldg(xr + k)));
         }
-        ex_sh[r] = norm_exp((s0 + s1) + (s2 + s3));
+        ex_sh[r] = row_scale_exp(fmaxf(fmaxf(m0, m1), fmaxf(m2, m3)), 1) - kInShift;
       }
       named_bar_sync(1, 2 * BM);
       const int ex = ex_sh[r];
-      if (h == 0) e_sh[it & 1][r] = ex + ey_sh[r];
+      if (h == 0) e_sh[it & 1][r] = ex + ey_sh[r] - kTabShift;  // W is stored times 2^kTabShift
       const float sx = pow2i(-ex);
       tick(7, ts0);
       int cur_l1 = -1;

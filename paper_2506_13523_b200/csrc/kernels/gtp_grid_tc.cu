@@ -112,38 +112,26 @@ __device__ __forceinline__ bool tile_tma_ok(const RowSpec& rs, int64_t tile) {
          ((reinterpret_cast<uintptr_t>(rs.y) & 15) == 0);
 }
 
-// 2^k for |k| <= 126, exact (exponent bits)
-__device__ __forceinline__ float pow2i(int k) { return __int_as_float((127 + k) << 23); }
 // degree of flat index k = l^2 + m + l (exact for k < 2^20)
 __device__ __forceinline__ int degree_of(int k) { return __float2int_rd(sqrtf(static_cast<float>(k) + 0.5f)); }
-// v * 2^k, exact for |k| <= 252 unless the result itself is subnormal
-__device__ __forceinline__ float mul_pow2(float v, int k) {
-  const int k1 = k >> 1;
-  return (v * pow2i(k1)) * pow2i(k - k1);
-}
-
-__device__ __forceinline__ uint32_t pack_half2(float a, float b) {
-  const __half2 h = __floats2half2_rn(a, b);
-  return *reinterpret_cast<const uint32_t*>(&h);
-}
 
 // Convert one input of the tile: raw fp32 rows [128][din] in shared memory ->
 // fp16 hi / lo in the canonical K-major layout (R = 128, K = kp), each row
-// scaled by 2^-e with ||row||_2 * 2^-e in [0.5, 1).  Thread (r, h) owns half
+// scaled by 2^-e with ||row||_2 * 2^-e < 1 (row_scale_exp).  Thread (r, h) owns half
 // h of row r.  Two phases separated by a worker barrier, so the raw rows may
 // alias the destination (in-place mode).
 // in-place staging (raw rows share the operand buffers): every value is read into registers
 // before the barrier, so no thread overwrites a raw value another thread has yet to read
 template <int KH>
-__device__ __noinline__ void convert_input_regs(const float* raw, const float* wdeg, int din, int kp, uint8_t* dst_hi,
-                                                   uint8_t* dst_lo, float* part, int* e_out, int r, int h,
-                                                   bool wait_free, uint64_t* xy_free, uint32_t xy_free_par) {
+__device__ __noinline__ void convert_input_regs(const float* raw, const float* wdeg, int din, int kp, int in_shift,
+                                                   uint8_t* dst_hi, uint8_t* dst_lo, float* part, int* e_out, int r,
+                                                   int h, bool wait_free, uint64_t* xy_free, uint32_t xy_free_par) {
   const int kh = kp >> 1;  // multiple of 8
   const int k0 = h * kh;
   const float* src = raw + r * din + k0;
   const int nv = min(kh, din - k0);  // valid raw values of this half (may be <= 0)
   float v[KH];
-  float ss = 0.f;
+  float mx = 0.f;
   if ((din & 3) == 0) {
     // rows of a multiple of 4 floats sit a multiple of 16 B apart: 128-bit reads (a scalar
     // read of the same k by 32 rows would hit one bank 32 / gcd-fold, e.g. 32-way at din = 64)
@@ -173,14 +161,13 @@ __device__ __noinline__ void convert_input_regs(const float* raw, const float* w
   }
 #pragma unroll
   for (int j = 0; j < KH; ++j)
-    if (j < kh) ss = fmaf(v[j], v[j], ss);
-  part[h * BM + r] = ss;
+    if (j < kh) mx = fmaxf(mx, fabsf(v[j]));
+  part[h * BM + r] = mx;
   named_bar_sync(1, kWorkers);
   if (wait_free) mbar_wait(xy_free, xy_free_par);  // the previous unit's GEMM 1 has retired
-  const float tot = part[r] + part[BM + r];
-  int e = 0;
-  if (tot > 0.f && tot < 3.0e38f) e = max(-120, min(120, ilogbf(tot) / 2 + 1));
-  // |x| * 2^-e <= 2: fp16 hi/lo stay normal for the row's dominant entries
+  // ||x||_2 2^-e < 2^in_shift: the products F_x F_y stay below 2^14 (host bound), far from fp16's
+  // subnormal range for all but negligible values
+  const int e = row_scale_exp(fmaxf(part[r], part[BM + r]), din) - in_shift;
   const float sc = pow2i(-e);
 #pragma unroll
   for (int j0 = 0; j0 < KH; j0 += 8) {
@@ -202,9 +189,9 @@ __device__ __noinline__ void convert_input_regs(const float* raw, const float* w
   if (h == 0) e_out[r] = e;
 }
 
-__device__ __noinline__ void convert_input(const float* raw, const float* wdeg, int din, int kp, uint8_t* dst_hi,
-                                              uint8_t* dst_lo, float* part, int* e_out, int r, int h, bool wait_free,
-                                              uint64_t* xy_free, uint32_t xy_free_par) {
+__device__ __noinline__ void convert_input(const float* raw, const float* wdeg, int din, int kp, int in_shift,
+                                              uint8_t* dst_hi, uint8_t* dst_lo, float* part, int* e_out, int r, int h,
+                                              bool wait_free, uint64_t* xy_free, uint32_t xy_free_par) {
   // two short passes over the staged row (norm, then scale + split): small code, which
   // matters because this runs once per tile and is otherwise cold in the instruction cache
   const int kh = kp >> 1;  // multiple of 8
@@ -229,24 +216,23 @@ __device__ __noinline__ void convert_input(const float* raw, const float* wdeg, 
       for (int q = 0; q < 8; ++q) v[q] *= wdeg[k0 + j0 + q];
     }
   };
-  float ss0 = 0.f, ss1 = 0.f;
+  float mx0 = 0.f, mx1 = 0.f;
 #pragma unroll 1
   for (int j0 = 0; j0 < kh; j0 += 8) {
     float v[8];
     load8(j0, v);
 #pragma unroll
     for (int q = 0; q < 8; q += 2) {
-      ss0 = fmaf(v[q], v[q], ss0);
-      ss1 = fmaf(v[q + 1], v[q + 1], ss1);
+      mx0 = fmaxf(mx0, fabsf(v[q]));
+      mx1 = fmaxf(mx1, fabsf(v[q + 1]));
     }
   }
-  part[h * BM + r] = ss0 + ss1;
+  part[h * BM + r] = fmaxf(mx0, mx1);
   named_bar_sync(1, kWorkers);
   if (wait_free) mbar_wait(xy_free, xy_free_par);  // the previous unit's GEMM 1 has retired
-  const float tot = part[r] + part[BM + r];
-  int e = 0;
-  if (tot > 0.f && tot < 3.0e38f) e = max(-120, min(120, ilogbf(tot) / 2 + 1));
-  // |x| * 2^-e <= 2: fp16 hi/lo stay normal for the row's dominant entries
+  // ||x||_2 2^-e < 2^in_shift: the products F_x F_y stay below 2^14 (host bound), far from fp16's
+  // subnormal range for all but negligible values
+  const int e = row_scale_exp(fmaxf(part[r], part[BM + r]), din) - in_shift;
   const float sc = pow2i(-e);
 #pragma unroll 1
   for (int j0 = 0; j0 < kh; j0 += 8) {
@@ -308,7 +294,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int i = 0; i < kNumBars; ++i) {
       uint32_t cnt = 1;
       if (i == B_RAW_FREE) cnt = kWorkers;
-      if (i == B_XY_READY || i == B_Z_EMPTY) cnt = kWorkers * kPair;
+      if (i == B_XY_READY) cnt = kWorkers * kPair;
+      if (i == B_Z_EMPTY) cnt = (t.split_roles ? kWorkers / 2 : kWorkers) * kPair;
       if (i >= B_P_READY && i < B_P_READY + kMaxSlices) cnt = BM * kPair;
       mbar_init(&bars[i], cnt);
     }
@@ -488,6 +475,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       int64_t j = 0;  // chunk counter
       int64_t i = 0;  // unit counter
       int64_t v = 0;  // tile sequence number
+      int64_t d = 0;  // Z hand-offs to the epilogue (one per accumulation segment)
       for (int64_t u = u_begin; u < u_end; ++u, ++i) {
         const Unit cu = unit_of(u, t.ngroups);
         const bool first_of_tile = (u == u_begin) || unit_of(u - 1, t.ngroups).tile != cu.tile;
@@ -540,10 +528,12 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           if (leader_lane) (PAIR ? tc_commit_pair : tc_commit)(&bars[B_F_FULL]);
           if (c == t.nchunks - 1 && last_of_tile) if (leader_lane) (PAIR ? tc_commit_pair : tc_commit)(&bars[B_XY_FREE]);
-          // ---- GEMM 2: Z += P A^T, P (hi/lo fp16) read from TMEM in place of F_x
-          if (c == 0 && i > 0) {  // previous unit's epilogue has drained Z
+          // ---- GEMM 2: Z += P A^T, P (hi/lo fp16) read from TMEM in place of F_x; a new
+          // accumulation segment starts a fresh Z once the epilogue has drained the last one
+          const bool seg_start = (c % t.seg_chunks) == 0;
+          if (seg_start && d > 0) {
             const auto t0 = now();
-            wait_leader<PAIR>(&bars[B_Z_EMPTY], static_cast<uint32_t>((i - 1) & 1));
+            wait_leader<PAIR>(&bars[B_Z_EMPTY], static_cast<uint32_t>((d - 1) & 1));
             pc[4] += now() - t0;
             tc_fence_after();
           }
@@ -559,15 +549,18 @@ __global__ void __launch_bounds__(kThreads, 1)
               const uint32_t sb = take_a(slot);
               const uint64_t bh = make_sdesc(sb, lbo_a, 128), bl = make_sdesc(sb + a_half, lbo_a, 128);
               const uint32_t zd = tmem + pt * t.zp;
-              if (leader_lane) (PAIR ? mma_f16_ts_pair : mma_f16_ts)(zd, p_hi, bh, id2, (c == 0 && s == 0) ? 0u : 1u);
+              if (leader_lane) (PAIR ? mma_f16_ts_pair : mma_f16_ts)(zd, p_hi, bh, id2, (seg_start && s == 0) ? 0u : 1u);
               if (leader_lane) (PAIR ? mma_f16_ts_pair : mma_f16_ts)(zd, p_hi, bl, id2, 1u);
               if (leader_lane) (PAIR ? mma_f16_ts_pair : mma_f16_ts)(zd, p_lo, bh, id2, 1u);
               if (leader_lane) (PAIR ? tc_commit_pair : tc_commit)(&bars[slot]);
             }
           }
           if (leader_lane) (PAIR ? tc_commit_pair : tc_commit)(&bars[B_G2_DONE]);
+          if ((c + 1) % t.seg_chunks == 0 || c + 1 == t.nchunks) {
+            if (leader_lane) (PAIR ? tc_commit_pair : tc_commit)(&bars[B_Z_FULL]);
+            ++d;
+          }
         }
-        if (leader_lane) (PAIR ? tc_commit_pair : tc_commit)(&bars[B_Z_FULL]);
         if (last_of_tile) ++v;
       }
       pc[0] = now() - t_start;
@@ -639,15 +632,18 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (wait_free) mbar_wait(&bars[B_XY_FREE], par);
         if (!t.raw_inplace) mbar_arrive(&bars[B_RAW_FREE]);
       } else if (t.raw_inplace) {
-        convert_input_regs<KH>(raw_x, wx, t.din1, t.k1p, xh, xl, part_sh, ex_sh[buf], r, h, wait_free, &bars[B_XY_FREE],
-                           par);
+        convert_input_regs<KH>(raw_x, wx, t.din1, t.k1p, t.in_shift, xh, xl, part_sh, ex_sh[buf], r, h, wait_free,
+                               &bars[B_XY_FREE], par);
         named_bar_sync(1, kWorkers);
-        convert_input_regs<KH>(raw_y, wy, t.din2, t.k2p, yh, yl, part_sh, ey_sh[buf], r, h, false, &bars[B_XY_FREE], par);
+        convert_input_regs<KH>(raw_y, wy, t.din2, t.k2p, t.in_shift, yh, yl, part_sh, ey_sh[buf], r, h, false,
+                               &bars[B_XY_FREE], par);
       } else {
         // both inputs are read before the raw buffer is handed back to the producer
-        convert_input(raw_x, wx, t.din1, t.k1p, xh, xl, part_sh, ex_sh[buf], r, h, wait_free, &bars[B_XY_FREE], par);
+        convert_input(raw_x, wx, t.din1, t.k1p, t.in_shift, xh, xl, part_sh, ex_sh[buf], r, h, wait_free,
+                      &bars[B_XY_FREE], par);
         named_bar_sync(1, kWorkers);
-        convert_input(raw_y, wy, t.din2, t.k2p, yh, yl, part_sh, ey_sh[buf], r, h, false, &bars[B_XY_FREE], par);
+        convert_input(raw_y, wy, t.din2, t.k2p, t.in_shift, yh, yl, part_sh, ey_sh[buf], r, h, false,
+                      &bars[B_XY_FREE], par);
         mbar_arrive(&bars[B_RAW_FREE]);
       }
       fence_proxy_async_smem();
@@ -656,51 +652,15 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     int64_t i = 0;  // unit counter
     int64_t v = 0;  // tile sequence number
-    { const auto t0 = now(); if (u_begin < u_end) convert(u_begin, 0); pc[11] += now() - t0; }
-    for (int64_t u = u_begin; u < u_end; ++u, ++i) {
-      const Unit cu = unit_of(u, t.ngroups);
-      const bool last_of_tile = (u + 1 == u_end) || unit_of(u + 1, t.ngroups).tile != cu.tile;
-      const int buf = static_cast<int>(v & 1);  // ex/ey of this unit's tile
-      // ---- pointwise product, chunk by chunk; P overwrites F_x slice by slice
-      for (int c = 0; c < t.nchunks; ++c, ++j) {
-        { const auto t0 = now(); mbar_wait(&bars[B_F_FULL], static_cast<uint32_t>(j & 1)); pc[9] += now() - t0; }
-        tc_fence_after();
-        const auto tp0 = now();
-        for (int s = h; s < t.nslices; s += 2) {
-          if (t.dbg & 1) {
-            signal_leader(&bars[B_P_READY + s], true);
-            continue;
-          }
-          uint32_t vx[16], vy[16];
-          tmem_ld16(lane_base + fx + 16 * s, vx);
-          tmem_ld16(lane_base + fy + 16 * s, vy);
-          tmem_wait_ld();
-          uint32_t hw[8], lw[8];
-#pragma unroll
-          for (int qq = 0; qq < 8; ++qq) {
-            const float a0 = __uint_as_float(vx[2 * qq]) * __uint_as_float(vy[2 * qq]);
-            const float a1 = __uint_as_float(vx[2 * qq + 1]) * __uint_as_float(vy[2 * qq + 1]);
-            const __half2 hh = __floats2half2_rn(a0, a1);
-            const float2 hf = __half22float2(hh);
-            hw[qq] = *reinterpret_cast<const uint32_t*>(&hh);
-            lw[qq] = pack_half2(a0 - hf.x, a1 - hf.y);
-          }
-          tmem_st8(lane_base + fx + 16 * s, hw);
-          tmem_st8(lane_base + fx + 16 * s + 8, lw);
-          tmem_wait_st();
-          tc_fence_before();
-          signal_leader(&bars[B_P_READY + s], true);
-        }
-        pc[10] += now() - tp0;
-      }
-      // ---- next unit's inputs (overlaps this unit's last GEMM 2)
-      if (last_of_tile && u + 1 < u_end) {
-        const auto t0 = now();
-        convert(u + 1, v + 1);
-        pc[11] += now() - t0;
-      }
-      // ---- epilogue: Z -> registers -> rescale -> staging -> coalesced row-segment stores
-      { const auto t0 = now(); mbar_wait(&bars[B_Z_FULL], static_cast<uint32_t>(i & 1)); pc[12] += now() - t0; }
+    int64_t d = 0;  // Z hand-offs received (one per accumulation segment)
+    // ---- epilogue of one accumulation segment: Z -> registers -> rescale -> staging -> coalesced
+    // row-segment stores; segments after the first add their partial sum to the one already
+    // stored (fp32, round to nearest): each lane reads back exactly the elements it wrote, through
+    // cp.async into lane-private shared-memory slots issued before the TMEM read
+    float* stage2 = reinterpret_cast<float*>(smem + t.off_stage) + kWorkerWarps * 32 * kStageStride + (warp - 2) * 512;
+    auto drain = [&](const Unit& cu, int buf, bool add, bool final_seg) {
+      { const auto t0 = now(); mbar_wait(&bars[B_Z_FULL], static_cast<uint32_t>(d & 1)); pc[12] += now() - t0; }
+      ++d;
       const auto te0 = now();
       tc_fence_after();
       const int e_row = ex_sh[buf][r] + ey_sh[buf][r] - t.a_shift;
@@ -715,7 +675,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       const bool full = left >= 32;
       const float* sp0 = stage + half_lane * kStageStride + cl;
       float* op0 = rs.out + (row0 + half_lane) * t.dout_total + col0 + cl;
-      for (int cb = h; cb < ((t.dbg & 2) ? 0 : nblk); cb += 2) {
+      const int cb0 = t.split_roles ? 0 : h, cbs = t.split_roles ? 1 : 2;
+      for (int cb = cb0; cb < ((t.dbg & 2) ? 0 : nblk); cb += cbs) {
+        const bool col_ok = col0 + cb * 16 + cl < col_end;
+        float* op = op0 + cb * 16;
+        if (add && col_ok && !t.seg_red) {  // previous segments' sum -> lane-private slots of stage2 (async, no registers)
+          for (int k = 0; k < 16; ++k)
+            if (full || 2 * k < left) cp_async4(stage2 + k * 32 + lane, op + k * stride2);
+        }
         uint32_t v0[16];
         tmem_ld16(lane_base + cb * 16, v0);
         tmem_wait_ld();
@@ -723,15 +690,26 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int qq = 0; qq < 16; ++qq) stage[lane * kStageStride + qq] = __uint_as_float(v0[qq]) * s_lo * s_hi;
         __syncwarp();
         // two rows per store instruction: lanes 0-15 row rr, lanes 16-31 row rr + 1
-        if (col0 + cb * 16 + cl < col_end) {
-          float* op = op0 + cb * 16;
+        if (col_ok) {
           const float* sp = sp0;
           const float wc = dw.on ? wtab_c[col0 + cb * 16 + cl] : 1.f;  // fused output weights (weighted GTP)
-          if (full) {
+          if (add && t.seg_red) {  // fire-and-forget fp32 reductions in L2 (red.global.add, round to nearest)
+            for (int k = 0; k < 16; ++k, sp += 2 * kStageStride)
+              if (full || 2 * k < left) atomicAdd(op + k * stride2, *sp * wc);
+          } else if (add) {  // out = previous sum + this segment, fp32 round to nearest
+            cp_async_wait_all();
+            if (full) {
 #pragma unroll
-            for (int rr = 0; rr < 32; rr += 2, op += stride2, sp += 2 * kStageStride) *op = *sp * wc;
+              for (int k = 0; k < 16; ++k, sp += 2 * kStageStride) op[k * stride2] = fmaf(*sp, wc, stage2[k * 32 + lane]);
+            } else {
+              for (int k = 0; k < 16 && 2 * k < left; ++k, sp += 2 * kStageStride)
+                op[k * stride2] = fmaf(*sp, wc, stage2[k * 32 + lane]);
+            }
+          } else if (full) {
+#pragma unroll
+            for (int k = 0; k < 16; ++k, sp += 2 * kStageStride) op[k * stride2] = *sp * wc;
           } else {
-            for (int rr = 0; rr < left; rr += 2, op += stride2, sp += 2 * kStageStride) *op = *sp * wc;
+            for (int k = 0; k < 16 && 2 * k < left; ++k, sp += 2 * kStageStride) op[k * stride2] = *sp * wc;
           }
         }
         __syncwarp();
@@ -740,13 +718,69 @@ __global__ void __launch_bounds__(kThreads, 1)
       signal_leader(&bars[B_Z_EMPTY], true);
       pc[13] += now() - te0;
       // degrees past the product band are exactly zero (proj/src/gtp.cpp:237-258)
-      if (cu.g == t.ngroups - 1 && t.dout_total > t.dout_eff && h == 0) {
+      if (final_seg && cu.g == t.ngroups - 1 && t.dout_total > t.dout_eff && h == (t.split_roles ? 1 : 0)) {
         for (int rr = 0; rr < 32; ++rr) {
           const int64_t g = row0 + rr;
           if (g >= rs.rows) break;
           for (int col = t.dout_eff + lane; col < t.dout_total; col += 32) rs.out[g * t.dout_total + col] = 0.f;
         }
       }
+    };
+    // split_roles: warps 2-5 run every slice's pointwise product, warps 6-9 drain Z (segment sums and
+    // the epilogue), so a drain never delays the next chunk's products; otherwise both halves share
+    // the slices and the column blocks
+    const bool do_products = !t.split_roles || h == 0;
+    const bool do_drains = !t.split_roles || h == 1;
+    const int s0 = t.split_roles ? 0 : h, sstep = t.split_roles ? 1 : 2;
+    { const auto t0 = now(); if (u_begin < u_end) convert(u_begin, 0); pc[11] += now() - t0; }
+    for (int64_t u = u_begin; u < u_end; ++u, ++i) {
+      const Unit cu = unit_of(u, t.ngroups);
+      const bool last_of_tile = (u + 1 == u_end) || unit_of(u + 1, t.ngroups).tile != cu.tile;
+      const int buf = static_cast<int>(v & 1);  // ex/ey of this unit's tile
+      // ---- pointwise product, chunk by chunk; P overwrites F_x slice by slice
+      for (int c = 0; c < t.nchunks; ++c, ++j) {
+        if (do_products) {
+          { const auto t0 = now(); mbar_wait(&bars[B_F_FULL], static_cast<uint32_t>(j & 1)); pc[9] += now() - t0; }
+          tc_fence_after();
+          const auto tp0 = now();
+          for (int s = s0; s < t.nslices; s += sstep) {
+            if (t.dbg & 1) {
+              signal_leader(&bars[B_P_READY + s], true);
+              continue;
+            }
+            uint32_t vx[16], vy[16];
+            tmem_ld16(lane_base + fx + 16 * s, vx);
+            tmem_ld16(lane_base + fy + 16 * s, vy);
+            tmem_wait_ld();
+            uint32_t hw[8], lw[8];
+#pragma unroll
+            for (int qq = 0; qq < 8; ++qq) {
+              const float a0 = __uint_as_float(vx[2 * qq]) * __uint_as_float(vy[2 * qq]);
+              const float a1 = __uint_as_float(vx[2 * qq + 1]) * __uint_as_float(vy[2 * qq + 1]);
+              const __half2 hh = __floats2half2_rn(a0, a1);
+              const float2 hf = __half22float2(hh);
+              hw[qq] = *reinterpret_cast<const uint32_t*>(&hh);
+              lw[qq] = pack_half2(a0 - hf.x, a1 - hf.y);
+            }
+            tmem_st8(lane_base + fx + 16 * s, hw);
+            tmem_st8(lane_base + fx + 16 * s + 8, lw);
+            tmem_wait_st();
+            tc_fence_before();
+            signal_leader(&bars[B_P_READY + s], true);
+          }
+          pc[10] += now() - tp0;
+        }
+        // ---- an accumulation segment ends before the unit's last chunk: drain its partial sum
+        // (overlaps the next chunk's GEMM 1)
+        if (do_drains && (c + 1) % t.seg_chunks == 0 && c + 1 < t.nchunks) drain(cu, buf, c + 1 > t.seg_chunks, false);
+      }
+      // ---- next unit's inputs (overlaps this unit's last GEMM 2)
+      if (last_of_tile && u + 1 < u_end) {
+        const auto t0 = now();
+        convert(u + 1, v + 1);
+        pc[11] += now() - t0;
+      }
+      if (do_drains) drain(cu, buf, t.nchunks > t.seg_chunks, true);
       if (last_of_tile) ++v;
     }
     pc[8] = now() - t_start;

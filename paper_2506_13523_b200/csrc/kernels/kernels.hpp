@@ -21,6 +21,18 @@ struct RowSpec {
   int y_shared;
 };
 
+// ---------------------------------------------------------------- 3xFP16 scaling
+// Exact power-of-two scales that keep the fp16 hi / lo parts of every GEMM operand well inside
+// fp16's normal range (its subnormals carry only absolute precision 2^-24, which was the
+// dominant error for small rows when values sat near 1):
+//   kInShift   input rows are scaled so that max|x| < 2^kInShift (CGTP blocks, edge kernel) or
+//              ||x||_2 < 2^kInShift (MTP, whose carrier matrices are isometric in x), so products
+//              of two scaled values stay below 2^14;
+//   kTabShift  constant operator tables with entries <= 1 (real CG blocks, MTP extract) are
+//              stored times 2^kTabShift; the epilogue divides both back out exactly.
+constexpr int kInShift = 7;
+constexpr int kTabShift = 11;
+
 // ---------------------------------------------------------------- CGTP
 // Output coefficient o is owned by thread o % kCgtpChunk of output pass
 // o / kCgtpChunk.  Terms {i1 | i2 << 16, coef bits} are stored term-major per
@@ -99,12 +111,21 @@ struct GridTcTables {
   int nparts, zp;            // GEMM 2 N-split: zg = nparts * zp, zp <= 128 (keeps ring stages small)
   int dout_eff;              // outputs computed (degrees <= min(L3, band))
   int dout_total;            // (L3+1)^2 written (zeros past the band)
-  int a_shift;               // device A = A * 2^a_shift
+  int a_shift;               // device A = A * 2^a_shift (max |A| in [2^12, 2^13))
+  int in_shift;              // input rows scaled to ||x||_2 < 2^in_shift: the largest scale keeping every
+                             // P = F_x F_y below 2^14 (|F(g)| <= ||x|| ||S row g||), so the fp16 hi / lo
+                             // parts of inputs and products stay clear of fp16's subnormal range
   int same_s;                // s2 == s1 (L1 == L2)
   int s_stages, a_stages;    // B-operand rings (S table -> GEMM 1, A table -> GEMM 2), one producer warp each
   uint32_t s_stage_bytes, a_stage_bytes;
   int raw_inplace;           // raw input tiles land in the X/Y operand buffers
   int safe_war;              // wait for GEMM 2 of chunk c before GEMM 1 of chunk c+1
+  int seg_chunks;            // GEMM-2 accumulation segment (chunks): the tensor pipe's fp32 accumulation
+                             // truncates (round toward zero) once per MMA, so the error grows with the
+                             // number of MMAs into one accumulator; each segment starts a fresh Z and its
+                             // partial sum is added in fp32 (round to nearest) into the output row
+  int seg_red;               // segment sums: 1 fp32 reductions in L2 (red.add), 0 read back through cp.async
+  int split_roles;           // warps 2-5 products, warps 6-9 drains (else both halves share both)
   int pair;                  // CTA pairs, tcgen05 cta_group::2 (M = 256); slices stored as two row halves
   int dbg;                   // timing experiments only (results invalid): 1 no product, 2 no epilogue, 4 no convert
   int smem_bytes;

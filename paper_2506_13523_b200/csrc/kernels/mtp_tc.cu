@@ -44,15 +44,6 @@ constexpr int B_D_FREE = B_G2_DONE + 1;      // epilogue read the output columns
 constexpr int B_STAGE_FULL = B_D_FREE + 1;   // TMA staging of a tile's raw inputs landed
 constexpr int kBars = B_STAGE_FULL + 1;
 
-__device__ __forceinline__ float pow2i(int k) { return __int_as_float((127 + k) << 23); }
-__device__ __forceinline__ float mul_pow2(float v, int k) {
-  const int k1 = k >> 1;
-  return (v * pow2i(k1)) * pow2i(k - k1);
-}
-__device__ __forceinline__ uint32_t pack_half2(float a, float b) {
-  const __half2 h = __floats2half2_rn(a, b);
-  return *reinterpret_cast<const uint32_t*>(&h);
-}
 __device__ __forceinline__ void tmem_ld8p(uint32_t taddr, uint32_t* r) {
   asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
@@ -182,16 +173,14 @@ __device__ __forceinline__ void middle_half(uint32_t lb, uint32_t zc1, int nb1, 
 // the exact scale 2^-e.
 __device__ __forceinline__ int convert_row(const float* st, int din, int kp, uint8_t* hi, uint8_t* lo, int r) {
   const float* src = st + r * din;
-  float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+  float m0 = 0.f, m1 = 0.f, m2 = 0.f, m3 = 0.f;
   int k = 0;
   for (; k + 4 <= din; k += 4) {
-    const float a = src[k], b = src[k + 1], c = src[k + 2], d = src[k + 3];
-    s0 = fmaf(a, a, s0); s1 = fmaf(b, b, s1); s2 = fmaf(c, c, s2); s3 = fmaf(d, d, s3);
+    m0 = fmaxf(m0, fabsf(src[k])); m1 = fmaxf(m1, fabsf(src[k + 1]));
+    m2 = fmaxf(m2, fabsf(src[k + 2])); m3 = fmaxf(m3, fabsf(src[k + 3]));
   }
-  for (; k < din; ++k) s0 = fmaf(src[k], src[k], s0);
-  const float ss = (s0 + s1) + (s2 + s3);
-  int e = 0;
-  if (ss > 0.f && ss < 3.0e38f) e = max(-120, min(120, ilogbf(ss) / 2 + 1));
+  for (; k < din; ++k) m0 = fmaxf(m0, fabsf(src[k]));
+  const int e = row_scale_exp(fmaxf(fmaxf(m0, m1), fmaxf(m2, m3)), din) - kInShift;  // ||x|| < 2^7: |Z| < 2^14
   const float sc = pow2i(-e);
 #pragma unroll 2
   for (int k0 = 0; k0 < kp; k0 += 8) {
@@ -436,7 +425,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_after();
       if (!hw) tick(4, t0);
       t0 = now();
-      const int e_row = ex_sh[it & 1][r] + ey_sh[it & 1][r];
+      const int e_row = ex_sh[it & 1][r] + ey_sh[it & 1][r] - kTabShift;  // Ext is stored times 2^kTabShift
       const bool bulk = bulk_ok(tile);
       if (bulk) {
         epilogue_bulk(lb, e_row, tile, q, hw);

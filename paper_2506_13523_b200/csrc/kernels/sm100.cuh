@@ -225,6 +225,34 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
 }
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
+// 4-byte global -> shared copy through the async copy unit (no register round trip)
+__device__ __forceinline__ void cp_async4(float* dst, const float* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+// ---------------------------------------------------------------- 3xFP16 helpers (shared by every tcgen05 kernel)
+// 2^k for |k| <= 126, exact (exponent bits)
+__device__ __forceinline__ float pow2i(int k) { return __int_as_float((127 + k) << 23); }
+// v * 2^k, exact for |k| <= 252 unless the result itself is subnormal
+__device__ __forceinline__ float mul_pow2(float v, int k) {
+  const int k1 = k >> 1;
+  return (v * pow2i(k1)) * pow2i(k - k1);
+}
+__device__ __forceinline__ uint32_t pack_half2(float a, float b) {
+  const __half2 h = __floats2half2_rn(a, b);
+  return *reinterpret_cast<const uint32_t*>(&h);
+}
+// Exact power-of-two row scale 2^-e for the fp16 hi / lo split, from the row's largest
+// magnitude `mx` (not its sum of squares, which overflows fp32 for rows near 1e19 and
+// underflows near 1e-19): max|x| 2^-e < 2^-h with 2^h >= sqrt(din), so ||x||_2 2^-e < 1 as
+// the kernels' range bounds on the transformed values assume.  Zero / non-finite rows: e = 0.
+__device__ __forceinline__ int row_scale_exp(float mx, int din) {
+  if (!(mx > 0.f) || mx > 3.0e38f) return 0;
+  const int h = din > 1 ? (33 - __clz(din - 1)) >> 1 : 0;  // ceil(log2(din)) / 2, rounded up
+  return max(-120, min(120, ilogbf(mx) + 1 + h));
+}
+
 #endif  // __CUDACC__
 
 // ---------------------------------------------------------------- descriptors
