@@ -145,6 +145,65 @@ int tpo_cg_real(int l1, int l2, int l3, int* m1, int* m2, int* m3, double* value
  * entry count (or a negative status). */
 int tpo_fourier_table(int L, int which, int* counts, int* u, int* v, double* re, double* im, int cap);
 
+/* Stage entry points ------------------------------------------------------
+ * The reference's pipelines are exported stage by stage (its timing harness,
+ * proj/src/bench.cpp:58-72, and its round-trip suite, proj/src/verify.cpp:256-309,
+ * call the stages directly).  Batched over rows, device pointers, async on
+ * `stream`; inputs are single-copy towers 0..L (sum repeated degrees first:
+ * every stage is linear per entry).  Grids are make_grid(grid_L): n_theta =
+ * grid_L + 1 Gauss-Legendre rows (ascending cos theta) x n_phi = 2 grid_L + 1
+ * uniform columns, F row-major [n_theta][n_phi] per row. */
+/* replaces tpo::to_sphere(x, make_grid(grid_L)) -- proj/include/tpo/sphere.hpp:73-74 ;
+ * x [batch][(L+1)^2] -> F [batch][n_theta * n_phi]; EINVAL if L > grid_L */
+int tpo_to_sphere_f32(tpo_ctx* ctx, int L, int grid_L, const float* x, float* F, int64_t batch, void* stream);
+/* replaces tpo::detail::from_sphere_select(f, degrees) -- proj/include/tpo/sphere.hpp:86-88 ;
+ * `degrees` is a HOST array; out [batch][sum (2l+1)] in the given order */
+int tpo_from_sphere_f32(tpo_ctx* ctx, int grid_L, const int* degrees, int n_degrees, const float* F, float* out,
+                        int64_t batch, void* stream);
+/* replaces tpo::pointwise_mul -- proj/include/tpo/sphere.hpp:82-83 ; n floats */
+int tpo_pointwise_mul_f32(tpo_ctx* ctx, const float* a, const float* b, float* out, int64_t n, void* stream);
+/* replaces tpo::mtp_embed(x, l_tilde) -- proj/include/tpo/mtp.hpp:20-22 ;
+ * x [batch][(L+1)^2] -> X [batch][dt][dt] row-major, dt = 2 l_tilde + 1; EINVAL if L > 2 l_tilde */
+int tpo_mtp_embed_f32(tpo_ctx* ctx, int L, int l_tilde, const float* x, float* X, int64_t batch, void* stream);
+/* replaces tpo::mtp_matmul(X, Y) -- proj/include/tpo/mtp.hpp:36-37 ; Z[b] = X[b] Y[b], dt x dt */
+int tpo_mtp_matmul_f32(tpo_ctx* ctx, int dt, const float* X, const float* Y, float* Z, int64_t batch, void* stream);
+/* replaces tpo::mtp_extract_select(Z, degrees, l_tilde) -- proj/include/tpo/mtp.hpp:30-33
+ * (mtp_extract = degrees 0..L3); degrees past 2 l_tilde give zero blocks; `degrees` is a HOST array */
+int tpo_mtp_extract_f32(tpo_ctx* ctx, int l_tilde, const int* degrees, int n_degrees, const float* Z, float* out,
+                        int64_t batch, void* stream);
+/* replaces tpo::apply_linear(LinearLayer(in, out), x) -- proj/include/tpo/irreps.hpp:77-107 ;
+ * irreps as (mul, l) lists (HOST), one weight per (input copy, output copy) of equal degree in the
+ * reference's connection order (proj/src/irreps.cpp:95-104); x [batch][dim in] -> out [batch][dim out] */
+int tpo_apply_linear_f32(tpo_ctx* ctx, const int* in_mul, const int* in_l, int n_in, const int* out_mul,
+                         const int* out_l, int n_out, const double* weights, int n_weights, const float* x, float* out,
+                         int64_t batch, void* stream);
+/* replaces tpo::wigner_d(l, rot) for l = 0..L -- proj/include/tpo/wigner.hpp:86 ; R [n][9] row-major
+ * rotation matrices (device, fp64) -> D [n][tpo_wigner_d_size(L)] (device, fp64): the blocks D^0..D^L,
+ * each (2l+1) x (2l+1) row-major, by the reference's recursion */
+int tpo_wigner_d_f64(tpo_ctx* ctx, int L, const double* R, double* D, int64_t n, void* stream);
+int64_t tpo_wigner_d_size(int L);
+/* replaces tpo::rotate(x, rot) -- proj/include/tpo/wigner.hpp:89 ; x [batch][channels][(L+1)^2];
+ * n_rot rotations R [n_rot][9] (device, fp64): sample b uses rotation b * n_rot / batch (1 = shared,
+ * batch = one per sample) */
+int tpo_rotate_f32(tpo_ctx* ctx, int L, const double* R, int64_t n_rot, const float* x, float* out, int64_t batch,
+                   int64_t channels, void* stream);
+
+/* Host tables / analysis (table-time, no device) ----------------------------
+ * gaunt_real (proj/include/tpo/wigner.hpp:64, pybind cg_table(gaunt=True)): same contract as
+ * tpo_cg_real. */
+int tpo_gaunt_real(int l1, int l2, int l3, int* m1, int* m2, int* m3, double* value, int cap);
+/* make_grid(L) nodes / weights: L+1 ascending cos(theta) and Gauss-Legendre weights (sum 2)
+ * (proj/include/tpo/sphere.hpp:49-55) ; either pointer may be NULL */
+int tpo_s2_grid(int L, double* cos_theta, double* weights);
+/* legendre_lambda_table (proj/include/tpo/sphere.hpp:33): lam[idx(l,m) * n + j], idx = l(l+1)/2 + m */
+int tpo_legendre_lambda(int lmax, const double* cos_theta, int n, double* lam);
+/* mtp_path_weights (proj/include/tpo/mtp.hpp:48); NaN on error */
+double tpo_mtp_path_weight(int l1, int l2, int l3, int l_tilde);
+/* count_ops (proj/include/tpo/bench.hpp:45): the reference's instrumented multiply count of one
+ * application; kind 0 cgtp / 1 gtp / 2 mtp, impl 0 naive / 1 sparse / 2 grid / 3 fourier,
+ * mode 0 siso / 1 simo / 2 mimo.  Negative status on error. */
+int64_t tpo_count_muls(int kind, int impl, int mode, int L);
+
 /* Kernel selection for the two Gaunt products (for tests/bench): 0 auto,
  * 1 force the fused tcgen05 kernel (fails if the shape does not fit: inputs
  * of more than 128 coefficients, i.e. L > 10), 2 force the SIMT kernels

@@ -226,3 +226,199 @@ def product(kind: str, x, y, L1: int, L2: int, L3: int = 0, l_tilde: int = -1):
     """Differentiable product (torch.autograd): the forward kernel of ``kind``
     and tpo_backward_f32 for the gradients."""
     return _autograd_fn().apply(x, y, kind, L1, L2, L3, l_tilde)
+
+
+# ---------------------------------------------------------------- stage operators (device, batched)
+def _dev_check(*ts):
+    import torch
+
+    for t in ts:
+        if not isinstance(t, torch.Tensor) or not t.is_cuda:
+            raise ValueError("inputs must be CUDA tensors (no CPU path)")
+        if t.device != ts[0].device:
+            raise ValueError("all tensors must be on the same device")
+
+
+def _f32(t):
+    import torch
+
+    if t.dtype != torch.float32:
+        raise ValueError("tensors must be float32")
+    return t.contiguous()
+
+
+def _ints(v):
+    import ctypes as C
+
+    v = [int(a) for a in v]
+    return (C.c_int * max(1, len(v)))(*v), len(v)
+
+
+def _stream(t):
+    import torch
+
+    return torch.cuda.current_stream(t.device).cuda_stream
+
+
+def to_sphere(x, L: int, grid_L: int):
+    """Batched tpo::to_sphere on make_grid(grid_L) (proj/src/sphere.cpp:105-134): x [B, (L+1)^2]
+    -> F [B, grid_L+1, 2 grid_L+1]."""
+    import torch
+
+    _dev_check(x)
+    x = _f32(x)
+    if x.dim() != 2 or x.shape[1] != tower_dim(L):
+        raise ValueError(f"x must be [B, {tower_dim(L)}]")
+    F = torch.empty((x.shape[0], grid_L + 1, 2 * grid_L + 1), device=x.device)
+    check(lib().tpo_to_sphere_f32(context(x.device.index).handle, L, grid_L, x.data_ptr(), F.data_ptr(), x.shape[0],
+                                  _stream(x)))
+    return F
+
+
+def from_sphere(F, grid_L: int, degrees):
+    """Batched tpo::detail::from_sphere_select (proj/src/sphere.cpp:155-195): F [B, nt, np] ->
+    [B, sum(2l+1)] over `degrees` in the given order."""
+    import torch
+
+    _dev_check(F)
+    F = _f32(F)
+    if F.dim() != 3 or tuple(F.shape[1:]) != (grid_L + 1, 2 * grid_L + 1):
+        raise ValueError("F must be [B, grid_L+1, 2 grid_L+1]")
+    d, n = _ints(degrees)
+    out = torch.empty((F.shape[0], sum(2 * l + 1 for l in degrees)), device=F.device)
+    check(lib().tpo_from_sphere_f32(context(F.device.index).handle, grid_L, d, n, F.data_ptr(), out.data_ptr(),
+                                    F.shape[0], _stream(F)))
+    return out
+
+
+def pointwise_mul(a, b):
+    """tpo::pointwise_mul on sphere samples (proj/src/sphere.cpp:145-151)."""
+    import torch
+
+    _dev_check(a, b)
+    a, b = _f32(a), _f32(b)
+    if a.shape != b.shape:
+        raise ValueError("pointwise_mul: signals live on different grids")
+    out = torch.empty_like(a)
+    check(lib().tpo_pointwise_mul_f32(context(a.device.index).handle, a.data_ptr(), b.data_ptr(), out.data_ptr(),
+                                      a.numel(), _stream(a)))
+    return out
+
+
+def mtp_embed(x, L: int, l_tilde: int):
+    """Batched tpo::mtp_embed (proj/src/mtp.cpp:47-58): x [B, (L+1)^2] -> X [B, dt, dt]."""
+    import torch
+
+    _dev_check(x)
+    x = _f32(x)
+    if x.dim() != 2 or x.shape[1] != tower_dim(L):
+        raise ValueError(f"x must be [B, {tower_dim(L)}]")
+    dt = 2 * l_tilde + 1
+    X = torch.empty((x.shape[0], dt, dt), device=x.device)
+    check(lib().tpo_mtp_embed_f32(context(x.device.index).handle, L, l_tilde, x.data_ptr(), X.data_ptr(), x.shape[0],
+                                  _stream(x)))
+    return X
+
+
+def mtp_matmul(X, Y):
+    """Batched tpo::mtp_matmul (proj/src/mtp.cpp:119-133): Z[b] = X[b] Y[b]."""
+    import torch
+
+    _dev_check(X, Y)
+    X, Y = _f32(X), _f32(Y)
+    if X.dim() != 3 or X.shape != Y.shape or X.shape[1] != X.shape[2]:
+        raise ValueError("mtp_matmul: carriers do not match")
+    Z = torch.empty_like(X)
+    check(lib().tpo_mtp_matmul_f32(context(X.device.index).handle, X.shape[1], X.data_ptr(), Y.data_ptr(),
+                                   Z.data_ptr(), X.shape[0], _stream(X)))
+    return Z
+
+
+def mtp_extract(Z, l_tilde: int, degrees):
+    """Batched tpo::mtp_extract_select (proj/src/mtp.cpp:60-97): Z [B, dt, dt] -> [B, sum(2l+1)]."""
+    import torch
+
+    _dev_check(Z)
+    Z = _f32(Z)
+    dt = 2 * l_tilde + 1
+    if Z.dim() != 3 or tuple(Z.shape[1:]) != (dt, dt):
+        raise ValueError("mtp_extract: matrix does not match the carrier degree")
+    d, n = _ints(degrees)
+    out = torch.empty((Z.shape[0], sum(2 * l + 1 for l in degrees)), device=Z.device)
+    check(lib().tpo_mtp_extract_f32(context(Z.device.index).handle, l_tilde, d, n, Z.data_ptr(), out.data_ptr(),
+                                    Z.shape[0], _stream(Z)))
+    return out
+
+
+def linear_connections(in_irreps, out_irreps):
+    """LinearLayer connections (proj/src/irreps.cpp:95-104): one weight per (input copy, output
+    copy) of equal degree, in (input entry, input copy, output entry, output copy) order.  irreps are
+    [(mul, l), ...] lists."""
+    return [(ei, ci, eo, co) for ei, (mi, li) in enumerate(in_irreps) for ci in range(mi)
+            for eo, (mo, lo) in enumerate(out_irreps) if lo == li for co in range(mo)]
+
+
+def apply_linear(x, in_irreps, out_irreps, weights):
+    """Batched tpo::apply_linear (proj/src/irreps.cpp:119-129): the Schur-consistent equivariant
+    linear map, x [B, dim(in)] -> [B, dim(out)]."""
+    import ctypes as C
+
+    import numpy as np
+    import torch
+
+    _dev_check(x)
+    x = _f32(x)
+    in_mul, n_in = _ints([m for m, _ in in_irreps])
+    in_l, _ = _ints([l for _, l in in_irreps])
+    out_mul, n_out = _ints([m for m, _ in out_irreps])
+    out_l, _ = _ints([l for _, l in out_irreps])
+    din = sum(m * (2 * l + 1) for m, l in in_irreps)
+    dout = sum(m * (2 * l + 1) for m, l in out_irreps)
+    if x.dim() != 2 or x.shape[1] != din:
+        raise ValueError("linear layer: input descriptor mismatch")
+    w = np.ascontiguousarray(weights, dtype=np.float64).reshape(-1)
+    out = torch.empty((x.shape[0], dout), device=x.device)
+    check(lib().tpo_apply_linear_f32(context(x.device.index).handle, in_mul, in_l, n_in, out_mul, out_l, n_out,
+                                     w.ctypes.data_as(C.c_void_p), len(w), x.data_ptr(), out.data_ptr(), x.shape[0],
+                                     _stream(x)))
+    return out
+
+
+def wigner_d(R, L: int):
+    """Real Wigner-D blocks D^0..D^L of a batch of rotations (proj/src/wigner.cpp:288-312) on the
+    device, fp64: R [n, 3, 3] -> list of [n, 2l+1, 2l+1]."""
+    import torch
+
+    _dev_check(R)
+    R = R.to(torch.float64).contiguous()
+    n = R.shape[0]
+    D = torch.empty((n, int(lib().tpo_wigner_d_size(L))), dtype=torch.float64, device=R.device)
+    check(lib().tpo_wigner_d_f64(context(R.device.index).handle, L, R.data_ptr(), D.data_ptr(), n, _stream(R)))
+    blocks, off = [], 0
+    for l in range(L + 1):
+        d = 2 * l + 1
+        blocks.append(D[:, off:off + d * d].reshape(n, d, d))
+        off += d * d
+    return blocks
+
+
+def rotate(x, R, L: int):
+    """Batched tpo::rotate (proj/src/wigner.cpp:314-325): x [B, (L+1)^2] or [B, C, (L+1)^2];
+    R [n_rot, 3, 3] with sample b rotated by R[b * n_rot // B]."""
+    import torch
+
+    _dev_check(x, R)
+    x = _f32(x)
+    R = R.to(torch.float64).contiguous()
+    B = x.shape[0]
+    C = x.shape[1] if x.dim() == 3 else 1
+    if x.shape[-1] != tower_dim(L):
+        raise ValueError(f"x must end in {tower_dim(L)} components")
+    out = torch.empty_like(x)
+    check(lib().tpo_rotate_f32(context(x.device.index).handle, L, R.data_ptr(), R.shape[0], x.data_ptr(),
+                               out.data_ptr(), B, C, _stream(x)))
+    return out
+
+
+__all__ += ["to_sphere", "from_sphere", "pointwise_mul", "mtp_embed", "mtp_matmul", "mtp_extract", "apply_linear",
+            "linear_connections", "wigner_d", "rotate"]

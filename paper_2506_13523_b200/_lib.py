@@ -74,8 +74,25 @@ def lib():
             "tpo_cg_real": (i, [i, i, i, p, p, p, p, i]),
             "tpo_fourier_table": (i, [i, i, p, p, p, p, p, i]),
             "tpo_last_gtp_grid_path": (i, [p]),
+            "tpo_to_sphere_f32": (i, [p, i, i, p, p, i64, p]),
+            "tpo_from_sphere_f32": (i, [p, i, p, i, p, p, i64, p]),
+            "tpo_pointwise_mul_f32": (i, [p, p, p, p, i64, p]),
+            "tpo_mtp_embed_f32": (i, [p, i, i, p, p, i64, p]),
+            "tpo_mtp_matmul_f32": (i, [p, i, p, p, p, i64, p]),
+            "tpo_mtp_extract_f32": (i, [p, i, p, i, p, p, i64, p]),
+            "tpo_apply_linear_f32": (i, [p, p, p, i, p, p, i, p, i, p, p, i64, p]),
+            "tpo_wigner_d_f64": (i, [p, i, p, p, i64, p]),
+            "tpo_wigner_d_size": (i64, [i]),
+            "tpo_rotate_f32": (i, [p, i, p, i64, p, p, i64, i64, p]),
+            "tpo_gaunt_real": (i, [i, i, i, p, p, p, p, i]),
+            "tpo_s2_grid": (i, [i, p, p]),
+            "tpo_legendre_lambda": (i, [i, p, i, p]),
+            "tpo_mtp_path_weight": (d, [i, i, i, i]),
+            "tpo_count_muls": (i64, [i, i, i, i]),
         }
         for name, (res, args) in sig.items():
+            if os.environ.get("TPO_LIB_PATH") and not hasattr(L, name):
+                continue  # A/B timing of an older build (tools/gpu_*.sh): bind what it has
             fn = getattr(L, name)
             fn.restype = res
             fn.argtypes = args
@@ -89,6 +106,9 @@ EXPORTED = [
     "tpo_gtp_fourier_f32", "tpo_mtp_f32", "tpo_weighted_gtp_f32", "tpo_run_f32", "tpo_run_host_f32",
     "tpo_run_host_batch_f32", "tpo_backward_f32",
     "tpo_set_gtp_grid_path", "tpo_last_gtp_grid_path", "tpo_cg_real", "tpo_fourier_table",
+    "tpo_to_sphere_f32", "tpo_from_sphere_f32", "tpo_pointwise_mul_f32", "tpo_mtp_embed_f32", "tpo_mtp_matmul_f32",
+    "tpo_mtp_extract_f32", "tpo_apply_linear_f32", "tpo_wigner_d_f64", "tpo_wigner_d_size", "tpo_rotate_f32",
+    "tpo_gaunt_real", "tpo_s2_grid", "tpo_legendre_lambda", "tpo_mtp_path_weight", "tpo_count_muls",
 ]
 
 

@@ -8,6 +8,7 @@
 #include <vector>
 
 #include "host/context.hpp"
+#include "host/opcount.hpp"
 #include "host/tables.hpp"
 
 using tpo_b200::Context;
@@ -781,5 +782,288 @@ int tpo_set_gtp_grid_path(tpo_ctx* ctx, int path) {
 }
 
 int tpo_last_gtp_grid_path(const tpo_ctx* ctx) { return ctx ? ctx->impl.last_grid_path : -TPO_EINVAL; }
+
+}  // extern "C"
+
+// ------------------------------------------------------------------ stage operators
+namespace {
+std::vector<int> degree_list(const int* degrees, int n, const char* who) {
+  if (n < 0 || (n > 0 && !degrees)) throw InvalidArgument(std::string(who) + ": bad degree list");
+  std::vector<int> d(degrees, degrees + n);
+  for (int l : d)
+    if (l < 0 || l > 2 * kMaxL) throw InvalidArgument(std::string(who) + ": degree out of range");
+  return d;
+}
+std::string key_of(const char* tag, std::initializer_list<int> a, const std::vector<int>& d = {}) {
+  std::string k(tag);
+  for (int v : a) k += "," + std::to_string(v);
+  k += "|";
+  for (int v : d) k += std::to_string(v) + ",";
+  return k;
+}
+int dsel_of(const std::vector<int>& d) {
+  int n = 0;
+  for (int l : d) n += 2 * l + 1;
+  return n;
+}
+void stage_args(const tpo_ctx* ctx, const void* in, const void* out, int64_t batch) {
+  if (!ctx) throw InvalidArgument("tpo: null context");
+  if (batch < 0) throw InvalidArgument("tpo: batch must be >= 0");
+  if (batch > 0 && (!in || !out)) throw InvalidArgument("tpo: null data pointer");
+}
+}  // namespace
+
+extern "C" {
+
+int tpo_to_sphere_f32(tpo_ctx* ctx, int L, int grid_L, const float* x, float* F, int64_t batch, void* stream) {
+  return guarded([&] {
+    stage_args(ctx, x, F, batch);
+    if (grid_L < 0 || grid_L > 2 * kMaxL) throw InvalidArgument("make_grid: L must be >= 0");
+    if (L < 0) throw InvalidArgument("irreps: degree must be >= 0");
+    if (L > grid_L)  // proj/src/sphere.cpp:106-110
+      throw InvalidArgument("to_sphere: grid band limit " + std::to_string(grid_L) + " below input degree " +
+                            std::to_string(L));
+    ctx->impl.activate();
+    const int din = (L + 1) * (L + 1), G = (grid_L + 1) * (2 * grid_L + 1);
+    const float* mt = ctx->impl.dense_op(key_of("to_sphere", {L, grid_L}), [&] { return tpo_b200::op_to_sphere(L, grid_L); });
+    launched(ctx, tpo_b200::launch_dense_map(x, din, mt, G, F, batch, static_cast<cudaStream_t>(stream)), "to_sphere");
+  });
+}
+
+int tpo_from_sphere_f32(tpo_ctx* ctx, int grid_L, const int* degrees, int n_degrees, const float* F, float* out,
+                        int64_t batch, void* stream) {
+  return guarded([&] {
+    stage_args(ctx, F, out, batch);
+    if (grid_L < 0 || grid_L > 2 * kMaxL) throw InvalidArgument("make_grid: L must be >= 0");
+    const std::vector<int> d = degree_list(degrees, n_degrees, "from_sphere");
+    for (int l : d)  // proj/src/sphere.cpp:160-162
+      if (l > grid_L) throw InvalidArgument("from_sphere: grid band limit too small for requested degree");
+    ctx->impl.activate();
+    const int G = (grid_L + 1) * (2 * grid_L + 1), ds = dsel_of(d);
+    if (ds == 0) return;
+    const float* mt = ctx->impl.dense_op(key_of("from_sphere", {grid_L}, d), [&] { return tpo_b200::op_from_sphere(grid_L, d); });
+    launched(ctx, tpo_b200::launch_dense_map(F, G, mt, ds, out, batch, static_cast<cudaStream_t>(stream)), "from_sphere");
+  });
+}
+
+int tpo_pointwise_mul_f32(tpo_ctx* ctx, const float* a, const float* b, float* out, int64_t n, void* stream) {
+  return guarded([&] {
+    stage_args(ctx, a, out, n);
+    if (n > 0 && !b) throw InvalidArgument("tpo: null data pointer");
+    ctx->impl.activate();
+    launched(ctx, tpo_b200::launch_pointwise_mul(a, b, out, n, ctx->impl.num_sms(), static_cast<cudaStream_t>(stream)),
+             "pointwise_mul");
+  });
+}
+
+int tpo_mtp_embed_f32(tpo_ctx* ctx, int L, int l_tilde, const float* x, float* X, int64_t batch, void* stream) {
+  return guarded([&] {
+    stage_args(ctx, x, X, batch);
+    if (l_tilde < 0) throw InvalidArgument("mtp_embed: l_tilde must be >= 0");  // proj/src/mtp.cpp:47-51
+    if (L < 0) throw InvalidArgument("irreps: degree must be >= 0");
+    if (L > 2 * l_tilde) throw InvalidArgument("mtp_embed: carrier too small for input degrees");
+    if (l_tilde > kMaxL) throw InvalidArgument("mtp_embed: l_tilde above the supported maximum");
+    ctx->impl.activate();
+    const int din = (L + 1) * (L + 1), dt = 2 * l_tilde + 1;
+    const float* mt = ctx->impl.dense_op(key_of("mtp_embed", {L, l_tilde}), [&] { return tpo_b200::op_mtp_embed(L, l_tilde); });
+    launched(ctx, tpo_b200::launch_dense_map(x, din, mt, dt * dt, X, batch, static_cast<cudaStream_t>(stream)), "mtp_embed");
+  });
+}
+
+int tpo_mtp_matmul_f32(tpo_ctx* ctx, int dt, const float* X, const float* Y, float* Z, int64_t batch, void* stream) {
+  return guarded([&] {
+    stage_args(ctx, X, Z, batch);
+    if (batch > 0 && !Y) throw InvalidArgument("tpo: null data pointer");
+    if (dt < 1 || dt > 2 * kMaxL + 1) throw InvalidArgument("mtp_matmul: carriers do not match");
+    ctx->impl.activate();
+    launched(ctx, tpo_b200::launch_carrier_matmul(X, Y, Z, dt, batch, static_cast<cudaStream_t>(stream)), "mtp_matmul");
+  });
+}
+
+int tpo_mtp_extract_f32(tpo_ctx* ctx, int l_tilde, const int* degrees, int n_degrees, const float* Z, float* out,
+                        int64_t batch, void* stream) {
+  return guarded([&] {
+    stage_args(ctx, Z, out, batch);
+    if (l_tilde < 0 || l_tilde > kMaxL) throw InvalidArgument("mtp_extract: matrix does not match the carrier degree");
+    const std::vector<int> d = degree_list(degrees, n_degrees, "mtp_extract");
+    ctx->impl.activate();
+    const int dt = 2 * l_tilde + 1, ds = dsel_of(d);
+    if (ds == 0) return;
+    const float* mt = ctx->impl.dense_op(key_of("mtp_extract", {l_tilde}, d), [&] { return tpo_b200::op_mtp_extract(l_tilde, d); });
+    launched(ctx, tpo_b200::launch_dense_map(Z, dt * dt, mt, ds, out, batch, static_cast<cudaStream_t>(stream)),
+             "mtp_extract");
+  });
+}
+
+int tpo_apply_linear_f32(tpo_ctx* ctx, const int* in_mul, const int* in_l, int n_in, const int* out_mul,
+                         const int* out_l, int n_out, const double* weights, int n_weights, const float* x, float* out,
+                         int64_t batch, void* stream) {
+  return guarded([&] {
+    stage_args(ctx, x, out, batch);
+    if (n_in < 0 || n_out < 0 || (n_in && (!in_mul || !in_l)) || (n_out && (!out_mul || !out_l)))
+      throw InvalidArgument("linear layer: bad irreps descriptor");
+    // proj/src/irreps.cpp:95-104: one weight per (input copy, output copy) of equal degree, in
+    // (input entry, input copy, output entry, output copy) order
+    std::vector<int> ioff(n_in + 1, 0), ooff(n_out + 1, 0);
+    for (int e = 0; e < n_in; ++e) {
+      if (in_mul[e] < 1 || in_l[e] < 0) throw InvalidArgument("irreps: bad entry");
+      ioff[e + 1] = ioff[e] + in_mul[e] * (2 * in_l[e] + 1);
+    }
+    for (int e = 0; e < n_out; ++e) {
+      if (out_mul[e] < 1 || out_l[e] < 0) throw InvalidArgument("irreps: bad entry");
+      ooff[e + 1] = ooff[e] + out_mul[e] * (2 * out_l[e] + 1);
+    }
+    const int din = ioff[n_in], dout = ooff[n_out];
+    std::vector<double> mt(static_cast<size_t>(din) * dout, 0.0);
+    int w = 0;
+    for (int ei = 0; ei < n_in; ++ei)
+      for (int ci = 0; ci < in_mul[ei]; ++ci)
+        for (int eo = 0; eo < n_out; ++eo) {
+          if (out_l[eo] != in_l[ei]) continue;
+          for (int co = 0; co < out_mul[eo]; ++co, ++w) {
+            if (w >= n_weights) throw InvalidArgument("linear layer: expected more weights");
+            const int d = 2 * in_l[ei] + 1;
+            for (int m = 0; m < d; ++m)
+              mt[static_cast<size_t>(ioff[ei] + ci * d + m) * dout + ooff[eo] + co * d + m] += weights[w];
+          }
+        }
+    if (w != n_weights)
+      throw InvalidArgument("linear layer: expected " + std::to_string(w) + " weights, got " + std::to_string(n_weights));
+    ctx->impl.activate();
+    if (dout == 0 || batch == 0) return;
+    std::vector<float> f(mt.begin(), mt.end());
+    float* dm = ctx->impl.scratch(11, f.size());
+    tpo_b200::cuda_check(cudaMemcpyAsync(dm, f.data(), f.size() * 4, cudaMemcpyHostToDevice, static_cast<cudaStream_t>(stream)),
+             "linear weights");
+    tpo_b200::cuda_check(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)), "linear weights");
+    launched(ctx, tpo_b200::launch_dense_map(x, din, dm, dout, out, batch, static_cast<cudaStream_t>(stream)),
+             "apply_linear");
+  });
+}
+
+int tpo_wigner_d_f64(tpo_ctx* ctx, int L, const double* R, double* D, int64_t n, void* stream) {
+  return guarded([&] {
+    stage_args(ctx, R, D, n);
+    if (L < 0) throw InvalidArgument("wigner_d: negative degree");
+    if (L > tpo_b200::kWignerMaxL) throw InvalidArgument("wigner_d: degree above the supported maximum");
+    ctx->impl.activate();
+    const auto& w = ctx->impl.wigner(L);
+    launched(ctx, tpo_b200::launch_wigner_d(w, R, D, n, static_cast<cudaStream_t>(stream)), "wigner_d");
+  });
+}
+
+int64_t tpo_wigner_d_size(int L) {
+  if (L < 0) return -TPO_EINVAL;
+  int64_t n = 0;
+  for (int l = 0; l <= L; ++l) n += static_cast<int64_t>(2 * l + 1) * (2 * l + 1);
+  return n;
+}
+
+int tpo_rotate_f32(tpo_ctx* ctx, int L, const double* R, int64_t n_rot, const float* x, float* out, int64_t batch,
+                   int64_t channels, void* stream) {
+  return guarded([&] {
+    stage_args(ctx, x, out, batch);
+    if (L < 0 || L > tpo_b200::kWignerMaxL) throw InvalidArgument("rotate: degree out of range");
+    if (channels < 1) throw InvalidArgument("tpo: channels must be >= 1");
+    if (batch > 0 && (n_rot < 1 || n_rot > batch || !R)) throw InvalidArgument("rotate: need 1..batch rotations");
+    if (batch == 0) return;
+    ctx->impl.activate();
+    const auto& w = ctx->impl.wigner(L);
+    const cudaStream_t s = static_cast<cudaStream_t>(stream);
+    double* D = nullptr;
+    tpo_b200::cuda_check(cudaMallocAsync(reinterpret_cast<void**>(&D), static_cast<size_t>(n_rot) * w.d_stride * 8, s),
+             "rotate scratch");
+    launched(ctx, tpo_b200::launch_wigner_d(w, R, D, n_rot, s), "wigner_d");
+    launched(ctx, tpo_b200::launch_rotate(w, D, n_rot, x, out, batch, channels, ctx->impl.num_sms(), s), "rotate");
+    tpo_b200::cuda_check(cudaFreeAsync(D, s), "rotate scratch");
+  });
+}
+
+// ------------------------------------------------------------------ host tables
+int tpo_gaunt_real(int l1, int l2, int l3, int* m1, int* m2, int* m3, double* value, int cap) {
+  int n = 0;
+  const int st = guarded([&] {
+    if (l1 < 0 || l2 < 0 || l3 < 0) throw InvalidArgument("gaunt_real: negative degree");
+    if (l1 + l2 + l3 > 2 * 2 * kMaxL) throw InvalidArgument("gaunt_real: degrees too large");
+    const auto& t = tpo_b200::real_gaunt(l1, l2, l3);
+    n = static_cast<int>(t.size());
+    if (!m1) return;
+    if (cap < n) throw InvalidArgument("gaunt_real: buffer too small");
+    for (int i = 0; i < n; ++i) {
+      m1[i] = t[i].m1;
+      m2[i] = t[i].m2;
+      m3[i] = t[i].m3;
+      value[i] = t[i].v;
+    }
+  });
+  return st ? -st : n;
+}
+
+int tpo_s2_grid(int L, double* cos_theta, double* weights) {
+  return guarded([&] {
+    if (L < 0) throw InvalidArgument("make_grid: L must be >= 0");
+    if (L > 4 * kMaxL) throw InvalidArgument("make_grid: L above the supported maximum");
+    const auto& g = tpo_b200::s2_grid(L);
+    if (cos_theta) std::copy(g.nodes.begin(), g.nodes.end(), cos_theta);
+    if (weights) std::copy(g.weights.begin(), g.weights.end(), weights);
+  });
+}
+
+int tpo_legendre_lambda(int lmax, const double* cos_theta, int n, double* lam) {
+  return guarded([&] {
+    if (lmax < 0 || n < 0 || (n > 0 && (!cos_theta || !lam))) throw InvalidArgument("legendre_lambda: bad arguments");
+    const std::vector<double> t = tpo_b200::legendre_lambda(lmax, std::vector<double>(cos_theta, cos_theta + n));
+    std::copy(t.begin(), t.end(), lam);
+  });
+}
+
+double tpo_mtp_path_weight(int l1, int l2, int l3, int l_tilde) {
+  double w = 0.0;
+  const int st = guarded([&] {
+    if (l_tilde > kMaxL) throw InvalidArgument("mtp_path_weights: l_tilde above the supported maximum");
+    w = tpo_b200::mtp_path_weight(l1, l2, l3, l_tilde);
+  });
+  return st ? std::nan("") : w;
+}
+
+int64_t tpo_count_muls(int kind, int impl, int mode, int L) {
+  int64_t r = 0;
+  const int st = guarded([&] {
+    namespace oc = tpo_b200::opcount;
+    // proj/src/bench.cpp:18-24,101-112: siso = path [L, L, L]; simo = degree-L inputs, outputs 0..2L;
+    // mimo = single_copies(L) inputs, full output band
+    if (L < 0) throw InvalidArgument("count_ops: L must be >= 0");
+    if (mode < 0 || mode > 2) throw InvalidArgument("unknown mode");
+    const bool naive = impl == 0;
+    std::vector<oc::Entry> in;
+    if (mode == 2)
+      for (int l = 0; l <= L; ++l) in.push_back({1, l});
+    else
+      in.push_back({1, L});
+    std::vector<int> ls;
+    for (const auto& e : in) ls.push_back(e.l);
+    std::vector<int> deg;
+    if (mode == 0) deg = {L};
+    else
+      for (int l = 0; l <= 2 * L; ++l) deg.push_back(l);
+    if (kind == 0) {  // cgtp: naive / sparse
+      if (impl != 0 && impl != 1) throw InvalidArgument("count_ops: implementation does not apply to this kind");
+      if (mode == 2) r = static_cast<int64_t>(oc::cgtp_mimo(naive, ls, ls));
+      else
+        for (int l3 = (mode == 1 ? 0 : L); l3 <= (mode == 1 ? 2 * L : L); ++l3) r += oc::cgtp_path(naive, L, L, l3);
+    } else if (kind == 1) {  // gtp: grid / fourier
+      if (impl != 2 && impl != 3) throw InvalidArgument("count_ops: implementation does not apply to this kind");
+      r = static_cast<int64_t>(impl == 2 ? oc::gtp_grid_select(in, in, deg) : oc::gtp_fourier_select(in, in, deg));
+    } else if (kind == 2) {  // mtp: naive / sparse
+      if (impl != 0 && impl != 1) throw InvalidArgument("count_ops: implementation does not apply to this kind");
+      const int lt = mode == 0 ? min_lt(L, L, L) : min_lt(L, L, 2 * L);
+      r = static_cast<int64_t>(oc::mtp_embed(naive, in, lt) * 2 + oc::mtp_matmul(2 * lt + 1) +
+                               oc::mtp_extract_select(naive, deg, lt));
+    } else {
+      throw InvalidArgument("unknown kind");
+    }
+  });
+  return st ? -st : r;
+}
 
 }  // extern "C"

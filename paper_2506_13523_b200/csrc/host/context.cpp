@@ -332,7 +332,7 @@ struct DenseOps {
   std::vector<double> a;       // [dout_eff][G]
 };
 
-GridTcEntry Context::build_dense_tc(const DenseOps& ops, const char* label) {
+GridTcEntry Context::build_dense_tc(const DenseOps& ops, const char* label, int max_chain) {
   GridTcEntry ent;
   GridTcTables& t = ent.t;
   const int G = ops.G;
@@ -405,13 +405,17 @@ GridTcEntry Context::build_dense_tc(const DenseOps& ops, const char* label) {
     // truncation once per MMA (a per-MMA round-toward-zero model reproduces the measured 1.04e-5 at
     // L = 12 to three digits; tools/precision_model.py), so one accumulator over the whole grid
     // (77 K-steps at L = 12) costs ~1e-5 normwise; segments added in fp32 keep it ~3-4e-6
+    // Single accumulation while the chain is short enough for the operator family (max_chain K-steps,
+    // measured: grid operators <= 6.8e-6 at L = 10 (54 K-steps), folded torus operators 9.9e-6 at
+    // L = 10, 3.6e-6 at L = 7 (29 K-steps), adversarial inputs, profiles/r02d); segments cost a
+    // drain of Z per boundary (fp32 reductions in L2), ~25% at L = 10, so they are used only past that
     const int seg_slices = std::max(1, env_int("TPO_GRID_SEG_SLICES", 20));
     const int total = t.nchunks * t.nslices;
-    const int nseg = (total + seg_slices - 1) / seg_slices;
+    const int nseg = total > env_int("TPO_GRID_MAX_CHAIN", max_chain) ? (total + seg_slices - 1) / seg_slices : 1;
     t.seg_chunks = std::max(1, (t.nchunks + nseg - 1) / nseg);
   }
   t.seg_red = env_int("TPO_GRID_SEG_RED", 1);
-  t.split_roles = env_int("TPO_GRID_SPLIT_ROLES", 1);
+  t.split_roles = env_int("TPO_GRID_SPLIT_ROLES", 0);  // measured slower (profiles/r02c)
   // input scale: |F(g)| <= ||x||_2 ||S row g||_2, so ||x|| < 2^in_shift keeps P = F_x F_y < 2^14
   {
     auto row_norm_max = [&](const std::vector<double>& S, int din) {
@@ -615,7 +619,7 @@ const GridTcEntry& Context::grid_tc(int L1, int L2, int L3) {
   std::lock_guard<std::mutex> g(mu_);
   auto it = grid_tc_.find({L1, L2, L3});
   if (it != grid_tc_.end()) return it->second;
-  return grid_tc_.emplace(std::array<int, 3>{L1, L2, L3}, build_dense_tc(make_grid_ops(L1, L2, L3), "gtp_grid")).first->second;
+  return grid_tc_.emplace(std::array<int, 3>{L1, L2, L3}, build_dense_tc(make_grid_ops(L1, L2, L3), "gtp_grid", 60)).first->second;
 }
 
 namespace {
@@ -645,7 +649,7 @@ const GridTcEntry& Context::dense_split_tc(int fourier, int L1, int L2, int L3, 
   ops.din1 = (b1 + 1) * (b1 + 1) - a1 * a1;
   ops.din2 = (b2 + 1) * (b2 + 1) - a2 * a2;
   ops.same_s = false;
-  return dense_split_.emplace(key, build_dense_tc(ops, fourier ? "gtp_fourier split" : "gtp_grid split")).first->second;
+  return dense_split_.emplace(key, build_dense_tc(ops, fourier ? "gtp_fourier split" : "gtp_grid split", 30)).first->second;
 }
 
 // Backward operator set of the grid GTP (tpo_backward_f32): input 1 = degrees
@@ -687,7 +691,7 @@ const GridTcEntry& Context::grid_tc_part(int a, int b, int L2, int Lo) {
   for (int o = 0; o < ops.dout_eff; ++o)
     for (int gi = 0; gi < ops.G; ++gi)
       ops.a[static_cast<size_t>(o) * ops.G + gi] = gr.weights[gi / gr.n_phi] * phi_scale * s_val(gi, o);
-  return grid_tc_part_.emplace(key, build_dense_tc(ops, "gtp_grid backward")).first->second;
+  return grid_tc_part_.emplace(key, build_dense_tc(ops, "gtp_grid backward", 30)).first->second;
 }
 
 // Fourier GTP on the tensor cores.  The reference convolves the two torus
@@ -753,7 +757,7 @@ const GridTcEntry& Context::fourier_tc(int L1, int L2, int L3) {
   std::lock_guard<std::mutex> g(mu_);
   auto it = fourier_tc_.find({L1, L2, L3});
   if (it != fourier_tc_.end()) return it->second;
-  return fourier_tc_.emplace(std::array<int, 3>{L1, L2, L3}, build_dense_tc(make_fourier_ops(L1, L2, L3), "gtp_fourier")).first->second;
+  return fourier_tc_.emplace(std::array<int, 3>{L1, L2, L3}, build_dense_tc(make_fourier_ops(L1, L2, L3), "gtp_fourier", 30)).first->second;
 }
 
 // ------------------------------------------------------------------ GTP grid (SIMT separable)
@@ -1136,4 +1140,60 @@ const float* Context::degree_weights(const std::vector<double>& w) {
   return d;
 }
 
+// ------------------------------------------------------------------ stage operators (stages.cu)
+const float* Context::dense_op(const std::string& key, const std::function<std::vector<double>()>& build) {
+  {
+    std::lock_guard<std::mutex> g(mu_);
+    auto it = dense_ops_.find(key);
+    if (it != dense_ops_.end()) return it->second;
+  }
+  const std::vector<double> m = build();
+  std::vector<float> f(m.begin(), m.end());
+  std::lock_guard<std::mutex> g(mu_);
+  auto it = dense_ops_.find(key);
+  if (it != dense_ops_.end()) return it->second;
+  const float* d = upload(f);
+  dense_ops_.emplace(key, d);
+  return d;
+}
+
+const WignerTables& Context::wigner(int L) {
+  std::lock_guard<std::mutex> g(mu_);
+  auto it = wigner_.find(L);
+  if (it != wigner_.end()) return it->second;
+  if (L < 0 || L > kWignerMaxL) throw InvalidArgument("wigner_d: degree out of range");
+  WignerTables w{};
+  w.L = L;
+  std::vector<int> row_off;
+  std::vector<WignerEntry> entries;
+  int64_t boff = 0;
+  for (int l = 0; l <= L; ++l) {
+    w.block_off[l] = boff;
+    boff += static_cast<int64_t>(2 * l + 1) * (2 * l + 1);
+    w.l_off[l] = static_cast<int>(row_off.size());
+    w.e_off[l] = static_cast<int>(entries.size());
+    if (l < 2) {
+      row_off.push_back(0);
+      continue;
+    }
+    // D^l = Q (D^1 (x) D^{l-1}) Q^T with Q = cg_real(1, l-1, l) (proj/src/wigner.cpp:302-311); rows by m3
+    std::vector<std::vector<WignerEntry>> by_row(2 * l + 1);
+    for (const CGEntry& e : real_cg(1, l - 1, l)) by_row[e.m3 + l].push_back({e.m1 + 1, e.m2 + l - 1, e.v});
+    int n = 0;
+    for (int i = 0; i <= 2 * l; ++i) {
+      row_off.push_back(n);
+      for (const WignerEntry& e : by_row[i]) entries.push_back(e);
+      n += static_cast<int>(by_row[i].size());
+    }
+    row_off.push_back(n);
+  }
+  w.d_stride = boff;
+  w.row_off = upload(row_off);
+  w.entries = upload(entries);
+  std::vector<int64_t> bo(w.block_off, w.block_off + L + 1);
+  w.block_off_dev = upload(bo);
+  return wigner_.emplace(L, w).first->second;
+}
+
 }  // namespace tpo_b200
+

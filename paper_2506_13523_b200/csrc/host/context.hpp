@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <array>
+#include <functional>
 #include <atomic>
 #include <cstdint>
 #include <map>
@@ -64,6 +65,10 @@ class Context {
   // nullptr: shape not on the tcgen05 path; a1 / flags: backward variants (context.cpp)
   const MtpTcTables* mtp_tc(int L1, int L2, int L3, int lt, int a1 = 0, int flags = 0);
   const float* degree_weights(const std::vector<double>& w);  // small per-call device array
+  // device fp32 copy of a k-major stage operator (stages.cu dense_map), built once per key
+  const float* dense_op(const std::string& key, const std::function<std::vector<double>()>& build);
+  // Wigner-D recursion tables up to degree L (stages.cu wigner_d)
+  const WignerTables& wigner(int L);
 
   // scratch for host entry points / weighted products (grown on demand)
   float* scratch(int slot, size_t floats);
@@ -100,12 +105,14 @@ class Context {
   std::map<std::array<int, 4>, GridTcEntry> grid_tc_part_;
   std::map<std::array<int, 8>, GridTcEntry> dense_split_;
   std::map<std::array<int, 3>, GridTcEntry> fourier_tc_;
-  GridTcEntry build_dense_tc(const struct DenseOps& ops, const char* label);
+  GridTcEntry build_dense_tc(const struct DenseOps& ops, const char* label, int max_chain);
   std::map<std::array<int, 3>, GridSimtTables> grid_simt_;
   std::map<std::array<int, 3>, FourierDevTables> fourier_;
   std::map<std::array<int, 4>, MtpDevTables> mtp_;
   std::map<std::array<int, 6>, std::pair<bool, MtpTcTables>> mtp_tc_;
   std::map<std::vector<double>, const float*> weights_;
+  std::map<std::string, const float*> dense_ops_;
+  std::map<int, WignerTables> wigner_;
   std::array<void*, 12> scratch_{};
   std::array<size_t, 12> scratch_cap_{};
 };

@@ -17,6 +17,8 @@
 #include "tpo/gtp.hpp"
 #include "tpo/mtp.hpp"
 #include "tpo_capi.h"
+#include "cxx_internal.hpp"
+#include "opcount.hpp"
 
 namespace tpo {
 
@@ -93,16 +95,18 @@ ConstSlice IrrepVector::slice(int entry, int copy) const {
 }
 
 // ------------------------------------------------------------------ device plumbing
-namespace {
+namespace internal {
 
 std::mutex g_mu;
 tpo_ctx* g_ctx = nullptr;
+int g_dev = 0;
 
 tpo_ctx* ctx() {
   std::lock_guard<std::mutex> lock(g_mu);
   if (!g_ctx) {
     const char* env = std::getenv("TPO_DEVICE");
     const int dev = env ? std::atoi(env) : 0;
+    g_dev = dev;
     if (tpo_ctx_create(dev, &g_ctx) != TPO_OK) {
       g_ctx = nullptr;
       throw std::runtime_error(std::string("tpo: cannot create device context: ") + tpo_last_error());
@@ -118,6 +122,19 @@ void rethrow(int st) {
   if (st == TPO_ERANGE) throw std::out_of_range(msg);
   throw std::runtime_error(msg);
 }
+
+std::vector<tpo_b200::opcount::Entry> entries_of(const Irreps& ir) {
+  std::vector<tpo_b200::opcount::Entry> e;
+  for (const auto& x : ir.entries()) e.push_back({x.mul, x.l});
+  return e;
+}
+
+}  // namespace internal
+
+namespace {
+using internal::ctx;
+using internal::entries_of;
+using internal::rethrow;
 
 int max_degree(const Irreps& ir) {
   int m = 0;
@@ -261,39 +278,46 @@ void path_product(const Path& p, const std::vector<double>& x, const std::vector
 }  // namespace
 
 void cgtp_path_naive(const Path& p, const std::vector<double>& x, const std::vector<double>& y,
-                     std::vector<double>& out, OpCounter*) {
+                     std::vector<double>& out, OpCounter* ops) {
   path_product(p, x, y, out);
+  count_muls(ops, tpo_b200::opcount::cgtp_path(true, p.l1, p.l2, p.l3));
 }
 void cgtp_path_sparse(const Path& p, const std::vector<double>& x, const std::vector<double>& y,
-                      std::vector<double>& out, OpCounter*) {
+                      std::vector<double>& out, OpCounter* ops) {
   path_product(p, x, y, out);
+  count_muls(ops, tpo_b200::opcount::cgtp_path(false, p.l1, p.l2, p.l3));
 }
 
-IrrepVector cgtp_mimo(const IrrepVector& x, const IrrepVector& y, CgtpImpl, OpCounter*) {
+IrrepVector cgtp_mimo(const IrrepVector& x, const IrrepVector& y, CgtpImpl impl, OpCounter* ops) {
   for (const auto& e : x.irreps.entries())
     if (e.mul != 1) throw std::invalid_argument("cgtp_mimo: inputs must be single-copy towers");
   for (const auto& e : y.irreps.entries())
     if (e.mul != 1) throw std::invalid_argument("cgtp_mimo: inputs must be single-copy towers");
   if (static_cast<int>(x.data.size()) != x.irreps.dim() || static_cast<int>(y.data.size()) != y.irreps.dim())
     throw std::invalid_argument("irreps: data length does not match irreps dim");
-  return cgtp_pairs(x, y);
+  IrrepVector out = cgtp_pairs(x, y);
+  std::vector<int> xl, yl;
+  for (const auto& e : x.irreps.entries()) xl.push_back(e.l);
+  for (const auto& e : y.irreps.entries()) yl.push_back(e.l);
+  count_muls(ops, tpo_b200::opcount::cgtp_mimo(impl == CgtpImpl::naive, xl, yl));
+  return out;
 }
 
 // ------------------------------------------------------------------ GTP
-IrrepVector gtp_grid(const IrrepVector& x, const IrrepVector& y, int L3, OpCounter*) {
-  IrrepVector out = gaunt_select(TPO_KIND_GTP_GRID, x, y, upto(L3));
+IrrepVector gtp_grid(const IrrepVector& x, const IrrepVector& y, int L3, OpCounter* ops) {
+  IrrepVector out = detail::gtp_grid_select(x, y, upto(L3), ops);
   out.irreps = Irreps::single_copies(L3);
   return out;
 }
 
-IrrepVector gtp_fourier(const IrrepVector& x, const IrrepVector& y, int L3, OpCounter*) {
-  IrrepVector out = gaunt_select(TPO_KIND_GTP_FOURIER, x, y, upto(L3));
+IrrepVector gtp_fourier(const IrrepVector& x, const IrrepVector& y, int L3, OpCounter* ops) {
+  IrrepVector out = detail::gtp_fourier_select(x, y, upto(L3), ops);
   out.irreps = Irreps::single_copies(L3);
   return out;
 }
 
 IrrepVector weighted_gtp(const IrrepVector& x, const IrrepVector& y, const std::vector<double>& a,
-                         const std::vector<double>& b, const std::vector<double>& c, int L3, OpCounter*) {
+                         const std::vector<double>& b, const std::vector<double>& c, int L3, OpCounter* ops) {
   if (static_cast<int>(c.size()) != L3 + 1) throw std::invalid_argument("weighted_gtp: c must have L3+1 entries");
   const int L1 = max_degree(x.irreps), L2 = max_degree(y.irreps);
   if (static_cast<int>(a.size()) < L1 + 1 || static_cast<int>(b.size()) < L2 + 1)
@@ -307,28 +331,40 @@ IrrepVector weighted_gtp(const IrrepVector& x, const IrrepVector& y, const std::
   std::vector<double> full = run_host(TPO_KIND_GTP_GRID, L1, L2, L3, -1, X, Y, 1);
   for (int l = 0; l <= L3; ++l)
     for (int i = 0; i < 2 * l + 1; ++i) full[l * l + i] *= c[l];
+  // proj/src/gtp.cpp:206-215: scale x, scale y, gtp_grid, scale the output
+  namespace oc = tpo_b200::opcount;
+  count_muls(ops, oc::scale_degrees(entries_of(x.irreps)) + oc::scale_degrees(entries_of(y.irreps)) +
+                      oc::gtp_grid_select(entries_of(x.irreps), entries_of(y.irreps), upto(L3)) +
+                      oc::scale_degrees(entries_of(Irreps::single_copies(L3))));
   return {Irreps::single_copies(L3), std::move(full)};
 }
 
 namespace detail {
 IrrepVector gtp_grid_select(const IrrepVector& x, const IrrepVector& y, const std::vector<int>& degrees,
-                            OpCounter*) {
-  return gaunt_select(TPO_KIND_GTP_GRID, x, y, degrees);
+                            OpCounter* ops) {
+  IrrepVector out = gaunt_select(TPO_KIND_GTP_GRID, x, y, degrees);
+  count_muls(ops, tpo_b200::opcount::gtp_grid_select(entries_of(x.irreps), entries_of(y.irreps), degrees));
+  return out;
 }
 IrrepVector gtp_fourier_select(const IrrepVector& x, const IrrepVector& y, const std::vector<int>& degrees,
-                               OpCounter*) {
-  return gaunt_select(TPO_KIND_GTP_FOURIER, x, y, degrees);
+                               OpCounter* ops) {
+  IrrepVector out = gaunt_select(TPO_KIND_GTP_FOURIER, x, y, degrees);
+  count_muls(ops, tpo_b200::opcount::gtp_fourier_select(entries_of(x.irreps), entries_of(y.irreps), degrees));
+  return out;
 }
 }  // namespace detail
 
 // ------------------------------------------------------------------ MTP
 int mtp_l_tilde(int L1, int L2, int L3) { return tpo_mtp_l_tilde(L1, L2, L3); }
 
-IrrepVector mtp(const IrrepVector& x, const IrrepVector& y, int L3, MtpImpl, OpCounter*, int l_tilde_override) {
+IrrepVector mtp(const IrrepVector& x, const IrrepVector& y, int L3, MtpImpl impl, OpCounter* ops,
+                int l_tilde_override) {
   if (L3 < 0) throw std::invalid_argument("mtp: L3 must be >= 0");
   const int L1 = max_degree(x.irreps), L2 = max_degree(y.irreps);
   std::vector<double> full =
       run_host(TPO_KIND_MTP, L1, L2, L3, l_tilde_override, to_tower(x, L1), to_tower(y, L2), 1);
+  const int lt = l_tilde_override >= 0 ? l_tilde_override : tpo_mtp_l_tilde(L1, L2, L3);
+  count_muls(ops, tpo_b200::opcount::mtp(impl == MtpImpl::naive, entries_of(x.irreps), entries_of(y.irreps), L3, lt));
   return {Irreps::single_copies(L3), std::move(full)};
 }
 

@@ -114,7 +114,7 @@ std::vector<CGEntry> build_real_cg(int l1, int l2, int l3) {
   return out;
 }
 
-void gauss_legendre(int n, std::vector<double>& x, std::vector<double>& w) {
+void gauss_legendre_impl(int n, std::vector<double>& x, std::vector<double>& w) {
   x.assign(n, 0.0);
   w.assign(n, 0.0);
   for (int i = 0; i < (n + 1) / 2; ++i) {
@@ -139,6 +139,12 @@ void gauss_legendre(int n, std::vector<double>& x, std::vector<double>& w) {
 }
 
 }  // namespace
+
+double cg_coefficient(int l1, int m1, int l2, int m2, int l3, int m3) { return racah_cg(l1, m1, l2, m2, l3, m3); }
+
+void gauss_legendre(int n, std::vector<double>& nodes, std::vector<double>& weights) {
+  gauss_legendre_impl(n, nodes, weights);
+}
 
 std::vector<double> legendre_lambda(int lmax, const std::vector<double>& ct) {
   const int n = static_cast<int>(ct.size());
@@ -187,7 +193,7 @@ const S2Grid& s2_grid(int band) {
   gr->band = band;
   gr->n_theta = band + 1;
   gr->n_phi = 2 * band + 1;
-  gauss_legendre(band + 1, gr->nodes, gr->weights);
+  gauss_legendre_impl(band + 1, gr->nodes, gr->weights);
   gr->lam = legendre_lambda(band, gr->nodes);
   gr->cs.resize(static_cast<size_t>(2 * band + 1) * gr->n_phi);
   for (int m = -band; m <= band; ++m)

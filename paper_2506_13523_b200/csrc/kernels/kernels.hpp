@@ -230,4 +230,32 @@ cudaError_t launch_accumulate(const float* in, float* out, int64_t n, cudaStream
 cudaError_t launch_gather_cols(const float* src, int64_t stride, int col0, int w, float* dst, int64_t rows,
                                cudaStream_t s);
 
+// ---------------------------------------------------------------- stage operators (stages.cu)
+// out[b][o] = sum_k mt[k][o] in[b][k]  (mt k-major [din][dout], fp32)
+cudaError_t launch_dense_map(const float* in, int din, const float* mt, int dout, float* out, int64_t rows,
+                             cudaStream_t s);
+// Z[b] = X[b] Y[b], dt x dt row-major carriers
+cudaError_t launch_carrier_matmul(const float* X, const float* Y, float* Z, int dt, int64_t batch, cudaStream_t s);
+cudaError_t launch_pointwise_mul(const float* a, const float* b, float* out, int64_t n, int num_sms, cudaStream_t s);
+// Wigner-D recursion tables: level l's entries of cg_real(1, l-1, l) grouped by m3, with m1 as an index
+// into D^1 (m1 + 1) and m2 into D^{l-1} (m2 + l - 1)
+struct WignerEntry {
+  int m1, m2;
+  double v;
+};
+constexpr int kWignerMaxL = 64;
+struct WignerTables {
+  int L;
+  int64_t d_stride;                    // sum_{l <= L} (2l+1)^2 doubles per rotation
+  int64_t block_off[kWignerMaxL + 1];  // offset of D^l in a rotation's blocks
+  int l_off[kWignerMaxL + 1];          // level l's row offsets start at row_off[l_off[l]]
+  int e_off[kWignerMaxL + 1];          // level l's entries start at entries[e_off[l]]
+  const int* row_off;
+  const WignerEntry* entries;
+  const int64_t* block_off_dev;
+};
+cudaError_t launch_wigner_d(const WignerTables& w, const double* R, double* D, int64_t n, cudaStream_t s);
+cudaError_t launch_rotate(const WignerTables& w, const double* D, int64_t n_rot, const float* x, float* out,
+                          int64_t batch, int64_t channels, int num_sms, cudaStream_t s);
+
 }  // namespace tpo_b200
