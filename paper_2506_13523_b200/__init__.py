@@ -44,7 +44,7 @@ def mtp_l_tilde(L1: int, L2: int, L3: int) -> int:
     return int(lib().tpo_mtp_l_tilde(L1, L2, L3))
 
 
-def _prep(x, y, L1, L2, kind, L3):
+def _prep(x, y, L1, L2, kind, L3, out=None):
     import torch
 
     if not (isinstance(x, torch.Tensor) and isinstance(y, torch.Tensor)):
@@ -79,18 +79,21 @@ def _prep(x, y, L1, L2, kind, L3):
     y = y.contiguous()
     dout = out_dim(kind, L1, L2, L3)
     shape = (B, dout) if x.dim() == 2 else (B, C, dout)
-    out = torch.empty(shape, dtype=torch.float32, device=x.device)
+    if out is None:
+        out = torch.empty(shape, dtype=torch.float32, device=x.device)
+    else:  # caller's buffer: must be exactly the output on the inputs' device
+        if not isinstance(out, torch.Tensor) or tuple(out.shape) != shape or out.dtype != torch.float32 \
+                or not out.is_contiguous():
+            raise ValueError("out has the wrong shape/dtype or is not contiguous")
+        if out.device != x.device:
+            raise ValueError("out must be on the inputs' device")
     stream = torch.cuda.current_stream(x.device).cuda_stream
     return x, y, out, B, C, y_shared, stream
 
 
 def run(kind: str, x, y, L1: int, L2: int, L3: int = 0, l_tilde: int = -1, out=None):
     """Generic batched dispatch through tpo_run_f32."""
-    x, y, o, B, C, ys, stream = _prep(x, y, L1, L2, kind, L3)
-    if out is not None:
-        if out.shape != o.shape or out.dtype != o.dtype or not out.is_contiguous():
-            raise ValueError("out has the wrong shape/dtype or is not contiguous")
-        o = out
+    x, y, o, B, C, ys, stream = _prep(x, y, L1, L2, kind, L3, out)
     ctx = context(x.device.index)
     check(lib().tpo_run_f32(ctx.handle, KINDS[kind], L1, L2, L3, l_tilde, x.data_ptr(), y.data_ptr(),
                             o.data_ptr(), B, C, ys, stream))
@@ -115,9 +118,21 @@ def run_host_batch(requests, device: int = 0):
         for t in (x, y, out):
             if t.device.type != "cpu" or not t.is_contiguous() or t.dtype != torch.float32:
                 raise ValueError("run_host_batch: host tensors must be contiguous fp32 on the CPU")
+        # the C ABI copies batch x channels rows through raw pointers: every extent must match
+        d1, d2 = tower_dim(L1), tower_dim(L2)
+        if x.dim() not in (2, 3) or x.shape[-1] != d1:
+            raise ValueError(f"run_host_batch: x must be [B, {d1}] or [B, C, {d1}]")
         B = x.shape[0]
         Cn = x.shape[1] if x.dim() == 3 else 1
         ys = 1 if (x.dim() == 3 and y.dim() == 2) else 0
+        if ys:
+            if tuple(y.shape) != (B, d2):
+                raise ValueError(f"run_host_batch: shared y must be [{B}, {d2}]")
+        elif tuple(y.shape) != tuple(x.shape[:-1]) + (d2,):
+            raise ValueError(f"run_host_batch: y must be {tuple(x.shape[:-1]) + (d2,)}")
+        dout = out_dim(kind, L1, L2, L3)
+        if out.numel() != B * Cn * dout:
+            raise ValueError(f"run_host_batch: out must hold {B} x {Cn} x {dout} floats")
         q = reqs[i]
         q.kind, q.L1, q.L2, q.L3, q.l_tilde, q.y_shared = KINDS[kind], L1, L2, L3, lt, ys
         q.batch, q.channels = B, Cn

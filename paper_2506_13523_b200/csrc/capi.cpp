@@ -26,8 +26,20 @@ namespace {
 constexpr int kMaxL = 32;  // inputs; outputs up to 2 * kMaxL
 thread_local std::string g_err;
 
+// restores the caller's current device (recorded by Context::activate) when a C-ABI call returns
+struct RestoreDevice {
+  ~RestoreDevice() {
+    int& prev = tpo_b200::caller_device();
+    if (prev >= 0) {
+      cudaSetDevice(prev);
+      prev = -1;
+    }
+  }
+};
+
 template <class F>
 int guarded(F&& f) {
+  RestoreDevice restore;
   try {
     f();
     return TPO_OK;
@@ -634,6 +646,13 @@ void run_host_requests(tpo_ctx* ctx, const tpo_host_request* reqs, int n) {
   for (int i = 0; i < n; ++i) {
     const tpo_host_request& q = reqs[i];
     check_args(ctx, q.L1, q.L2, q.x, q.y, q.out, q.batch, q.channels);
+    // everything run_kind would reject is rejected here, before any chunk is queued
+    if (q.kind != TPO_KIND_CGTP) check_L3(q.L3, "tpo_run_host");
+    if (q.kind == TPO_KIND_MTP && q.l_tilde >= 0) {
+      if (q.l_tilde < min_lt(q.L1, q.L2, q.L3))
+        throw InvalidArgument("mtp: l_tilde below the minimal carrier degree");
+      if (q.l_tilde > kMaxL) throw InvalidArgument("mtp: l_tilde above the supported maximum");
+    }
     Plan& pl = plan[static_cast<size_t>(i)];
     pl.dout = out_dim(q.kind, q.L1, q.L2, q.L3);
     pl.d1 = (q.L1 + 1) * (q.L1 + 1);
@@ -660,6 +679,19 @@ void run_host_requests(tpo_ctx* ctx, const tpo_host_request* reqs, int n) {
     dz[b] = c.scratch(3 * b + 2, need_z);
   }
   const cudaStream_t si = c.h2d_stream(), sc = c.host_stream(), so = c.d2h_stream();
+  // on any exception below, drain the three pipeline streams before returning: queued async copies
+  // must not keep writing into the caller's buffers after the call reports its error
+  struct Drain {
+    cudaStream_t a, b, c;
+    bool armed = true;
+    ~Drain() {
+      if (armed) {
+        cudaStreamSynchronize(a);
+        cudaStreamSynchronize(b);
+        cudaStreamSynchronize(c);
+      }
+    }
+  } drain{si, sc, so};
   // optional (TPO_HOST_RAMP=1) chunk ramp bc/8 .. bc .. bc/8 to shorten the unoverlapped first
   // copy-in / last copy-out; measured slower than uniform chunks (more per-chunk overhead)
   static const bool ramp = [] {
@@ -703,6 +735,7 @@ void run_host_requests(tpo_ctx* ctx, const tpo_host_request* reqs, int n) {
       cuda_check_s(cudaEventRecord(c.pipe_event(2, b), so), "record d2h");
     }
   }
+  drain.armed = false;
   cuda_check_s(cudaStreamSynchronize(so), "sync");
   cuda_check_s(cudaStreamSynchronize(sc), "sync");
   cuda_check_s(cudaStreamSynchronize(si), "sync");
@@ -776,12 +809,10 @@ int tpo_fourier_table(int L, int which, int* counts, int* u, int* v, double* re,
 
 int tpo_set_gtp_grid_path(tpo_ctx* ctx, int path) {
   if (!ctx || path < 0 || path > 2) return -TPO_EINVAL;
-  const int prev = ctx->impl.grid_path;
-  ctx->impl.grid_path = path;
-  return prev;
+  return ctx->impl.grid_path.exchange(path);
 }
 
-int tpo_last_gtp_grid_path(const tpo_ctx* ctx) { return ctx ? ctx->impl.last_grid_path : -TPO_EINVAL; }
+int tpo_last_gtp_grid_path(const tpo_ctx* ctx) { return ctx ? ctx->impl.last_grid_path.load() : -TPO_EINVAL; }
 
 }  // extern "C"
 

@@ -59,12 +59,14 @@ Context::Context(int device) : device_(device) {
   cuda_check(cudaSetDevice(device), "cudaSetDevice");
   cudaDeviceProp prop{};
   cuda_check(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
-  if (prop.major != 10)
+  if (prop.major != 10 || prop.minor != 0)  // the fatbin holds sm_100a SASS only (no PTX, no sm_103)
     throw CudaFailure("device is sm_" + std::to_string(prop.major) + std::to_string(prop.minor) +
                       "; this library is built for sm_100a (B200) only");
   num_sms_ = prop.multiProcessorCount;
   {  // stream-ordered temporaries (backward / weighted / degree-group passes) stay mapped between
-     // calls up to 4 GiB (re-mapping them per call cost ~1.3 ms); larger pools shrink at syncs
+     // calls up to 4 GiB (re-mapping them per call cost ~1.3 ms); larger pools shrink at syncs.
+     // Note: this is the device's default pool, shared with the rest of the process (e.g. other
+     // libraries' cudaMallocAsync), whose release threshold it raises to 4 GiB.
     cudaMemPool_t pool;
     if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
       uint64_t keep = 4ull << 30;
@@ -91,7 +93,19 @@ Context::~Context() {
       if (e) cudaEventDestroy(e);
 }
 
-void Context::activate() const { cuda_check(cudaSetDevice(device_), "cudaSetDevice"); }
+int& caller_device() {
+  thread_local int dev = -1;
+  return dev;
+}
+
+void Context::activate() const {
+  int& prev = caller_device();
+  if (prev < 0) {
+    int cur = 0;
+    if (cudaGetDevice(&cur) == cudaSuccess) prev = cur;
+  }
+  cuda_check(cudaSetDevice(device_), "cudaSetDevice");
+}
 
 void* Context::dev_alloc(size_t bytes) {
   void* p = nullptr;

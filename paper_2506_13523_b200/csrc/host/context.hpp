@@ -31,6 +31,11 @@ struct CudaFailure : std::runtime_error {
 
 void cuda_check(cudaError_t e, const char* what);
 
+// Device the calling thread had current before the first Context::activate() of the running C-ABI
+// call (-1: untouched); the C-ABI wrapper restores it when the call returns, so an entry point never
+// leaves the caller's current device switched.
+int& caller_device();
+
 // 2-D TMA tensor map (driver cuTensorMapEncodeTiled through the runtime's entry point)
 void encode_tmap_2d(CUtensorMap* m, CUtensorMapDataType dt, const void* base, uint64_t inner, uint64_t outer,
                     uint64_t row_stride_bytes, uint32_t box_inner, uint32_t box_outer, CUtensorMapSwizzle sw);
@@ -81,8 +86,8 @@ class Context {
   std::mutex& host_path_mutex() { return host_mu_; }
 
   std::atomic<int64_t> launches{0};
-  int grid_path = 0;       // 0 auto, 1 tcgen05, 2 simt (also selects the Fourier GTP path)
-  int last_grid_path = 0;
+  std::atomic<int> grid_path{0};       // 0 auto, 1 tcgen05, 2 simt (also selects the Fourier GTP path)
+  std::atomic<int> last_grid_path{0};  // diagnostics: path of the most recent GTP call on this context
 
  private:
   template <class T>

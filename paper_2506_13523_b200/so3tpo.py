@@ -4,10 +4,11 @@ product per call, irreps strings, numpy fp64 vectors in and out, ValueError
 on bad input (proj/README.md:149-152).  Computation runs on the B200 through
 the C ABI (tpo_run_host_f32); results are fp32-accurate (normwise 1e-5).
 
-Provided: irreps_dim, single_copies, cg_table (real CG only), cgtp, gtp
-(impl "grid" | "fourier"), mtp.  The analysis functions of the reference
-module (expressivity_*, interactable, count_ops, verify*, wigner_d, rotate,
-mtp_path_weights) are outside the hot path and not provided.
+Provided: irreps_dim, single_copies, cg_table (real CG or Gaunt), cgtp, gtp
+(impl "grid" | "fourier"), mtp, mtp_path_weights, wigner_d, rotate (GPU),
+count_ops (the reference's instrumented multiply counts).  The analysis
+suites of the reference module (expressivity_*, interactable, verify*) are
+outside the hot path and not provided.
 """
 from __future__ import annotations
 
@@ -16,7 +17,7 @@ import re
 
 import numpy as np
 
-from ._lib import KINDS, check, context, lib
+from ._lib import KINDS, TPO_EINVAL, check, context, lib
 
 _ENTRY = re.compile(r"^(\d+)x(\d+)$")
 
@@ -48,16 +49,95 @@ def single_copies(L: int) -> str:
 
 
 def cg_table(l1: int, l2: int, l3: int, gaunt: bool = False):
-    """Sparse real CG table as (m1, m2, m3, value) tuples (py_core.cpp:62-72)."""
-    if gaunt:
-        raise NotImplementedError("gaunt tables are not part of the device path")
-    n = lib().tpo_cg_real(l1, l2, l3, None, None, None, None, 0)
+    """Sparse real coupling table as (m1, m2, m3, value) tuples: real CG or, with gaunt=True, the
+    real Gaunt coefficients (py_core.cpp:62-72)."""
+    fn = lib().tpo_gaunt_real if gaunt else lib().tpo_cg_real
+    n = fn(l1, l2, l3, None, None, None, None, 0)
     if n < 0:
         check(-n)
     a = np.empty(n, np.int32); b = np.empty(n, np.int32); c = np.empty(n, np.int32); v = np.empty(n)
     p = lambda z: z.ctypes.data_as(C.c_void_p)  # noqa: E731
-    lib().tpo_cg_real(l1, l2, l3, p(a), p(b), p(c), p(v), n)
+    fn(l1, l2, l3, p(a), p(b), p(c), p(v), n)
     return [(int(i), int(j), int(k), float(x)) for i, j, k, x in zip(a, b, c, v)]
+
+
+def mtp_path_weights(l1: int, l2: int, l3: int, l_tilde: int) -> float:
+    """Per-path CG weight realized by the matrix product (py_core.cpp:110-116)."""
+    w = lib().tpo_mtp_path_weight(l1, l2, l3, l_tilde)
+    if w != w:
+        check(TPO_EINVAL)
+    return float(w)
+
+
+_KIND = {"cgtp": 0, "gtp": 1, "mtp": 2}
+_IMPL = {"naive": 0, "sparse": 1, "grid": 2, "fourier": 3}
+_MODE = {"siso": 0, "simo": 1, "mimo": 2}
+
+
+def count_ops(kind: str, impl: str, mode: str, L: int) -> int:
+    """Instrumented multiply count for one application (py_core.cpp:157-172)."""
+    if kind not in _KIND:
+        raise ValueError(f"unknown kind '{kind}'")
+    if impl not in _IMPL:
+        raise ValueError(f"unknown impl '{impl}'")
+    if mode not in _MODE:
+        raise ValueError(f"unknown mode '{mode}'")
+    r = int(lib().tpo_count_muls(_KIND[kind], _IMPL[impl], _MODE[mode], L))
+    if r < 0:
+        check(-r)
+    return r
+
+
+def _axis_angle(axis, angle):
+    """Rotation::from_axis_angle (proj/src/wigner.cpp:200-206), row-major 3x3."""
+    a = np.asarray(axis, dtype=np.float64).reshape(3)
+    n = float(np.linalg.norm(a))
+    if n == 0.0:
+        raise ValueError("rotation: zero axis")
+    u = a / n
+    c, s = np.cos(angle), np.sin(angle)
+    K = np.array([[0, -u[2], u[1]], [u[2], 0, -u[0]], [-u[1], u[0], 0]])
+    return c * np.eye(3) + (1 - c) * np.outer(u, u) + s * K
+
+
+def wigner_d(l: int, axis, angle: float):
+    """Real Wigner-D matrix of the rotation by `angle` about `axis` (py_core.cpp:118-124), computed
+    on the GPU (tpo_wigner_d_f64)."""
+    import torch
+
+    if l < 0:
+        raise ValueError("wigner_d: negative degree")
+    R = torch.from_numpy(_axis_angle(axis, angle)[None]).cuda()
+    from . import wigner_d as _wd
+
+    return _wd(R, l)[l][0].cpu().numpy()
+
+
+def rotate(irreps: str, x, axis, angle: float):
+    """Apply a rotation blockwise through the Wigner-D matrices (py_core.cpp:126-133), on the GPU
+    (tpo_rotate_f32)."""
+    import torch
+
+    from . import rotate as _rot
+
+    ents, data = _vector(irreps, x)
+    if not ents:
+        return data.copy()
+    L = max(l for _, l in ents)
+    rows, offs, off = [], [], 0
+    for mul, l in ents:  # one row per copy: a tower of the largest degree holding that block
+        for _ in range(mul):
+            r = np.zeros((L + 1) ** 2, np.float32)
+            r[l * l:(l + 1) ** 2] = data[off:off + 2 * l + 1]
+            rows.append(r)
+            offs.append((l, off))
+            off += 2 * l + 1
+    R = torch.from_numpy(_axis_angle(axis, angle)[None]).cuda()
+    out = _rot(torch.from_numpy(np.stack(rows)).cuda(), R, L).cpu().numpy().astype(np.float64)
+    res = np.empty_like(data)
+    for i, (l, o) in enumerate(offs):
+        res[o:o + 2 * l + 1] = out[i, l * l:(l + 1) ** 2]
+    return res
 
 
 def _vector(irreps: str, data):

@@ -79,3 +79,35 @@ def test_gtp_impls_agree_and_scalars(so3):
     assert np.abs(grid - fourier).max() <= 1e-5 * np.abs(grid).max()
     _, z = so3.mtp("1x0", np.array([3.0]), "1x0", np.array([-2.0]), 0)
     assert z[0] == pytest.approx(-6.0, rel=1e-6)
+
+
+def test_shim_tables_and_counts_cpu(orc):
+    # host-side pieces of the module need no device: cg_table(gaunt=True), mtp_path_weights, count_ops
+    from paper_2506_13523_b200 import so3tpo
+
+    g = so3tpo.cg_table(2, 4, 2, gaunt=True)
+    ref = orc.gaunt_real(2, 4, 2)
+    assert [e[:3] for e in g] == [e[:3] for e in ref]
+    assert max(abs(a[3] - b[3]) for a, b in zip(g, ref)) < 1e-13
+    assert abs(so3tpo.mtp_path_weights(1, 1, 2, 1) - orc.mtp_path_weight(1, 1, 2, 1)) < 1e-12
+    assert so3tpo.count_ops("cgtp", "sparse", "mimo", 2) == orc.count_ops("cgtp", "sparse", "mimo", 2) == 1560
+    with pytest.raises(ValueError):
+        so3tpo.count_ops("gtp", "naive", "mimo", 2)
+    with pytest.raises(ValueError):
+        so3tpo.count_ops("cgtp", "sparse", "bogus", 2)
+
+
+@pytest.mark.gpu
+def test_shim_wigner_rotate(orc):
+    # py_core.cpp:118-133 signatures, on the GPU
+    import numpy as np
+
+    from paper_2506_13523_b200 import so3tpo
+
+    D = so3tpo.wigner_d(3, [1.0, 2.0, -0.5], 0.7)
+    R = so3tpo._axis_angle([1.0, 2.0, -0.5], 0.7)
+    assert np.abs(D - orc.wigner_d(3, R)).max() < 1e-10
+    x = np.random.default_rng(1).standard_normal(so3tpo.irreps_dim("2x1+1x3"))
+    out = so3tpo.rotate("2x1+1x3", x, [0.0, 0.0, 1.0], 1.1)
+    ref = orc.rotate([1, 1, 3], x, so3tpo._axis_angle([0.0, 0.0, 1.0], 1.1))
+    assert np.abs(out - ref).max() < 1e-5 * np.abs(ref).max()
