@@ -68,6 +68,11 @@ def bytes_per_tp(kind, L):
     return 4 * (2 * din(L) + dout(kind, L))
 
 
+def c4_bytes_per_edge():
+    """read x (128 channels x 16) and the shared y (16) once, write 128 x 256."""
+    return C4_CHANNELS * 16 * 4 + 16 * 4 + C4_CHANNELS * 256 * 4
+
+
 def dense_flops_per_tp(kind, L):
     """Dense-GEMM flops of the fused tcgen05 kernels: grid 2 G (2 Din + Dout) with
     G = (2L+1)(4L+1) product-grid points; Fourier the same on the N^2/2 folded torus
@@ -359,8 +364,8 @@ def plan_only(args, world, rank):
     if world > 1:
         dist.init_process_group("gloo")
     units = step_units(args, world)
-    mine = [sum(n for _, _, n in units), sum(bytes_per_tp("cgtp" if k == "cgtp_edge" else k, L) * n
-                                               for k, L, n in units)]
+    mine = [sum(n for _, _, n in units), sum(c4_bytes_per_edge() * (n // C4_CHANNELS) if k == "cgtp_edge"
+                                               else bytes_per_tp(k, L) * n for k, L, n in units)]
     every = gather_checksums(mine)
     if rank == 0:
         print(json.dumps({"plan": True, "n_gpus": world, "config": workload_config(args, world),
@@ -536,7 +541,7 @@ def run_ours(args, world, rank, local):
             path = "simt"
         t_roof, bound = roofline_time(ek, L, n, peaks, path)
         if w == "c4":
-            t_roof = n // C4_CHANNELS * (C4_CHANNELS * 16 * 4 + 16 * 4 + C4_CHANNELS * 256 * 4) / (peaks["hbm_gbs"] * 1e9)
+            t_roof = n // C4_CHANNELS * c4_bytes_per_edge() / (peaks["hbm_gbs"] * 1e9)
             bound = "hbm"
         per[f"{kind}_L{L}"] = {"ms": round(ms, 5), "tp_per_s": round(n / (ms / 1e3), 1), "bound": bound,
                                "roofline_frac": round(t_roof / (ms / 1e3), 4)}
@@ -553,7 +558,7 @@ def run_ours(args, world, rank, local):
                     "peak_note": f"{peaks['source']} bf16 dense {peaks['bf16_tflops']} TF/s / 3 (three fp16 MMAs per "
                                  f"3xFP16 product); algorithmic flops = dense 2*G*(2Din+Dout) per TP x {dn} TPs per launch"}
     else:
-        by = (dn // C4_CHANNELS * (C4_CHANNELS * 16 * 4 + 16 * 4 + C4_CHANNELS * 256 * 4) if w == "c4"
+        by = (dn // C4_CHANNELS * c4_bytes_per_edge() if w == "c4"
               else bytes_per_tp("cgtp" if dk == "cgtp" else dk, dL) * dn)
         ach = by / (dms / 1e3) / 1e9
         kname = {"cgtp": "cgtp_edge_tc_kernel" if w == "c4" else "cgtp (tcgen05 blocks / SIMT)",
@@ -581,7 +586,7 @@ def run_ours(args, world, rank, local):
     gather_ms = None
     if not args.no_parity:
         t0 = time.perf_counter()
-        parity, gather_ms = gather_and_check(args, world, rank, probs, dev, dist)
+        parity, gather_ms = gather_and_check(args, world, rank, probs, dev, dist, launch)
         parity["seconds"] = round(time.perf_counter() - t0, 2)
 
     # ---------------- e2e through the C ABI with pinned host buffers
@@ -624,7 +629,7 @@ def run_ours(args, world, rank, local):
         dist.destroy_process_group()
 
 
-def gather_and_check(args, world, rank, probs, dev, dist):
+def gather_and_check(args, world, rank, probs, dev, dist, launch):
     """After the timed region: every rank's parity subsample (inputs + outputs of strided rows,
     the last rows included) goes to rank 0 over NCCL (c2/c3: the whole output shards are
     all-gathered first, as the result gather), and rank 0 checks it against the fp64 oracle."""
@@ -646,6 +651,10 @@ def gather_and_check(args, world, rank, probs, dev, dist):
             dist.all_gather_into_tensor(full, o.contiguous())
             torch.cuda.synchronize()
             t_gather = (t_gather or 0.0) + (time.perf_counter() - t0) * 1e3
+        # outputs past 4 GiB share one ring buffer across chunks (and the timed steps overwrote it):
+        # recompute the sampled launch (deterministic) before reading its rows
+        launch(p)
+        torch.cuda.synchronize()
         rows = x.shape[0]
         idx = torch.from_numpy(subsample_idx(rows, k_rows)).to(dev)
         xs, ys, os_ = x[idx].contiguous(), y[idx].contiguous(), o[idx].contiguous()

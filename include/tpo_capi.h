@@ -188,6 +188,16 @@ int64_t tpo_wigner_d_size(int L);
 int tpo_rotate_f32(tpo_ctx* ctx, int L, const double* R, int64_t n_rot, const float* x, float* out, int64_t batch,
                    int64_t channels, void* stream);
 
+/* Per-path weighted CGTP (the MACE "uvu" edge product): path p = (l1, l2, l3) in
+ * the reference's order (proj/src/cgtp.cpp:152-163) is scaled by w[e * n_paths + p] for edge e =
+ * row / channels (w_per_edge != 0; the usual case, weights from a radial network per edge) or by
+ * w[p] for every row (w_per_edge == 0); w is a DEVICE fp32 array.  Fused into the shared-y edge
+ * kernel's M_y (config C4 shape), an output scaling pass otherwise. */
+int tpo_cgtp_num_paths(int L1, int L2);
+int tpo_cgtp_weighted_f32(tpo_ctx* ctx, int L1, int L2, const float* w, int w_per_edge, const float* x,
+                          const float* y, float* out, int64_t batch, int64_t channels, int y_shared,
+                          void* stream);
+
 /* Host tables / analysis (table-time, no device) ----------------------------
  * gaunt_real (proj/include/tpo/wigner.hpp:64, pybind cg_table(gaunt=True)): same contract as
  * tpo_cg_real. */

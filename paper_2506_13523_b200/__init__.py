@@ -437,3 +437,32 @@ def rotate(x, R, L: int):
 
 __all__ += ["to_sphere", "from_sphere", "pointwise_mul", "mtp_embed", "mtp_matmul", "mtp_extract", "apply_linear",
             "linear_connections", "wigner_d", "rotate"]
+
+
+def cgtp_num_paths(L1: int, L2: int) -> int:
+    """Number of (l1, l2, l3) paths of cgtp(L1, L2), the reference's order (proj/src/cgtp.cpp:152-163)."""
+    return int(lib().tpo_cgtp_num_paths(L1, L2))
+
+
+def cgtp_weighted(x, y, w, L1: int, L2: int, out=None):
+    """Per-path weighted CGTP (MACE "uvu"): path p of sample b scaled by w[b, p] (w [B, n_paths], per
+    edge) or w[p] (w [n_paths], shared).  Fused into the shared-y edge kernel (C4 shape)."""
+    import torch
+
+    x, y, o, B, C, ys, stream = _prep(x, y, L1, L2, "cgtp", 0, out)
+    npth = cgtp_num_paths(L1, L2)
+    if not isinstance(w, torch.Tensor) or w.device != x.device or w.dtype != torch.float32:
+        raise ValueError("w must be a float32 tensor on the inputs' device")
+    if tuple(w.shape) == (B, npth):
+        per_edge = 1
+    elif tuple(w.shape) == (npth,):
+        per_edge = 0
+    else:
+        raise ValueError(f"w must be [{B}, {npth}] or [{npth}]")
+    w = w.contiguous()
+    check(lib().tpo_cgtp_weighted_f32(context(x.device.index).handle, L1, L2, w.data_ptr(), per_edge, x.data_ptr(),
+                                      y.data_ptr(), o.data_ptr(), B, C, ys, stream))
+    return o
+
+
+__all__ += ["cgtp_num_paths", "cgtp_weighted"]

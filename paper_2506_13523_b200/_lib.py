@@ -89,6 +89,8 @@ def lib():
             "tpo_legendre_lambda": (i, [i, p, i, p]),
             "tpo_mtp_path_weight": (d, [i, i, i, i]),
             "tpo_count_muls": (i64, [i, i, i, i]),
+            "tpo_cgtp_num_paths": (i, [i, i]),
+            "tpo_cgtp_weighted_f32": (i, [p, i, i, p, i, p, p, p, i64, i64, i, p]),
         }
         for name, (res, args) in sig.items():
             if os.environ.get("TPO_LIB_PATH") and not hasattr(L, name):
@@ -109,6 +111,7 @@ EXPORTED = [
     "tpo_to_sphere_f32", "tpo_from_sphere_f32", "tpo_pointwise_mul_f32", "tpo_mtp_embed_f32", "tpo_mtp_matmul_f32",
     "tpo_mtp_extract_f32", "tpo_apply_linear_f32", "tpo_wigner_d_f64", "tpo_wigner_d_size", "tpo_rotate_f32",
     "tpo_gaunt_real", "tpo_s2_grid", "tpo_legendre_lambda", "tpo_mtp_path_weight", "tpo_count_muls",
+    "tpo_cgtp_num_paths", "tpo_cgtp_weighted_f32",
 ]
 
 

@@ -3,6 +3,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <cstring>
 #include <cmath>
 #include <string>
 #include <vector>
@@ -95,8 +96,22 @@ void launched(tpo_ctx* ctx, cudaError_t e, const char* what) {
 
 int min_lt(int L1, int L2, int L3) { return (std::max({L1, L2, L3}) + 1) / 2; }
 
-void run_cgtp(tpo_ctx* ctx, int L1, int L2, const RowSpec& rs, cudaStream_t s) {
+// optional per-path weights of the CGTP (f2): w[(row / channels) * stride + path]
+struct PathWeights {
+  const float* w;
+  int64_t stride;
+  const int* path_of_out;
+};
+
+void run_cgtp(tpo_ctx* ctx, int L1, int L2, const RowSpec& rs, cudaStream_t s, const PathWeights* pw = nullptr) {
   const auto& t = ctx->impl.cgtp(L1, L2);
+  // kernels without a fused weight: scale the written outputs afterwards
+  auto post_scale = [&] {
+    if (pw)
+      launched(ctx, tpo_b200::launch_path_scale(rs.out, rs.rows, rs.channels, t.dout, pw->path_of_out, pw->w, pw->stride,
+                                                ctx->impl.num_sms(), s),
+               "cgtp path weights");
+  };
   // shared y per edge (config C4): per-edge dense GEMMs on tcgen05 when the shape allows
   const int kp = (t.din1 + 15) / 16 * 16, dout_pad = (t.dout + 15) / 16 * 16;
   const bool aligned = (reinterpret_cast<uintptr_t>(rs.x) % 16 == 0) && (reinterpret_cast<uintptr_t>(rs.out) % 16 == 0) &&
@@ -116,6 +131,11 @@ void run_cgtp(tpo_ctx* ctx, int L1, int L2, const RowSpec& rs, cudaStream_t s) {
     tpo_b200::encode_tmap_2d(&p.tm_out, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, rs.out, static_cast<uint64_t>(t.dout),
                              static_cast<uint64_t>(rs.rows), static_cast<uint64_t>(t.dout) * 4, 32, 128,
                              CU_TENSOR_MAP_SWIZZLE_128B);
+    if (pw) {  // fused: the weights scale the edge's M_y columns
+      p.path_w = pw->w;
+      p.w_stride = pw->stride;
+      p.path_of_out = pw->path_of_out;
+    }
     launched(ctx, tpo_b200::launch_cgtp_edge_tc(t, p, rs, ctx->impl.num_sms(), s), "cgtp edge tcgen05 kernel");
     return;
   }
@@ -127,9 +147,11 @@ void run_cgtp(tpo_ctx* ctx, int L1, int L2, const RowSpec& rs, cudaStream_t s) {
   if (std::max(L1, L2) >= tc_min_l)
     if (const tpo_b200::CgtpTcTables* tc = ctx->impl.cgtp_tc(L1, L2)) {
       launched(ctx, tpo_b200::launch_cgtp_tc(*tc, rs, ctx->impl.num_sms(), s), "cgtp tcgen05 kernel");
+      post_scale();
       return;
     }
   launched(ctx, tpo_b200::launch_cgtp(t, rs, ctx->impl.num_sms(), s), "cgtp kernel");
+  post_scale();
 }
 
 // Inputs wider than the tcgen05 kernel's K limit (L > 12): the product is bilinear,
@@ -137,9 +159,17 @@ void run_cgtp(tpo_ctx* ctx, int L1, int L2, const RowSpec& rs, cudaStream_t s) {
 // operators restricted to those columns (Context::dense_split_tc), input windows
 // packed by a gather kernel, partial outputs accumulated.  Returns false when a
 // part does not fit either.
-// L <= 14: at L = 16 the summed 3xFP16 parts reach 1.02e-5 (grid) / 1.08e-5 (Fourier) normwise,
-// past the 1e-5 contract, and gain little over SIMT (70 vs 81 ms per 2^19 shard)
-constexpr int kMaxSplitL = 14;
+// Fourier: up to L = 16 (L = 15 / 16 adversarial worst 3.8e-6 / 2.7e-6 after the operand scaling and
+// segmented accumulation; 118 / 155 ms per 2^19 shard against 299 / 503 ms on SIMT, profiles/r02i).
+// Grid: L <= 14 (the SIMT separable path is faster at 15 / 16: 61 / 80 vs 109 / 154 ms).
+const int kMaxSplitL = [] {
+  const char* v = std::getenv("TPO_GRID_SPLIT_MAXL");  // accuracy experiments only
+  return v ? std::atoi(v) : 14;
+}();
+const int kMaxSplitLFourier = [] {
+  const char* v = std::getenv("TPO_FOURIER_SPLIT_MAXL");  // accuracy experiments only
+  return v ? std::atoi(v) : 16;
+}();
 bool run_dense_split(tpo_ctx* ctx, int fourier, int L1, int L2, int L3, const RowSpec& rs, cudaStream_t s) {
   Context& c = ctx->impl;
   static const int kmax = [] {
@@ -236,7 +266,8 @@ void run_fourier(tpo_ctx* ctx, int L1, int L2, int L3, const RowSpec& rs, cudaSt
       launched(ctx, tpo_b200::launch_gtp_grid_tc(e.t, rs, c.num_sms(), s), "gtp_fourier tcgen05 kernel");
       return;
     }
-    if (std::max(L1, L2) > 12 && std::max(L1, L2) <= kMaxSplitL && run_dense_split(ctx, 1, L1, L2, L3, rs, s)) return;
+    if (std::max(L1, L2) > 12 && std::max(L1, L2) <= kMaxSplitLFourier && run_dense_split(ctx, 1, L1, L2, L3, rs, s))
+      return;
     if (c.grid_path == 1) throw InvalidArgument("gtp_fourier: shape does not fit the tcgen05 tiling");
   }
   c.last_grid_path = 2;
@@ -1095,6 +1126,44 @@ int64_t tpo_count_muls(int kind, int impl, int mode, int L) {
     }
   });
   return st ? -st : r;
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------------ per-path weighted CGTP (f2)
+namespace {
+int num_paths(int L1, int L2) {
+  int n = 0;
+  for (int l1 = 0; l1 <= L1; ++l1)
+    for (int l2 = 0; l2 <= L2; ++l2) n += 2 * std::min(l1, l2) + 1;
+  return n;
+}
+}  // namespace
+
+extern "C" {
+
+int tpo_cgtp_num_paths(int L1, int L2) { return (L1 < 0 || L2 < 0) ? -TPO_EINVAL : num_paths(L1, L2); }
+
+int tpo_cgtp_weighted_f32(tpo_ctx* ctx, int L1, int L2, const float* w, int w_per_edge, const float* x, const float* y,
+                          float* out, int64_t batch, int64_t channels, int y_shared, void* stream) {
+  return guarded([&] {
+    check_args(ctx, L1, L2, x, y, out, batch, channels);
+    if (batch > 0 && !w) throw InvalidArgument("cgtp_weighted: null weights");
+    ctx->impl.activate();
+    if (batch == 0) return;
+    const int np = num_paths(L1, L2);
+    const int* pof = ctx->impl.int_table("cgtp_path_of_out," + std::to_string(L1) + "," + std::to_string(L2), [&] {
+      std::vector<int> v;  // output column -> path index, the reference's path order (proj/src/cgtp.cpp:152-163)
+      int p = 0;
+      for (int l1 = 0; l1 <= L1; ++l1)
+        for (int l2 = 0; l2 <= L2; ++l2)
+          for (int l3 = std::abs(l1 - l2); l3 <= l1 + l2; ++l3, ++p)
+            for (int m = 0; m < 2 * l3 + 1; ++m) v.push_back(p);
+      return v;
+    });
+    PathWeights pw{w, w_per_edge ? np : 0, pof};
+    run_cgtp(ctx, L1, L2, rows_of(x, y, out, batch, channels, y_shared), static_cast<cudaStream_t>(stream), &pw);
+  });
 }
 
 }  // extern "C"

@@ -72,6 +72,8 @@ class Context {
   const float* degree_weights(const std::vector<double>& w);  // small per-call device array
   // device fp32 copy of a k-major stage operator (stages.cu dense_map), built once per key
   const float* dense_op(const std::string& key, const std::function<std::vector<double>()>& build);
+  // device copy of a small int table, built once per key
+  const int* int_table(const std::string& key, const std::function<std::vector<int>()>& build);
   // Wigner-D recursion tables up to degree L (stages.cu wigner_d)
   const WignerTables& wigner(int L);
 
@@ -117,6 +119,7 @@ class Context {
   std::map<std::array<int, 6>, std::pair<bool, MtpTcTables>> mtp_tc_;
   std::map<std::vector<double>, const float*> weights_;
   std::map<std::string, const float*> dense_ops_;
+  std::map<std::string, const int*> int_tables_;
   std::map<int, WignerTables> wigner_;
   std::array<void*, 12> scratch_{};
   std::array<size_t, 12> scratch_cap_{};

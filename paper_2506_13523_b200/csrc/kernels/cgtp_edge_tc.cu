@@ -155,6 +155,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const float ysc = pow2i(-ey_sh[b]);
       uint8_t* mh = mh_of(b);
       uint8_t* ml = mh + p.dout_pad * kp * 2;
+      const int64_t edge = u / blocks_per_edge;
       for (int o = r; o < p.dout_pad; o += 128) {
         float* row = mrow + o * (kp + 1);  // owned by this thread
         for (int k = 0; k < kp; ++k) row[k] = 0.f;
@@ -162,10 +163,12 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int w = o >> 5, ln = o & 31;
           const int nt = __ldg(t.warp_nt + w);
           const uint2* terms = t.terms + __ldg(t.warp_off + w) + ln;
+          // per-path weight of this output column, folded into M_y (f2)
+          const float yso = p.path_w ? ysc * __ldg(p.path_w + edge * p.w_stride + __ldg(p.path_of_out + o)) : ysc;
           for (int k = 0; k < nt; ++k) {
             const uint2 tw = __ldg(terms + k * 32);
             const int i1 = static_cast<int>(tw.x & 0xFFFFu), i2 = static_cast<int>(tw.x >> 16);
-            row[i1] += __uint_as_float(tw.y) * ysb[i2] * ysc;  // padding terms: coefficient 0
+            row[i1] += __uint_as_float(tw.y) * ysb[i2] * yso;  // padding terms: coefficient 0
           }
         }
         for (int j0 = 0; j0 < kp; j0 += 8) {

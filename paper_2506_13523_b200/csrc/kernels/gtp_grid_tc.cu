@@ -269,7 +269,9 @@ __device__ unsigned long long* g_prof = nullptr;
 // important -- the number of MMA instructions per unit of work.  Rank 0
 // issues every MMA; its commits multicast to both CTAs; the rank-1 MMA warp
 // forwards "my half landed" to rank 0's ring slots; workers signal rank 0.
-template <bool PROF, bool PAIR, int KH = kKHalfStd>
+// SEG: GEMM 2 runs in several accumulation segments (t.seg_chunks < t.nchunks); the single-segment
+// instantiation compiles without the segment hand-offs and the L2 reductions.
+template <bool PROF, bool PAIR, int KH = kKHalfStd, bool SEG = false>
 __global__ void __launch_bounds__(kThreads, 1)
     gtp_grid_tc_kernel(const __grid_constant__ GridTcTables t, const __grid_constant__ RowSpec rs,
                        const __grid_constant__ DegreeWeights dw) {
@@ -294,8 +296,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int i = 0; i < kNumBars; ++i) {
       uint32_t cnt = 1;
       if (i == B_RAW_FREE) cnt = kWorkers;
-      if (i == B_XY_READY) cnt = kWorkers * kPair;
-      if (i == B_Z_EMPTY) cnt = (t.split_roles ? kWorkers / 2 : kWorkers) * kPair;
+      if (i == B_XY_READY || i == B_Z_EMPTY) cnt = kWorkers * kPair;
       if (i >= B_P_READY && i < B_P_READY + kMaxSlices) cnt = BM * kPair;
       mbar_init(&bars[i], cnt);
     }
@@ -530,7 +531,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (c == t.nchunks - 1 && last_of_tile) if (leader_lane) (PAIR ? tc_commit_pair : tc_commit)(&bars[B_XY_FREE]);
           // ---- GEMM 2: Z += P A^T, P (hi/lo fp16) read from TMEM in place of F_x; a new
           // accumulation segment starts a fresh Z once the epilogue has drained the last one
-          const bool seg_start = (c % t.seg_chunks) == 0;
+          const bool seg_start = SEG ? (c % t.seg_chunks) == 0 : c == 0;
           if (seg_start && d > 0) {
             const auto t0 = now();
             wait_leader<PAIR>(&bars[B_Z_EMPTY], static_cast<uint32_t>((d - 1) & 1));
@@ -556,7 +557,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
           if (leader_lane) (PAIR ? tc_commit_pair : tc_commit)(&bars[B_G2_DONE]);
-          if ((c + 1) % t.seg_chunks == 0 || c + 1 == t.nchunks) {
+          if (SEG ? ((c + 1) % t.seg_chunks == 0 || c + 1 == t.nchunks) : c + 1 == t.nchunks) {
             if (leader_lane) (PAIR ? tc_commit_pair : tc_commit)(&bars[B_Z_FULL]);
             ++d;
           }
@@ -654,10 +655,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     int64_t v = 0;  // tile sequence number
     int64_t d = 0;  // Z hand-offs received (one per accumulation segment)
     // ---- epilogue of one accumulation segment: Z -> registers -> rescale -> staging -> coalesced
-    // row-segment stores; segments after the first add their partial sum to the one already
-    // stored (fp32, round to nearest): each lane reads back exactly the elements it wrote, through
-    // cp.async into lane-private shared-memory slots issued before the TMEM read
-    float* stage2 = reinterpret_cast<float*>(smem + t.off_stage) + kWorkerWarps * 32 * kStageStride + (warp - 2) * 512;
+    // row-segment stores; segments after the first add their partial sum to the stored one with
+    // fp32 reductions in L2 (round to nearest; only the lane that stored an element adds to it, in
+    // program order, so the result is deterministic)
     auto drain = [&](const Unit& cu, int buf, bool add, bool final_seg) {
       { const auto t0 = now(); mbar_wait(&bars[B_Z_FULL], static_cast<uint32_t>(d & 1)); pc[12] += now() - t0; }
       ++d;
@@ -675,14 +675,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const bool full = left >= 32;
       const float* sp0 = stage + half_lane * kStageStride + cl;
       float* op0 = rs.out + (row0 + half_lane) * t.dout_total + col0 + cl;
-      const int cb0 = t.split_roles ? 0 : h, cbs = t.split_roles ? 1 : 2;
-      for (int cb = cb0; cb < ((t.dbg & 2) ? 0 : nblk); cb += cbs) {
-        const bool col_ok = col0 + cb * 16 + cl < col_end;
-        float* op = op0 + cb * 16;
-        if (add && col_ok && !t.seg_red) {  // previous segments' sum -> lane-private slots of stage2 (async, no registers)
-          for (int k = 0; k < 16; ++k)
-            if (full || 2 * k < left) cp_async4(stage2 + k * 32 + lane, op + k * stride2);
-        }
+      for (int cb = h; cb < ((t.dbg & 2) ? 0 : nblk); cb += 2) {
         uint32_t v0[16];
         tmem_ld16(lane_base + cb * 16, v0);
         tmem_wait_ld();
@@ -690,26 +683,18 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int qq = 0; qq < 16; ++qq) stage[lane * kStageStride + qq] = __uint_as_float(v0[qq]) * s_lo * s_hi;
         __syncwarp();
         // two rows per store instruction: lanes 0-15 row rr, lanes 16-31 row rr + 1
-        if (col_ok) {
+        if (col0 + cb * 16 + cl < col_end) {
+          float* op = op0 + cb * 16;
           const float* sp = sp0;
           const float wc = dw.on ? wtab_c[col0 + cb * 16 + cl] : 1.f;  // fused output weights (weighted GTP)
-          if (add && t.seg_red) {  // fire-and-forget fp32 reductions in L2 (red.global.add, round to nearest)
-            for (int k = 0; k < 16; ++k, sp += 2 * kStageStride)
-              if (full || 2 * k < left) atomicAdd(op + k * stride2, *sp * wc);
-          } else if (add) {  // out = previous sum + this segment, fp32 round to nearest
-            cp_async_wait_all();
-            if (full) {
-#pragma unroll
-              for (int k = 0; k < 16; ++k, sp += 2 * kStageStride) op[k * stride2] = fmaf(*sp, wc, stage2[k * 32 + lane]);
-            } else {
-              for (int k = 0; k < 16 && 2 * k < left; ++k, sp += 2 * kStageStride)
-                op[k * stride2] = fmaf(*sp, wc, stage2[k * 32 + lane]);
-            }
+          if (SEG && add) {  // later segments: fire-and-forget fp32 reductions in L2 (red.global.add, round to nearest)
+            for (int rr = 0; rr < (full ? 32 : left); rr += 2, op += stride2, sp += 2 * kStageStride)
+              atomicAdd(op, *sp * wc);
           } else if (full) {
 #pragma unroll
-            for (int k = 0; k < 16; ++k, sp += 2 * kStageStride) op[k * stride2] = *sp * wc;
+            for (int rr = 0; rr < 32; rr += 2, op += stride2, sp += 2 * kStageStride) *op = *sp * wc;
           } else {
-            for (int k = 0; k < 16 && 2 * k < left; ++k, sp += 2 * kStageStride) op[k * stride2] = *sp * wc;
+            for (int rr = 0; rr < left; rr += 2, op += stride2, sp += 2 * kStageStride) *op = *sp * wc;
           }
         }
         __syncwarp();
@@ -718,7 +703,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       signal_leader(&bars[B_Z_EMPTY], true);
       pc[13] += now() - te0;
       // degrees past the product band are exactly zero (proj/src/gtp.cpp:237-258)
-      if (final_seg && cu.g == t.ngroups - 1 && t.dout_total > t.dout_eff && h == (t.split_roles ? 1 : 0)) {
+      if (final_seg && cu.g == t.ngroups - 1 && t.dout_total > t.dout_eff && h == 0) {
         for (int rr = 0; rr < 32; ++rr) {
           const int64_t g = row0 + rr;
           if (g >= rs.rows) break;
@@ -726,12 +711,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     };
-    // split_roles: warps 2-5 run every slice's pointwise product, warps 6-9 drain Z (segment sums and
-    // the epilogue), so a drain never delays the next chunk's products; otherwise both halves share
-    // the slices and the column blocks
-    const bool do_products = !t.split_roles || h == 0;
-    const bool do_drains = !t.split_roles || h == 1;
-    const int s0 = t.split_roles ? 0 : h, sstep = t.split_roles ? 1 : 2;
     { const auto t0 = now(); if (u_begin < u_end) convert(u_begin, 0); pc[11] += now() - t0; }
     for (int64_t u = u_begin; u < u_end; ++u, ++i) {
       const Unit cu = unit_of(u, t.ngroups);
@@ -739,40 +718,38 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int buf = static_cast<int>(v & 1);  // ex/ey of this unit's tile
       // ---- pointwise product, chunk by chunk; P overwrites F_x slice by slice
       for (int c = 0; c < t.nchunks; ++c, ++j) {
-        if (do_products) {
-          { const auto t0 = now(); mbar_wait(&bars[B_F_FULL], static_cast<uint32_t>(j & 1)); pc[9] += now() - t0; }
-          tc_fence_after();
-          const auto tp0 = now();
-          for (int s = s0; s < t.nslices; s += sstep) {
-            if (t.dbg & 1) {
-              signal_leader(&bars[B_P_READY + s], true);
-              continue;
-            }
-            uint32_t vx[16], vy[16];
-            tmem_ld16(lane_base + fx + 16 * s, vx);
-            tmem_ld16(lane_base + fy + 16 * s, vy);
-            tmem_wait_ld();
-            uint32_t hw[8], lw[8];
-#pragma unroll
-            for (int qq = 0; qq < 8; ++qq) {
-              const float a0 = __uint_as_float(vx[2 * qq]) * __uint_as_float(vy[2 * qq]);
-              const float a1 = __uint_as_float(vx[2 * qq + 1]) * __uint_as_float(vy[2 * qq + 1]);
-              const __half2 hh = __floats2half2_rn(a0, a1);
-              const float2 hf = __half22float2(hh);
-              hw[qq] = *reinterpret_cast<const uint32_t*>(&hh);
-              lw[qq] = pack_half2(a0 - hf.x, a1 - hf.y);
-            }
-            tmem_st8(lane_base + fx + 16 * s, hw);
-            tmem_st8(lane_base + fx + 16 * s + 8, lw);
-            tmem_wait_st();
-            tc_fence_before();
+        { const auto t0 = now(); mbar_wait(&bars[B_F_FULL], static_cast<uint32_t>(j & 1)); pc[9] += now() - t0; }
+        tc_fence_after();
+        const auto tp0 = now();
+        for (int s = h; s < t.nslices; s += 2) {
+          if (t.dbg & 1) {
             signal_leader(&bars[B_P_READY + s], true);
+            continue;
           }
-          pc[10] += now() - tp0;
+          uint32_t vx[16], vy[16];
+          tmem_ld16(lane_base + fx + 16 * s, vx);
+          tmem_ld16(lane_base + fy + 16 * s, vy);
+          tmem_wait_ld();
+          uint32_t hw[8], lw[8];
+#pragma unroll
+          for (int qq = 0; qq < 8; ++qq) {
+            const float a0 = __uint_as_float(vx[2 * qq]) * __uint_as_float(vy[2 * qq]);
+            const float a1 = __uint_as_float(vx[2 * qq + 1]) * __uint_as_float(vy[2 * qq + 1]);
+            const __half2 hh = __floats2half2_rn(a0, a1);
+            const float2 hf = __half22float2(hh);
+            hw[qq] = *reinterpret_cast<const uint32_t*>(&hh);
+            lw[qq] = pack_half2(a0 - hf.x, a1 - hf.y);
+          }
+          tmem_st8(lane_base + fx + 16 * s, hw);
+          tmem_st8(lane_base + fx + 16 * s + 8, lw);
+          tmem_wait_st();
+          tc_fence_before();
+          signal_leader(&bars[B_P_READY + s], true);
         }
+        pc[10] += now() - tp0;
         // ---- an accumulation segment ends before the unit's last chunk: drain its partial sum
         // (overlaps the next chunk's GEMM 1)
-        if (do_drains && (c + 1) % t.seg_chunks == 0 && c + 1 < t.nchunks) drain(cu, buf, c + 1 > t.seg_chunks, false);
+        if (SEG && (c + 1) % t.seg_chunks == 0 && c + 1 < t.nchunks) drain(cu, buf, c + 1 > t.seg_chunks, false);
       }
       // ---- next unit's inputs (overlaps this unit's last GEMM 2)
       if (last_of_tile && u + 1 < u_end) {
@@ -780,7 +757,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         convert(u + 1, v + 1);
         pc[11] += now() - t0;
       }
-      if (do_drains) drain(cu, buf, t.nchunks > t.seg_chunks, true);
+      drain(cu, buf, SEG && t.nchunks > t.seg_chunks, true);
       if (last_of_tile) ++v;
     }
     pc[8] = now() - t_start;
@@ -815,15 +792,19 @@ cudaError_t launch_gtp_grid_tc(const GridTcTables& t, const RowSpec& rs, int num
   DegreeWeights dw{};
   if (w) dw = *w;
   if (rs.rows <= 0) return cudaSuccess;
-  static const bool prof = [] {
+  static const bool prof_env = [] {
     const char* v = std::getenv("TPO_GRID_PROF");
     return v && *v == '1';
   }();
+  const bool prof = prof_env && t.seg_chunks >= t.nchunks;
   // K > 128 (L = 11, 12): a separate instantiation with the wider register conversion, so the
   // default one keeps its register budget (the wide one spills ~100 B in cold code)
   const bool big = t.k1p > 2 * kKHalfStd || t.k2p > 2 * kKHalfStd;
   if (big && t.pair) return cudaErrorInvalidValue;  // planner never pairs K > 128
-  auto kern = big ? gtp_grid_tc_kernel<false, false, kKHalfMax>
+  const bool seg = t.seg_chunks < t.nchunks;
+  if (seg && t.pair) return cudaErrorInvalidValue;  // the planner never pairs segmented shapes
+  auto kern = big ? (seg ? gtp_grid_tc_kernel<false, false, kKHalfMax, true> : gtp_grid_tc_kernel<false, false, kKHalfMax>)
+              : seg ? gtp_grid_tc_kernel<false, false, kKHalfStd, true>  // (no cycle accounting variant)
               : t.pair ? (prof ? gtp_grid_tc_kernel<true, true> : gtp_grid_tc_kernel<false, true>)
                        : (prof ? gtp_grid_tc_kernel<true, false> : gtp_grid_tc_kernel<false, false>);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, t.smem_bytes);

@@ -71,6 +71,12 @@ struct EdgeTcParams {
   int kp;        // Din1 padded to 16 (<= 64)
   int dout_pad;  // Dout padded to 16 (<= 256: two TMEM accumulators)
   int tmem_cols;
+  // optional per-path weights (MACE "uvu"): output o of edge e is scaled by
+  // path_w[e * w_stride + path_of_out[o]] (w_stride 0: one weight vector for every edge); folded
+  // into the edge's M_y columns, so the weighted product costs nothing extra
+  const float* path_w;
+  int64_t w_stride;
+  const int* path_of_out;
   alignas(64) CUtensorMap tm_out;
 };
 int cgtp_edge_tc_smem(const CgtpTables& t, int kp, int dout_pad);
@@ -124,8 +130,6 @@ struct GridTcTables {
                              // truncates (round toward zero) once per MMA, so the error grows with the
                              // number of MMAs into one accumulator; each segment starts a fresh Z and its
                              // partial sum is added in fp32 (round to nearest) into the output row
-  int seg_red;               // segment sums: 1 fp32 reductions in L2 (red.add), 0 read back through cp.async
-  int split_roles;           // warps 2-5 products, warps 6-9 drains (else both halves share both)
   int pair;                  // CTA pairs, tcgen05 cta_group::2 (M = 256); slices stored as two row halves
   int dbg;                   // timing experiments only (results invalid): 1 no product, 2 no epilogue, 4 no convert
   int smem_bytes;
@@ -184,6 +188,7 @@ cudaError_t launch_gtp_fourier(const FourierDevTables& t, const RowSpec& rs, int
 // ---------------------------------------------------------------- MTP
 struct MtpDevTables {
   int lt, dt, din1, din2, dout_total, dout_eff;
+  int dtp;  // dt rounded up to 4: the kernel's padded carrier pitch
   // embed: per carrier cell (m1,m2) a CSR list of (input idx, coef)
   const int* emb1_off;  // [dt*dt + 1]
   const int* emb1_idx;
@@ -191,7 +196,7 @@ struct MtpDevTables {
   const int* emb2_off;
   const int* emb2_idx;
   const float* emb2_c;
-  // extract: per output coefficient a CSR list of (cell idx, coef)
+  // extract: per output coefficient a CSR list of (padded cell a * dtp + b, coef)
   const int* ext_off;   // [dout_eff + 1]
   const int* ext_idx;
   const float* ext_c;
@@ -229,6 +234,11 @@ cudaError_t launch_accumulate(const float* in, float* out, int64_t n, cudaStream
 // dst[r][k] = src[r * stride + col0 + k], k < w (backward: a window of grad_out columns, packed)
 cudaError_t launch_gather_cols(const float* src, int64_t stride, int col0, int w, float* dst, int64_t rows,
                                cudaStream_t s);
+
+// ---------------------------------------------------------------- per-path weights (stages.cu)
+// out[row][o] *= w[(row / channels) * w_stride + path_of_out[o]]
+cudaError_t launch_path_scale(float* out, int64_t rows, int64_t channels, int dout, const int* path_of_out,
+                              const float* w, int64_t w_stride, int num_sms, cudaStream_t s);
 
 // ---------------------------------------------------------------- stage operators (stages.cu)
 // out[b][o] = sum_k mt[k][o] in[b][k]  (mt k-major [din][dout], fp32)

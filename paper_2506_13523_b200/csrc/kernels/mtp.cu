@@ -1,181 +1,170 @@
-// Matrix tensor product (SIMT, batched small matrices).
+// Matrix tensor product (SIMT, batched small matrices) -- the path for carriers the tcgen05 kernel
+// does not hold (dt = 2 lt + 1 > 13, i.e. L >= 7 at L3 = 2L, and any l_tilde override past that).
 //
-// Reference: tpo::mtp with MtpImpl::sparse (proj/src/mtp.cpp:99-117):
-// embed both inputs into (2lt+1)^2 carrier matrices through the real CG
-// tables (proj/src/mtp.cpp:20-58), classical cubic matmul Z = X Y
-// (:119-133, sub-cubic forbidden by the cost model), extract every output
-// degree by the adjoint CG contraction (:60-97).
+// Reference: tpo::mtp with MtpImpl::sparse (proj/src/mtp.cpp:99-117): embed both inputs into
+// (2lt+1)^2 carrier matrices through the real CG tables (proj/src/mtp.cpp:20-58), classical cubic
+// matmul Z = X Y (:119-133, sub-cubic forbidden by the cost model), extract every output degree by
+// the adjoint CG contraction (:60-97).
 //
-// A block owns a tile of R products with all intermediates in shared memory
-// (odd row pitches, so column-wise reads are bank-conflict free).  The embed
-// and extract maps are CSR gather lists over the CG nonzeros (host/context.cpp);
-// each list entry is fetched once per tile and applied to all R products from
-// registers.  The R x dt matmul row tasks keep one output row of Z in
-// registers and stream X / Y from shared memory.
+// A block of 512 threads owns a tile of R products (R = 4..32, a multiple of 4) with every
+// intermediate in shared memory, stored product-minor: element e of product r at [e][r].  One
+// 128-bit shared load then feeds the same term to 4 products:
+//   embed    item = (carrier cell, 4 products): per CSR term one coefficient fetch, one LDS.128,
+//            four FMAs (host/context.cpp builds the per-cell lists over the CG nonzeros)
+//   matmul   item = (4 x 4 block of Z, 4 products): per k, 8 LDS.128 and 64 FMAs; carriers are
+//            padded to dtp = dt rounded up to 4 with zero rows / columns, so blocks need no guards;
+//            Z overwrites X once every block has its sums in registers
+//   extract  item = (output coefficient, 4 products): per CSR term one LDS.128, four FMAs;
+//            outputs past the carrier band are exactly zero
 #include <algorithm>
-#include <cstdlib>
 
 #include "kernels.hpp"
 
 namespace tpo_b200 {
 namespace {
 
-constexpr int kThreads = 256;
-constexpr int kMaxDt = 33;  // lt <= 16
+constexpr int kThreads = 512;
 
-template <int R, int ZR>
-__global__ void __launch_bounds__(kThreads)
+template <int R>
+__global__ void __launch_bounds__(kThreads, 1)
     mtp_kernel(const __grid_constant__ MtpDevTables t, const __grid_constant__ RowSpec rs) {
-  extern __shared__ float sm[];
-  const int dt = t.dt, dt2 = dt * dt;
-  const int px = t.din1 | 1, py = t.din2 | 1, pc = dt2 | 1;
-  float* xs = sm;             // [R][px]
-  float* ys = xs + R * px;    // [R][py]
-  float* X = ys + R * py;     // [R][pc]
-  float* Y = X + R * pc;      // [R][pc]
-  float* Z = Y + R * pc;      // [R][pc]
+  extern __shared__ float4 sm4[];
+  constexpr int G = R / 4;  // float4 groups per element
+  const int dt = t.dt, dtp = t.dtp, dt2 = dt * dt, cells = dtp * dtp;
+  float4* xs = sm4;                 // [din1][G]
+  float4* ys = xs + t.din1 * G;     // [din2][G]
+  float4* X = ys + t.din2 * G;      // [dtp * dtp][G], i * dtp + k; Z after the matmul
+  float4* Y = X + cells * G;        // [dtp * dtp][G], k * dtp + j
   const int tid = threadIdx.x;
+  for (int i = tid; i < 2 * cells * G; i += kThreads) X[i] = make_float4(0.f, 0.f, 0.f, 0.f);  // padding stays 0
+  const int nb = dtp / 4;
   const int64_t ntiles = (rs.rows + R - 1) / R;
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int64_t row0 = tile * R;
-    const int64_t left = rs.rows - row0;
-    const int nr = left < R ? static_cast<int>(left) : R;
-    __syncthreads();
-    for (int i = tid; i < R * t.din1; i += kThreads) {
-      const int r = i / t.din1, k = i - r * t.din1;
-      xs[r * px + k] = r < nr ? __ldg(rs.x + row0 * t.din1 + i) : 0.f;
+    const int nr = static_cast<int>(rs.rows - row0 < R ? rs.rows - row0 : R);
+    __syncthreads();  // previous tile's extract has read Z
+    {  // stage inputs product-minor (coalesced global reads)
+      float* xf = reinterpret_cast<float*>(xs);
+      float* yf = reinterpret_cast<float*>(ys);
+      for (int i = tid; i < R * t.din1; i += kThreads) {
+        const int r = i / t.din1, k = i - r * t.din1;
+        xf[k * R + r] = r < nr ? __ldg(rs.x + row0 * t.din1 + i) : 0.f;
+      }
+      for (int i = tid; i < R * t.din2; i += kThreads) {
+        const int r = i / t.din2, k = i - r * t.din2;
+        const int64_t gr = row0 + r;
+        const int64_t yr = rs.y_shared ? gr / rs.channels : gr;
+        yf[k * R + r] = r < nr ? __ldg(rs.y + yr * t.din2 + k) : 0.f;
+      }
     }
-    for (int i = tid; i < R * t.din2; i += kThreads) {
-      const int r = i / t.din2, k = i - r * t.din2;
-      const int64_t g = row0 + r;
-      const int64_t yr = rs.y_shared ? g / rs.channels : g;
-      ys[r * py + k] = r < nr ? __ldg(rs.y + yr * t.din2 + k) : 0.f;
-    }
     __syncthreads();
-    // ---- embed (proj/src/mtp.cpp:20-58): X[cell] = sum_e c_e x[idx_e]
-    for (int cell = tid; cell < 2 * dt2; cell += kThreads) {
-      const bool second = cell >= dt2;
-      const int cl = second ? cell - dt2 : cell;
+    // ---- embed (proj/src/mtp.cpp:20-58): X[a][b] = sum_e c_e x[idx_e], Y likewise
+    for (int item = tid; item < 2 * dt2 * G; item += kThreads) {
+      const bool second = item >= dt2 * G;
+      const int it = second ? item - dt2 * G : item;
+      const int cell = it / G, g = it - cell * G;
       const int* off = second ? t.emb2_off : t.emb1_off;
       const int* idx = second ? t.emb2_idx : t.emb1_idx;
       const float* cf = second ? t.emb2_c : t.emb1_c;
-      const float* src = second ? ys : xs;
-      const int pitch = second ? py : px;
-      float acc[R];
-#pragma unroll
-      for (int r = 0; r < R; ++r) acc[r] = 0.f;
-      for (int e = __ldg(off + cl), e1 = __ldg(off + cl + 1); e < e1; ++e) {
+      const float4* src = second ? ys : xs;
+      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int e = __ldg(off + cell), e1 = __ldg(off + cell + 1); e < e1; ++e) {
         const float c = __ldg(cf + e);
-        const int k = __ldg(idx + e);
-#pragma unroll
-        for (int r = 0; r < R; ++r) acc[r] = fmaf(c, src[r * pitch + k], acc[r]);
+        const float4 v = src[__ldg(idx + e) * G + g];
+        acc.x = fmaf(c, v.x, acc.x);
+        acc.y = fmaf(c, v.y, acc.y);
+        acc.z = fmaf(c, v.z, acc.z);
+        acc.w = fmaf(c, v.w, acc.w);
       }
-      float* dst = (second ? Y : X) + cl;
-#pragma unroll
-      for (int r = 0; r < R; ++r) dst[r * pc] = acc[r];
+      const int a = cell / dt, b = cell - a * dt;
+      (second ? Y : X)[(a * dtp + b) * G + g] = acc;
     }
     __syncthreads();
-    // ---- Z = X Y, classical cubic (proj/src/mtp.cpp:119-133): task = (row r, Z rows i0 .. i0+ZR-1);
-    // every Y element loaded from shared memory feeds ZR rows
-    const int ntr = (dt + ZR - 1) / ZR;
-    for (int task = tid; task < R * ntr; task += kThreads) {
-      const int r = task / ntr, i0 = (task - r * ntr) * ZR;
-      const float* xr = X + r * pc + i0 * dt;
-      const float* yb = Y + r * pc;
-      float acc[ZR][kMaxDt];
+    // ---- Z = X Y, classical cubic (proj/src/mtp.cpp:119-133): one 4 x 4 block of 4 products per thread
+    const int ntask = nb * nb * G;
+    const bool has = tid < ntask;
+    const int g = tid % G, blk = tid / G, i0 = (blk / nb) * 4, j0 = (blk % nb) * 4;
+    float4 acc[4][4];
 #pragma unroll
-      for (int q = 0; q < ZR; ++q)
+    for (int q = 0; q < 4; ++q)
 #pragma unroll
-        for (int j = 0; j < kMaxDt; ++j) acc[q][j] = 0.f;
+      for (int p = 0; p < 4; ++p) acc[q][p] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (has) {
       for (int k = 0; k < dt; ++k) {
-        float a[ZR];
+        float4 a[4], b[4];
 #pragma unroll
-        for (int q = 0; q < ZR; ++q) a[q] = i0 + q < dt ? xr[q * dt + k] : 0.f;
-        const float* yk = yb + k * dt;
-        // 8-wide blocks guarded as a whole: no issue slots spent past dt
+        for (int q = 0; q < 4; ++q) a[q] = X[((i0 + q) * dtp + k) * G + g];
 #pragma unroll
-        for (int j0 = 0; j0 < kMaxDt; j0 += 8) {
-          if (j0 < dt) {
+        for (int p = 0; p < 4; ++p) b[p] = Y[(k * dtp + j0 + p) * G + g];
 #pragma unroll
-            for (int jj = 0; jj < 8; ++jj)
-              if (j0 + jj < kMaxDt && j0 + jj < dt) {
-                const float yv = yk[j0 + jj];
+        for (int q = 0; q < 4; ++q)
 #pragma unroll
-                for (int q = 0; q < ZR; ++q) acc[q][j0 + jj] = fmaf(a[q], yv, acc[q][j0 + jj]);
-              }
+          for (int p = 0; p < 4; ++p) {
+            acc[q][p].x = fmaf(a[q].x, b[p].x, acc[q][p].x);
+            acc[q][p].y = fmaf(a[q].y, b[p].y, acc[q][p].y);
+            acc[q][p].z = fmaf(a[q].z, b[p].z, acc[q][p].z);
+            acc[q][p].w = fmaf(a[q].w, b[p].w, acc[q][p].w);
           }
-        }
-      }
-#pragma unroll
-      for (int q = 0; q < ZR; ++q) {
-        if (i0 + q >= dt) break;
-        float* zr = Z + r * pc + (i0 + q) * dt;
-#pragma unroll
-        for (int j = 0; j < kMaxDt; ++j)
-          if (j < dt) zr[j] = acc[q][j];
       }
     }
+    __syncthreads();  // every block read X: Z may overwrite it
+    if (has)
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int p = 0; p < 4; ++p) X[((i0 + q) * dtp + j0 + p) * G + g] = acc[q][p];
     __syncthreads();
     // ---- extract (proj/src/mtp.cpp:60-97): out[o] = sum_e c_e Z[cell_e]; zero past the carrier band
-    for (int o = tid; o < t.dout_total; o += kThreads) {
-      float acc[R];
-#pragma unroll
-      for (int r = 0; r < R; ++r) acc[r] = 0.f;
-      if (o < t.dout_eff) {
+    for (int item = tid; item < t.dout_total * G; item += kThreads) {
+      const int o = item / G, gg = item - o * G;
+      float4 acc4 = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (o < t.dout_eff)
         for (int e = __ldg(t.ext_off + o), e1 = __ldg(t.ext_off + o + 1); e < e1; ++e) {
           const float c = __ldg(t.ext_c + e);
-          const int cell = __ldg(t.ext_idx + e);
-#pragma unroll
-          for (int r = 0; r < R; ++r) acc[r] = fmaf(c, Z[r * pc + cell], acc[r]);
+          const float4 z = X[__ldg(t.ext_idx + e) * G + gg];
+          acc4.x = fmaf(c, z.x, acc4.x);
+          acc4.y = fmaf(c, z.y, acc4.y);
+          acc4.z = fmaf(c, z.z, acc4.z);
+          acc4.w = fmaf(c, z.w, acc4.w);
         }
-      }
-      float* op = rs.out + row0 * t.dout_total + o;
-#pragma unroll
-      for (int r = 0; r < R; ++r)
-        if (r < nr) op[static_cast<int64_t>(r) * t.dout_total] = acc[r];
+      const int r = 4 * gg;
+      float* op = rs.out + (row0 + r) * t.dout_total + o;
+      if (r < nr) op[0] = acc4.x;
+      if (r + 1 < nr) op[t.dout_total] = acc4.y;
+      if (r + 2 < nr) op[2 * static_cast<int64_t>(t.dout_total)] = acc4.z;
+      if (r + 3 < nr) op[3 * static_cast<int64_t>(t.dout_total)] = acc4.w;
     }
   }
 }
 
-template <int R, int ZR>
-cudaError_t launch_rz(const MtpDevTables& t, const RowSpec& rs, int num_sms, cudaStream_t s) {
-  const int dt2 = t.dt * t.dt;
-  const size_t smem = sizeof(float) * R * ((t.din1 | 1) + (t.din2 | 1) + 3 * (dt2 | 1));
-  cudaError_t e = cudaFuncSetAttribute(mtp_kernel<R, ZR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(smem));
-  if (e != cudaSuccess) return e;
-  int occ = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, mtp_kernel<R, ZR>, kThreads, smem);
-  const int64_t ntiles = (rs.rows + R - 1) / R;
-  const int grid = static_cast<int>(std::min<int64_t>(ntiles, static_cast<int64_t>(num_sms) * std::max(occ, 1)));
-  mtp_kernel<R, ZR><<<grid, kThreads, smem, s>>>(t, rs);
-  return cudaGetLastError();
+template <int R>
+size_t smem_for(const MtpDevTables& t) {
+  return sizeof(float) * R * (t.din1 + t.din2 + 2 * t.dtp * t.dtp);
 }
 
-// Z rows per matmul task: 2 measured fastest at every dt (fewer shared loads per FMA beats the
-// lost task parallelism; tools/mtp_simt_timing.py); TPO_MTP_ZR=1|3 for experiments
 template <int R>
 cudaError_t launch_r(const MtpDevTables& t, const RowSpec& rs, int num_sms, cudaStream_t s) {
-  static const int zr = [] {
-    const char* v = std::getenv("TPO_MTP_ZR");
-    return v ? std::atoi(v) : 2;
-  }();
-  if (zr == 1) return launch_rz<R, 1>(t, rs, num_sms, s);
-  if (zr == 3) return launch_rz<R, 3>(t, rs, num_sms, s);
-  return launch_rz<R, 2>(t, rs, num_sms, s);
+  const size_t smem = smem_for<R>(t);
+  cudaError_t e = cudaFuncSetAttribute(mtp_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  const int64_t ntiles = (rs.rows + R - 1) / R;
+  const int grid = static_cast<int>(std::min<int64_t>(ntiles, num_sms));
+  mtp_kernel<R><<<grid, kThreads, smem, s>>>(t, rs);
+  return cudaGetLastError();
 }
 
 }  // namespace
 
 cudaError_t launch_mtp(const MtpDevTables& t, const RowSpec& rs, int num_sms, cudaStream_t s) {
   if (rs.rows <= 0) return cudaSuccess;
-  if (t.dt > kMaxDt) return cudaErrorInvalidValue;
-  // rows per tile: as many as keep >= 2 blocks per SM within 227 KB
-  const int per_row = ((t.din1 | 1) + (t.din2 | 1) + 3 * ((t.dt * t.dt) | 1)) * 4;
-  if (per_row * 32 <= 110 * 1024) return launch_r<32>(t, rs, num_sms, s);
-  if (per_row * 16 <= 110 * 1024) return launch_r<16>(t, rs, num_sms, s);
-  if (per_row * 8 <= 220 * 1024) return launch_r<8>(t, rs, num_sms, s);
-  return launch_r<4>(t, rs, num_sms, s);
+  // the largest tile whose intermediates fit in shared memory and whose matmul blocks fit the block
+  const int nb = t.dtp / 4;
+  auto fits = [&](size_t smem, int R) { return smem <= 220u * 1024u && nb * nb * (R / 4) <= kThreads; };
+  if (fits(smem_for<32>(t), 32)) return launch_r<32>(t, rs, num_sms, s);
+  if (fits(smem_for<16>(t), 16)) return launch_r<16>(t, rs, num_sms, s);
+  if (fits(smem_for<8>(t), 8)) return launch_r<8>(t, rs, num_sms, s);
+  if (fits(smem_for<4>(t), 4)) return launch_r<4>(t, rs, num_sms, s);
+  return cudaErrorInvalidValue;
 }
 
 }  // namespace tpo_b200

@@ -165,12 +165,31 @@ __global__ void rotate_kernel(const double* __restrict__ D, int64_t d_stride, in
   }
 }
 
+__global__ void path_scale_kernel(float* __restrict__ out, int64_t rows, int64_t channels, int dout,
+                                  const int* __restrict__ path_of_out, const float* __restrict__ w, int64_t w_stride) {
+  const int64_t total = rows * dout;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t row = i / dout;
+    const int o = static_cast<int>(i - row * dout);
+    out[i] *= __ldg(w + (row / channels) * w_stride + __ldg(path_of_out + o));
+  }
+}
+
 int grid_for(int64_t work, int per_block, int num_sms) {
   const int64_t b = (work + per_block - 1) / per_block;
   return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(b, static_cast<int64_t>(num_sms) * 8)));
 }
 
 }  // namespace
+
+cudaError_t launch_path_scale(float* out, int64_t rows, int64_t channels, int dout, const int* path_of_out,
+                              const float* w, int64_t w_stride, int num_sms, cudaStream_t s) {
+  if (rows <= 0 || dout <= 0) return cudaSuccess;
+  path_scale_kernel<<<grid_for(rows * dout, 256 * 4, num_sms), 256, 0, s>>>(out, rows, channels, dout, path_of_out, w,
+                                                                            w_stride);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_dense_map(const float* in, int din, const float* mt, int dout, float* out, int64_t rows,
                              cudaStream_t s) {

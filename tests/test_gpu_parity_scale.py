@@ -108,7 +108,21 @@ def test_gtp_bench_config_exact(tpo, orc):
     assert max(worst.values()) <= TOL, worst
 
 
-@pytest.mark.parametrize("L", [1, 3, 6])
+@pytest.mark.parametrize("L", [15, 16])
+def test_fourier_degree_groups_high_L(tpo, orc, L):
+    # L = 15, 16 Fourier GTP on tcgen05 degree groups (the SIMT path is 2.5-3x slower there)
+    err, used = _run_big(tpo, orc, "gtp_fourier", L, 148 * 128 // 4 + 77, 9300 + L)
+    assert used == "tcgen05"
+    assert err <= TOL, (L, err)
+
+
+def test_cgtp_blocks_L15(tpo, orc):
+    # CGTP block GEMMs at L = 15 (several tiles per CTA, ragged tail)
+    err, _ = _run_big(tpo, orc, "cgtp", 15, 128 * 3 + 5, 9415)
+    assert err <= TOL, err
+
+
+@pytest.mark.parametrize("L", [1, 3, 6, 7, 10])
 def test_mtp_bench_scale(tpo, orc, L):
     err, _ = _run_big(tpo, orc, "mtp", L, BIG, 9400 + L)
     assert err <= TOL, (L, err)
@@ -171,7 +185,7 @@ _TABLE = {}
 
 
 @pytest.mark.parametrize("kind", ["gtp_grid", "gtp_fourier", "mtp", "cgtp"])
-@pytest.mark.parametrize("L", list(range(1, 15)))
+@pytest.mark.parametrize("L", list(range(1, 17)))
 def test_adversarial_precision(tpo, orc, kind, L):
     import torch
 

@@ -236,3 +236,27 @@ def test_equivariance_large_batch(tpo):
     out_dir = Path(__file__).resolve().parents[1] / "gpurun_out"
     if out_dir.exists():
         (out_dir / "equivariance_large.json").write_text(json.dumps(rep, indent=1))
+
+
+@pytest.mark.parametrize("L,C,shared,per_edge", [(3, 128, True, True), (3, 128, True, False), (2, 24, True, True),
+                                                 (5, None, False, True), (2, 7, False, False)])
+def test_cgtp_per_path_weights(tpo, orc, L, C, shared, per_edge):
+    # f2: path p of edge b scaled by w[b, p]; reference = oracle CGTP with each path block scaled
+    import torch
+
+    rng = np.random.default_rng(L + (C or 0))
+    B = 9
+    d = (L + 1) ** 2
+    x = rng.standard_normal((B, C, d) if C else (B, d)).astype(np.float32)
+    y = rng.standard_normal((B, d) if (shared or not C) else (B, C, d)).astype(np.float32)
+    npth = tpo.cgtp_num_paths(L, L)
+    w = rng.standard_normal((B, npth) if per_edge else (npth,)).astype(np.float32)
+    out = tpo.cgtp_weighted(torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda(), torch.from_numpy(w).cuda(), L, L)
+    out = out.cpu().numpy().reshape(B, C or 1, -1)
+    ref = orc.batch_mimo("cgtp", L, x.astype(np.float64).reshape(B, C or 1, d),
+                         y.astype(np.float64) if shared else y.astype(np.float64).reshape(B, C or 1, d),
+                         channels=C or 1, y_shared=bool(shared and C))
+    pcol = np.concatenate([np.full(2 * l3 + 1, p) for p, (l1, l2, l3) in enumerate(
+        [(a, b, c) for a in range(L + 1) for b in range(L + 1) for c in range(abs(a - b), a + b + 1)])])
+    wb = (w[:, None, pcol] if per_edge else w[None, None, pcol]).astype(np.float64)
+    assert _rel(out, ref * wb) <= TOL

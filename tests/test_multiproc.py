@@ -71,3 +71,34 @@ def test_gloo_world2_shard_and_gather(orc):
     assert err == 0.0
     assert tmax == 2.0
     assert len(cks) == 2 and cks[0][1] + cks[1][1] == 37
+
+
+@pytest.mark.parametrize("workload", ["c4", "c5", "c2"])
+def test_bench_plan_world2_gloo(workload):
+    """bench.py under torchrun with 2 ranks (gloo, CPU): the per-rank plan of the multi-GPU run.  c4
+    strong-scales 2^20 edges (each rank owns half, 128 channels per edge); c2/c5 are weak-scaled
+    (every rank owns its own shard).  The rank-0 line carries every rank's share, gathered over
+    the process group."""
+    import json
+    import socket
+    import subprocess
+    import sys
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr=127.0.0.1", f"--master-port={port}", str(ROOT / "bench.py"), "--gpus", "2",
+           "--workload", workload, "--plan-only"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=300, cwd=str(ROOT))
+    assert r.returncode == 0, r.stderr[-3000:]
+    line = json.loads([x for x in r.stdout.splitlines() if x.startswith("{")][-1])
+    assert line["n_gpus"] == 2 and len(line["per_rank_products"]) == 2
+    if workload == "c4":
+        assert line["per_rank_products"] == [(1 << 19) * 128, (1 << 19) * 128]
+        assert line["per_rank_bytes"][0] == (1 << 19) * 139328
+        assert "strong" in line["config"]["parallelism"]
+    elif workload == "c5":
+        assert line["per_rank_products"] == [4 * 16 * (1 << 19)] * 2
+    else:
+        assert line["per_rank_products"] == [10 * 65536] * 2
