@@ -220,6 +220,12 @@ int64_t tpo_count_muls(int kind, int impl, int mode, int L);
  * (separable grid GTP; direct half-plane spectral convolution for the
  * Fourier GTP).  Returns the previous setting. */
 int tpo_set_gtp_grid_path(tpo_ctx* ctx, int path);
+/* Accumulation precision of the tcgen05 Gaunt products (grid / Fourier).  The tensor pipe rounds
+ * its fp32 accumulator toward zero once per MMA, so long accumulation chains are cut into segments
+ * summed in fp32.  0 (default): segments past the per-operator limits, normwise
+ * error <= 6.8e-6 on adversarial rows at every L; 1 (strict): segments past 20 K-steps for every
+ * shape, <= ~4e-6, about 25% slower at L = 8..10.  Returns the previous mode. */
+int tpo_set_precision(tpo_ctx* ctx, int mode);
 /* Which kernel the last GTP-grid / GTP-Fourier call used (1 tc, 2 simt). */
 int tpo_last_gtp_grid_path(const tpo_ctx* ctx);
 

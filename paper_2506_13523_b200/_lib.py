@@ -90,6 +90,7 @@ def lib():
             "tpo_mtp_path_weight": (d, [i, i, i, i]),
             "tpo_count_muls": (i64, [i, i, i, i]),
             "tpo_cgtp_num_paths": (i, [i, i]),
+            "tpo_set_precision": (i, [p, i]),
             "tpo_cgtp_weighted_f32": (i, [p, i, i, p, i, p, p, p, i64, i64, i, p]),
         }
         for name, (res, args) in sig.items():
@@ -111,7 +112,7 @@ EXPORTED = [
     "tpo_to_sphere_f32", "tpo_from_sphere_f32", "tpo_pointwise_mul_f32", "tpo_mtp_embed_f32", "tpo_mtp_matmul_f32",
     "tpo_mtp_extract_f32", "tpo_apply_linear_f32", "tpo_wigner_d_f64", "tpo_wigner_d_size", "tpo_rotate_f32",
     "tpo_gaunt_real", "tpo_s2_grid", "tpo_legendre_lambda", "tpo_mtp_path_weight", "tpo_count_muls",
-    "tpo_cgtp_num_paths", "tpo_cgtp_weighted_f32",
+    "tpo_cgtp_num_paths", "tpo_cgtp_weighted_f32", "tpo_set_precision",
 ]
 
 
@@ -157,6 +158,15 @@ class Context:
         r = lib().tpo_set_gtp_grid_path(self.handle, code)
         if r < 0:
             check(-r)
+
+    def set_precision(self, mode: str) -> str:
+        """"default" or "strict" accumulation segmentation of the tcgen05 Gaunt products
+        (tpo_set_precision); returns the previous mode."""
+        code = {"default": 0, "strict": 1}[mode]
+        r = lib().tpo_set_precision(self.handle, code)
+        if r < 0:
+            check(-r)
+        return {0: "default", 1: "strict"}[r]
 
     @property
     def last_grid_path(self) -> str:

@@ -1167,3 +1167,8 @@ int tpo_cgtp_weighted_f32(tpo_ctx* ctx, int L1, int L2, const float* w, int w_pe
 }
 
 }  // extern "C"
+
+extern "C" int tpo_set_precision(tpo_ctx* ctx, int mode) {
+  if (!ctx || mode < 0 || mode > 1) return -TPO_EINVAL;
+  return ctx->impl.precision_mode.exchange(mode);
+}

@@ -629,9 +629,12 @@ DenseOps make_grid_ops(int L1, int L2, int L3) {
 
 const GridTcEntry& Context::grid_tc(int L1, int L2, int L3) {
   std::lock_guard<std::mutex> g(mu_);
-  auto it = grid_tc_.find({L1, L2, L3});
+  const int strict = precision_mode.load();
+  auto it = grid_tc_.find({L1, L2, L3, strict});
   if (it != grid_tc_.end()) return it->second;
-  return grid_tc_.emplace(std::array<int, 3>{L1, L2, L3}, build_dense_tc(make_grid_ops(L1, L2, L3), "gtp_grid", 60)).first->second;
+  return grid_tc_.emplace(std::array<int, 4>{L1, L2, L3, strict},
+                          build_dense_tc(make_grid_ops(L1, L2, L3), "gtp_grid", strict ? 20 : 60))
+      .first->second;
 }
 
 namespace {
@@ -767,9 +770,12 @@ DenseOps make_fourier_ops(int L1, int L2, int L3) {
 
 const GridTcEntry& Context::fourier_tc(int L1, int L2, int L3) {
   std::lock_guard<std::mutex> g(mu_);
-  auto it = fourier_tc_.find({L1, L2, L3});
+  const int strict = precision_mode.load();
+  auto it = fourier_tc_.find({L1, L2, L3, strict});
   if (it != fourier_tc_.end()) return it->second;
-  return fourier_tc_.emplace(std::array<int, 3>{L1, L2, L3}, build_dense_tc(make_fourier_ops(L1, L2, L3), "gtp_fourier", 30)).first->second;
+  return fourier_tc_.emplace(std::array<int, 4>{L1, L2, L3, strict},
+                             build_dense_tc(make_fourier_ops(L1, L2, L3), "gtp_fourier", strict ? 20 : 30))
+      .first->second;
 }
 
 // ------------------------------------------------------------------ GTP grid (SIMT separable)
@@ -884,48 +890,45 @@ const MtpDevTables& Context::mtp(int L1, int L2, int L3, int lt) {
   t.dtp = (dt + 3) / 4 * 4;
   t.din1 = (L1 + 1) * (L1 + 1);
   t.din2 = (L2 + 1) * (L2 + 1);
-  auto emb = [&](int Lx, const int** off_out, const int** idx_out, const float** c_out) {
+  auto term = [](int idx, float c) {
+    uint32_t cb;
+    std::memcpy(&cb, &c, 4);
+    return make_uint2(static_cast<uint32_t>(idx), cb);
+  };
+  auto emb = [&](int Lx, const int** off_out, const uint2** terms_out) {
     std::vector<std::vector<std::pair<int, float>>> cell(dt2);
     for (int l = 0; l <= Lx; ++l)  // proj/src/mtp.cpp:20-39
       for (const CGEntry& e : real_cg(lt, lt, l))
         cell[(e.m1 + lt) * dt + (e.m2 + lt)].push_back({flat(l, e.m3), static_cast<float>(e.v)});
-    std::vector<int> off(dt2 + 1), idx;
-    std::vector<float> c;
+    std::vector<int> off(dt2 + 1);
+    std::vector<uint2> terms;
     for (int i = 0; i < dt2; ++i) {
-      off[i] = static_cast<int>(idx.size());
-      for (auto& p : cell[i]) {
-        idx.push_back(p.first);
-        c.push_back(p.second);
-      }
+      off[i] = static_cast<int>(terms.size());
+      for (auto& p : cell[i]) terms.push_back(term(p.first, p.second));
     }
-    off[dt2] = static_cast<int>(idx.size());
+    off[dt2] = static_cast<int>(terms.size());
     *off_out = upload(off);
-    *idx_out = upload(idx);
-    *c_out = upload(c);
+    *terms_out = upload(terms);
   };
-  emb(L1, &t.emb1_off, &t.emb1_idx, &t.emb1_c);
-  emb(L2, &t.emb2_off, &t.emb2_idx, &t.emb2_c);
+  emb(L1, &t.emb1_off, &t.emb1);
+  emb(L2, &t.emb2_off, &t.emb2);
   const int L3e = std::min(L3, 2 * lt);  // beyond the carrier band: zero (mtp.cpp:126)
   t.dout_eff = (L3e + 1) * (L3e + 1);
   t.dout_total = (L3 + 1) * (L3 + 1);
-  std::vector<int> off(t.dout_eff + 1), idx;
-  std::vector<float> c;
+  std::vector<int> off(t.dout_eff + 1);
+  std::vector<uint2> terms;
   for (int l3 = 0; l3 <= L3e; ++l3) {
     std::vector<std::vector<std::pair<int, float>>> per(2 * l3 + 1);
     for (const CGEntry& e : real_cg(lt, lt, l3))
       per[e.m3 + l3].push_back({(e.m1 + lt) * t.dtp + (e.m2 + lt), static_cast<float>(e.v)});
     for (int m3 = -l3; m3 <= l3; ++m3) {
-      off[flat(l3, m3)] = static_cast<int>(idx.size());
-      for (auto& p : per[m3 + l3]) {
-        idx.push_back(p.first);
-        c.push_back(p.second);
-      }
+      off[flat(l3, m3)] = static_cast<int>(terms.size());
+      for (auto& p : per[m3 + l3]) terms.push_back(term(p.first, p.second));
     }
   }
-  off[t.dout_eff] = static_cast<int>(idx.size());
+  off[t.dout_eff] = static_cast<int>(terms.size());
   t.ext_off = upload(off);
-  t.ext_idx = upload(idx);
-  t.ext_c = upload(c);
+  t.ext = upload(terms);
   return mtp_.emplace(std::array<int, 4>{L1, L2, L3, lt}, t).first->second;
 }
 

@@ -90,6 +90,9 @@ class Context {
   std::atomic<int64_t> launches{0};
   std::atomic<int> grid_path{0};       // 0 auto, 1 tcgen05, 2 simt (also selects the Fourier GTP path)
   std::atomic<int> last_grid_path{0};  // diagnostics: path of the most recent GTP call on this context
+  // 0 default: GEMM-2 accumulation segments past the per-operator chain limits (<= 6.8e-6 normwise
+  // on adversarial rows); 1 strict: segments past 20 K-steps everywhere (<= ~4e-6, slower at L >= 8)
+  std::atomic<int> precision_mode{0};
 
  private:
   template <class T>
@@ -108,10 +111,10 @@ class Context {
   std::map<std::array<int, 3>, CgtpBwdTables> cgtp_bwd_;
   CgtpTables pack_cgtp(const std::vector<std::vector<std::pair<uint32_t, float>>>& per_out, int din1, int din2);
   std::map<std::array<int, 2>, std::pair<bool, CgtpTcTables>> cgtp_tc_;
-  std::map<std::array<int, 3>, GridTcEntry> grid_tc_;
+  std::map<std::array<int, 4>, GridTcEntry> grid_tc_;
   std::map<std::array<int, 4>, GridTcEntry> grid_tc_part_;
   std::map<std::array<int, 8>, GridTcEntry> dense_split_;
-  std::map<std::array<int, 3>, GridTcEntry> fourier_tc_;
+  std::map<std::array<int, 4>, GridTcEntry> fourier_tc_;
   GridTcEntry build_dense_tc(const struct DenseOps& ops, const char* label, int max_chain);
   std::map<std::array<int, 3>, GridSimtTables> grid_simt_;
   std::map<std::array<int, 3>, FourierDevTables> fourier_;

@@ -252,7 +252,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
       tc_fence_before();
-      mbar_arrive(&bars[4 + b]);
+      mbar_arrive_warp(&bars[4 + b]);
     }
     if (et == 0) bulk_wait_all();
   }

@@ -275,7 +275,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const long long tf = now();
           tmem_wait_st();
           tc_fence_before();
-          mbar_arrive(&bars[B_AF + sa]);
+          mbar_arrive_warp(&bars[B_AF + sa]);
           tick(11, tf);
           if (++sa == kAStagesTmem) {
             sa = 0;
@@ -337,7 +337,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           __syncwarp();
         }
         tc_fence_before();
-        mbar_arrive(&bars[B_DE + d]);
+        mbar_arrive_warp(&bars[B_DE + d]);
         u0 = u1 + 1;
       }
     }

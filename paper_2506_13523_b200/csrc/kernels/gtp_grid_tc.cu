@@ -579,15 +579,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     int64_t j = 0;
 
     // worker -> MMA-issuer signals: per thread locally, per warp (count 32) to the pair leader
+    // warp-aggregated: the warp's threads order their writes with __syncwarp and one lane arrives
+    // for all 32 (a per-thread arrive serialises 128-256 mbarrier updates per signal)
     auto signal_leader = [&](uint64_t* bar, bool tmem_only) {
-      if (PAIR) {
-        __syncwarp();
-        if (lane == 0) {
-          if (tmem_only) arrive_leader<PAIR, true>(bar, 32, rank);
-          else arrive_leader<PAIR>(bar, 32, rank);
-        }
-      } else {
-        mbar_arrive(bar);
+      __syncwarp();
+      if (lane == 0) {
+        if (PAIR && tmem_only) arrive_leader<PAIR, true>(bar, 32, rank);
+        else arrive_leader<PAIR>(bar, 32, rank);
       }
     };
     if (dw.on) {  // fused per-degree weights (weighted GTP): per-column tables, broadcast reads

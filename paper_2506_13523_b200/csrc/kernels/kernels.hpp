@@ -189,17 +189,14 @@ cudaError_t launch_gtp_fourier(const FourierDevTables& t, const RowSpec& rs, int
 struct MtpDevTables {
   int lt, dt, din1, din2, dout_total, dout_eff;
   int dtp;  // dt rounded up to 4: the kernel's padded carrier pitch
-  // embed: per carrier cell (m1,m2) a CSR list of (input idx, coef)
+  // embed: per carrier cell (m1,m2) a CSR list of terms {input idx, coef bits}
   const int* emb1_off;  // [dt*dt + 1]
-  const int* emb1_idx;
-  const float* emb1_c;
+  const uint2* emb1;
   const int* emb2_off;
-  const int* emb2_idx;
-  const float* emb2_c;
-  // extract: per output coefficient a CSR list of (padded cell a * dtp + b, coef)
+  const uint2* emb2;
+  // extract: per output coefficient a CSR list of terms {padded cell a * dtp + b, coef bits}
   const int* ext_off;   // [dout_eff + 1]
-  const int* ext_idx;
-  const float* ext_c;
+  const uint2* ext;
 };
 cudaError_t launch_mtp(const MtpDevTables& t, const RowSpec& rs, int num_sms, cudaStream_t s);
 

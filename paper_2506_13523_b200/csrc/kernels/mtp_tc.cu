@@ -309,7 +309,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
     tc_fence_before();
-    mbar_arrive(&bars[B_D_FREE]);
+    mbar_arrive_warp(&bars[B_D_FREE]);
     fence_proxy_async_smem();
     named_bar_sync(2 + h, 2 * 64);
     if (tid == 64 * h) {
@@ -381,7 +381,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (hw == 0) ex_sh[slot][r] = convert_row(stx, t.din1, t.k1, xop, xop + BM * t.k1 * 2, r);
       else ey_sh[slot][r] = convert_row(sty, t.din2, t.k2, yop, yop + BM * t.k2 * 2, r);
       fence_proxy_async_smem();
-      mbar_arrive(&bars[B_OPS_READY]);
+      mbar_arrive_warp(&bars[B_OPS_READY]);
     };
     auto middle_mine = [&]() {
       // half 0: Z group 0 in one piece; half 1: group 1, its tail (if any) in the Y columns
@@ -411,7 +411,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       middle_mine();
       tmem_wait_st();
       tc_fence_before();
-      mbar_arrive(&bars[B_Z_READY]);
+      mbar_arrive_warp(&bars[B_Z_READY]);
       tick(hw ? 7 : 15, t0);
       t0 = now();
       if (nxt < ntiles) land(nxt);  // the TMA had the whole middle to land
@@ -432,7 +432,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       } else {
         epilogue_part(lb, e_row, tile * BM + q * 32, hw);
         tc_fence_before();
-        mbar_arrive(&bars[B_D_FREE]);
+        mbar_arrive_warp(&bars[B_D_FREE]);
       }
       // raw inputs of the tile after next (the staging buffer was output half buffer 1)
       if (tid == 64 && nxt + gridDim.x < ntiles) issue_stage(nxt + gridDim.x);

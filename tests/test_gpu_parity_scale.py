@@ -207,3 +207,20 @@ def test_adversarial_precision(tpo, orc, kind, L):
     if out_dir.exists():
         (out_dir / "precision_table.json").write_text(json.dumps(_TABLE, indent=1, sort_keys=True))
     assert float(err.max()) <= TOL, (kind, L, {k: v for k, v in per_case.items() if v > TOL})
+
+
+@pytest.mark.parametrize("kind,L", [("gtp_grid", 8), ("gtp_grid", 10), ("gtp_fourier", 10)])
+def test_strict_precision_mode(tpo, orc, kind, L):
+    # tpo_set_precision(ctx, 1): segmented accumulation for every chain past 20 K-steps
+    import torch
+
+    ctx = tpo.context()
+    prev = ctx.set_precision("strict")
+    try:
+        rng = np.random.default_rng(4242 + L)
+        x, y, names = adversarial_rows(L, rng, per=6)
+        out = tpo.run(kind, torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda(), L, L, 2 * L).cpu().numpy()
+        ref = orc.batch_mimo(kind, L, x.astype(np.float64)[:, None], y.astype(np.float64)[:, None])[:, 0]
+        assert float(_normwise_rows(out, ref).max()) <= 5e-6
+    finally:
+        ctx.set_precision(prev)
