@@ -945,20 +945,27 @@ const CgtpTcTables* Context::cgtp_tc(int L1, int L2) {
     return nullptr;
   };
   const char* env = std::getenv("TPO_CGTP_TC");
-  // L <= 15: with the operands scaled into fp16's normal range the block path stays <= 2.6e-6
-  // normwise on adversarial rows through L = 15 (profiles/r02i; before: 1.1-1.4e-5 at L = 15); at
-  // L = 16 the blocks do not fit the kernel's staging, SIMT beyond
+  // L <= 16: with the operands scaled into fp16's normal range the block path stays <= 2.6e-6
+  // normwise on adversarial rows through L = 15 (profiles/r02i; before: 1.1-1.4e-5 at L = 15)
   static const int max_l = [] {
     const char* v = std::getenv("TPO_CGTP_TC_MAXL");  // A/B and accuracy experiments only
-    return v ? std::atoi(v) : 15;
+    return v ? std::atoi(v) : 16;
   }();
   if ((env && env[0] == '0') || L1 > std::min(max_l, 16) || L2 > std::min(max_l, 16)) return fail();
   CgtpTcTables t{};
   t.din1 = (L1 + 1) * (L1 + 1);
   t.din2 = (L2 + 1) * (L2 + 1);
+  // per-row staging (y row + x_{l1} segment) takes most of shared memory at large L: the W ring
+  // needs two stages of 64 * part-width bytes, so the block outputs are cut into narrower N parts
+  // when 192-column parts do not fit (L = 16)
   std::vector<CgtpTcUnit> units;
   std::vector<uint16_t> w;
   int out_off = 0, max_npad = 16;
+  t.xy_pitch = (t.din2 + 33 + 8) | 1;  // y row | x_{l1} (kXSeg; reads may run 7 past a y segment)
+  const int xy_bytes = 128 * t.xy_pitch * 4;
+  const int budget = 186 * 1024 - xy_bytes;  // the kernel's static staging takes ~35 KB
+  int part_cols = 192;
+  while (part_cols > 32 && budget / (64 * part_cols) < 2) part_cols -= 32;
   for (int l1 = 0; l1 <= L1; ++l1)
     for (int l2 = 0; l2 <= L2; ++l2) {
       const int n1 = 2 * l1 + 1, n2 = 2 * l2 + 1, n = n1 * n2;
@@ -972,7 +979,7 @@ const CgtpTcTables* Context::cgtp_tc(int L1, int L2) {
       // K order k = m1 * n2p + m2 (n2p = n2 padded to 8; zero columns at the padding)
       const int n2p = pad_to(n2, 8), kw = n1 * n2p;
       const int kpad = pad_to(kw, 16), npad_all = pad_to(n, 16);
-      const int parts = (npad_all + 191) / 192;  // accumulators of 192 columns (cgtp_tc.cu kDCols)
+      const int parts = (npad_all + part_cols - 1) / part_cols;  // accumulators of <= 192 columns (cgtp_tc.cu kDCols)
       const int np = pad_to((n + parts - 1) / parts, 16);
       for (int p = 0; p < parts; ++p) {
         CgtpTcUnit u{};
@@ -1020,9 +1027,6 @@ const CgtpTcTables* Context::cgtp_tc(int L1, int L2) {
   t.w = reinterpret_cast<const uint8_t*>(upload(w));
   // shared memory: A ring (8 KB stages) | W ring | per-row x | y staging (odd pitch)
   t.b_stage_bytes = 64 * max_npad;
-  t.xy_pitch = (t.din2 + 33 + 8) | 1;  // y row | x_{l1} (kXSeg; reads may run 7 past a y segment)
-  const int xy_bytes = 128 * t.xy_pitch * 4;
-  const int budget = 186 * 1024 - xy_bytes;  // the kernel's static staging takes ~35 KB
   const char* as_env = std::getenv("TPO_CGTP_ASTAGES");
   (void)as_env;
   t.a_stages = 4;  // the P ring lives in TMEM (cgtp_tc.cu kAStagesTmem)
