@@ -536,9 +536,7 @@ def run_ours(args, world, rank, local):
     for (kind, L), ms in per_ms.items():
         n = sum(p[5] for p in probs if (p[0], p[1]) == (kind, L))
         ek = "cgtp" if kind == "cgtp" else kind
-        path = "tc"
-        if kind in ("gtp_grid", "gtp_fourier") and L > 14:
-            path = "simt"
+        path = "simt" if (kind == "gtp_grid" and L > 14) or (kind == "gtp_fourier" and L > 16) else "tc"
         t_roof, bound = roofline_time(ek, L, n, peaks, path)
         if w == "c4":
             t_roof = n // C4_CHANNELS * c4_bytes_per_edge() / (peaks["hbm_gbs"] * 1e9)
@@ -550,7 +548,7 @@ def run_ours(args, world, rank, local):
     dk, dL = dom
     dn = sum(p[5] for p in probs if (p[0], p[1]) == dom)
     dms = per_ms[dom]
-    if dk in ("gtp_grid", "gtp_fourier") and dL <= 14:
+    if (dk == "gtp_grid" and dL <= 14) or dk == "gtp_fourier":
         ach = dense_flops_per_tp(dk, dL) * dn / (dms / 1e3) / 1e12
         roofline = {"bound": "tensor", "kernel": f"gtp_grid_tc_kernel {dk} L={dL} (3xFP16 tcgen05)",
                     "achieved": round(ach, 2), "peak": round(peaks["bf16_tflops"] / 3, 1), "unit": "TFLOP/s",
@@ -570,13 +568,24 @@ def run_ours(args, world, rank, local):
     roofline["share_of_step"] = round(sum(per_ms[k] for k in [dom]) / ms_per_step, 3)
     roofline["traffic"] = None
     tf_path = ROOT / "profiles" / "ncu_traffic.json"
-    if tf_path.exists():
+    if tf_path.exists():  # DRAM bytes of one ncu --set full capture of the same kernel (tools/profile_kernel.py)
         try:
-            roofline["traffic"] = json.loads(tf_path.read_text()).get(f"{dk}_L{dL}" + ("_c4" if w == "c4" else ""))
+            tr = json.loads(tf_path.read_text()).get(f"{dk}_L{dL}" + ("_c4" if w == "c4" else ""))
+            if tr is not None:
+                # captures: 65,536 rows (c2 / c3 / grid), 16,384 edges x 128 channels (c4), 16,384 rows
+                # (MTP SIMT, Fourier L >= 13), 2,048 rows (CGTP L = 16): scaled to this launch's rows
+                cap_rows = {"c4": 16384 * C4_CHANNELS}.get(w, 65536)
+                if dk == "cgtp" and dL == 16:
+                    cap_rows = 2048
+                elif (dk == "mtp" and dL > 6) or (dk == "gtp_fourier" and dL > 12):
+                    cap_rows = 16384
+                roofline["traffic"] = round(tr * dn / cap_rows, 1)
+                roofline["traffic_note"] = (f"ncu dram__bytes_read+write of a {cap_rows}-row capture "
+                                            f"(profiles/ncu_traffic.json), scaled to the {dn}-row launch")
         except Exception:
             pass
     step_roof = sum(roofline_time("cgtp" if k == "cgtp" else k, L, sum(p[5] for p in probs if (p[0], p[1]) == (k, L)),
-                                  peaks, "simt" if (k in ("gtp_grid", "gtp_fourier") and L > 14) else "tc")[0]
+                                  peaks, "simt" if (k == "gtp_grid" and L > 14) else "tc")[0]
                     for (k, L) in per_ms) if w != "c4" else None
     if step_roof is not None:
         roofline["step_frac"] = round(step_roof / (ms_per_step / 1e3), 4)

@@ -420,9 +420,10 @@ GridTcEntry Context::build_dense_tc(const DenseOps& ops, const char* label, int 
     // L = 12 to three digits; tools/precision_model.py), so one accumulator over the whole grid
     // (77 K-steps at L = 12) costs ~1e-5 normwise; segments added in fp32 keep it ~3-4e-6
     // Single accumulation while the chain is short enough for the operator family (max_chain K-steps,
-    // measured: grid operators <= 6.8e-6 at L = 10 (54 K-steps), folded torus operators 9.9e-6 at
-    // L = 10, 3.6e-6 at L = 7 (29 K-steps), adversarial inputs, profiles/r02d); segments cost a
-    // drain of Z per boundary (fp32 reductions in L2), ~25% at L = 10, so they are used only past that
+    // measured on adversarial rows, profiles/r02d: grid operators <= 6.8e-6 at L = 10 (54 K-steps);
+    // folded torus operators 3.6e-6 at L = 7 (<= 32 K-steps), 7.0e-6 / 9.9e-6 at L = 8 / 10);
+    // segments cost a drain of Z per boundary (fp32 reductions in L2), ~25-45%, so they are used
+    // only past those limits
     const int seg_slices = std::max(1, env_int("TPO_GRID_SEG_SLICES", 20));
     const int total = t.nchunks * t.nslices;
     const int nseg = total > env_int("TPO_GRID_MAX_CHAIN", max_chain) ? (total + seg_slices - 1) / seg_slices : 1;
@@ -774,7 +775,7 @@ const GridTcEntry& Context::fourier_tc(int L1, int L2, int L3) {
   auto it = fourier_tc_.find({L1, L2, L3, strict});
   if (it != fourier_tc_.end()) return it->second;
   return fourier_tc_.emplace(std::array<int, 4>{L1, L2, L3, strict},
-                             build_dense_tc(make_fourier_ops(L1, L2, L3), "gtp_fourier", strict ? 20 : 30))
+                             build_dense_tc(make_fourier_ops(L1, L2, L3), "gtp_fourier", strict ? 20 : 36))
       .first->second;
 }
 
