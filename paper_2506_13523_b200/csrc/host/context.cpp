@@ -424,7 +424,9 @@ GridTcEntry Context::build_dense_tc(const DenseOps& ops, const char* label, int 
     // folded torus operators 3.6e-6 at L = 7 (<= 32 K-steps), 7.0e-6 / 9.9e-6 at L = 8 / 10);
     // segments cost a drain of Z per boundary (fp32 reductions in L2), ~25-45%, so they are used
     // only past those limits
-    const int seg_slices = std::max(1, env_int("TPO_GRID_SEG_SLICES", 20));
+    // segment length: 30 K-steps by default (two segments up to 60: torus L = 8-10; three for grid
+    // L = 11, Fourier L = 11-12), 20 in strict mode
+    const int seg_slices = std::max(1, env_int("TPO_GRID_SEG_SLICES", max_chain <= 20 ? 20 : 30));
     const int total = t.nchunks * t.nslices;
     const int nseg = total > env_int("TPO_GRID_MAX_CHAIN", max_chain) ? (total + seg_slices - 1) / seg_slices : 1;
     t.seg_chunks = std::max(1, (t.nchunks + nseg - 1) / nseg);

@@ -685,7 +685,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           float* op = op0 + cb * 16;
           const float* sp = sp0;
           const float wc = dw.on ? wtab_c[col0 + cb * 16 + cl] : 1.f;  // fused output weights (weighted GTP)
-          if (SEG && add) {  // later segments: fire-and-forget fp32 reductions in L2 (red.global.add, round to nearest)
+          if (SEG && add && !(t.dbg & 8)) {  // later segments: fire-and-forget fp32 reductions in L2 (red.global.add, round to nearest)
             for (int rr = 0; rr < (full ? 32 : left); rr += 2, op += stride2, sp += 2 * kStageStride)
               atomicAdd(op, *sp * wc);
           } else if (full) {

@@ -131,7 +131,8 @@ struct GridTcTables {
                              // number of MMAs into one accumulator; each segment starts a fresh Z and its
                              // partial sum is added in fp32 (round to nearest) into the output row
   int pair;                  // CTA pairs, tcgen05 cta_group::2 (M = 256); slices stored as two row halves
-  int dbg;                   // timing experiments only (results invalid): 1 no product, 2 no epilogue, 4 no convert
+  int dbg;                   // timing experiments only (results invalid): 1 no product, 2 no epilogue, 4 no convert,
+                             // 8 plain stores instead of reductions for segment sums
   int smem_bytes;
   uint32_t off_x, off_y, off_raw, off_sring, off_aring, off_stage;  // dynamic shared-memory carve-up
   const uint8_t* s1;
