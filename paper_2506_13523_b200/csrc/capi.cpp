@@ -597,6 +597,35 @@ int tpo_backward_f32(tpo_ctx* ctx, int kind, int L1, int L2, int L3, int l_tilde
     switch (kind) {
       case TPO_KIND_CGTP: {
         if (rows == 0) return;
+        // both gradients in one pass over grad_out on the tensor cores (cgtp_bwd_tc.cu); grad_out is
+        // read through a [rows / 4][4 Dout] TMA view, so a ragged tail of < 4 rows and unaligned
+        // buffers take the SIMT term-list kernel
+        const tpo_b200::CgtpBwdTcTables* tc =
+            !y_shared && (reinterpret_cast<uintptr_t>(grad_out) & 15) == 0 ? c.cgtp_bwd_tc(L1, L2) : nullptr;
+        const int64_t rows4 = tc ? (rows & ~int64_t{3}) : 0;
+        if (rows4 > 0) {
+          const int64_t d1 = (L1 + 1) * (L1 + 1), d2 = (L2 + 1) * (L2 + 1), dout = d1 * d2;
+          CUtensorMap tm;
+          tpo_b200::encode_tmap_2d(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, grad_out, 4 * dout, rows4 / 4, 16 * dout, 36,
+                                   32, CU_TENSOR_MAP_SWIZZLE_NONE);
+          launched(ctx, tpo_b200::launch_cgtp_bwd_tc(*tc, x, y, grad_out, tm, grad_x, grad_y, rows4, c.num_sms(), s),
+                   "cgtp backward tcgen05 kernel");
+          if (rows4 == rows) return;
+          const int64_t tail = rows - rows4;
+          if (grad_x)
+            launched(ctx, tpo_b200::launch_cgtp_bwd(c.cgtp_bwd(L1, L2, 0),
+                                                    rows_of(grad_out + rows4 * dout, y + rows4 * d2, grad_x + rows4 * d1,
+                                                            tail, 1, 0),
+                                                    c.num_sms(), s),
+                     "cgtp backward kernel");
+          if (grad_y)
+            launched(ctx, tpo_b200::launch_cgtp_bwd(c.cgtp_bwd(L1, L2, 1),
+                                                    rows_of(grad_out + rows4 * dout, x + rows4 * d1, grad_y + rows4 * d2,
+                                                            tail, 1, 0),
+                                                    c.num_sms(), s),
+                     "cgtp backward kernel");
+          return;
+        }
         if (grad_x)
           launched(ctx, tpo_b200::launch_cgtp_bwd(c.cgtp_bwd(L1, L2, 0), rows_of(grad_out, y, grad_x, batch, channels, y_shared),
                                                   c.num_sms(), s),

@@ -1045,6 +1045,112 @@ const CgtpTcTables* Context::cgtp_tc(int L1, int L2) {
   return &cgtp_tc_.emplace(std::array<int, 2>{L1, L2}, std::make_pair(true, t)).first->second.second;
 }
 
+// CGTP backward blocks (cgtp_bwd_tc.cu): the transposed block W^T[k][o] with k unpadded,
+// k = (m1 + l1)(2 l2 + 1) + m2 + l2, o in the forward's path order.  The kernel keeps the row's
+// x | y and grad_x | grad_y in shared memory beside the grad_out and W^T rings, which bounds it to
+// din1 + din2 <= 98 (L <= 6); shapes whose blocks fit one accumulator hand-off per tile (L1 + L2 <= 4
+// or so) are faster on the SIMT kernel.
+const CgtpBwdTcTables* Context::cgtp_bwd_tc(int L1, int L2) {
+  const char* env = std::getenv("TPO_CGTP_BWD_TC");  // "0": the SIMT kernel (A/B and tests; read per call)
+  if (env && env[0] == '0') return nullptr;
+  std::lock_guard<std::mutex> g(mu_);
+  auto it = cgtp_bwd_tc_.find({L1, L2});
+  if (it != cgtp_bwd_tc_.end()) return it->second.first ? &it->second.second : nullptr;
+  auto fail = [&]() -> const CgtpBwdTcTables* {
+    cgtp_bwd_tc_.emplace(std::array<int, 2>{L1, L2}, std::make_pair(false, CgtpBwdTcTables{}));
+    return nullptr;
+  };
+  if (L1 > 6 || L2 > 6) return fail();
+  CgtpBwdTcTables t{};
+  t.din1 = (L1 + 1) * (L1 + 1);
+  t.din2 = (L2 + 1) * (L2 + 1);
+  t.nblocks = (L1 + 1) * (L2 + 1);
+  std::vector<CgtpBwdTcUnit> units;
+  std::vector<uint16_t> w;
+  int g_off = 0, max_npad = 16;
+  for (int l1 = 0; l1 <= L1; ++l1)
+    for (int l2 = 0; l2 <= L2; ++l2) {
+      const int n1 = 2 * l1 + 1, n2 = 2 * l2 + 1, n = n1 * n2;
+      std::vector<double> W(static_cast<size_t>(n) * n, 0.0);  // W[o][k]
+      int o0 = 0;
+      for (int l3 = std::abs(l1 - l2); l3 <= l1 + l2; ++l3) {
+        for (const CGEntry& e : real_cg(l1, l2, l3))
+          W[static_cast<size_t>(o0 + e.m3 + l3) * n + (e.m1 + l1) * n2 + (e.m2 + l2)] += e.v;
+        o0 += 2 * l3 + 1;
+      }
+      const int npad_all = pad_to(n, 16), parts = (npad_all + 191) / 192;
+      const int np = pad_to((n + parts - 1) / parts, 16);
+      for (int p = 0; p < parts; ++p) {
+        CgtpBwdTcUnit u{};
+        u.l1 = l1;
+        u.l2 = l2;
+        u.blk = l1 * (L2 + 1) + l2;
+        u.g_off = g_off;
+        u.n = n;
+        u.k0 = p * np;
+        u.n_valid = std::min(np, n - p * np);
+        u.n_pad = pad_to(u.n_valid, 16);
+        u.ksteps = pad_to(n, 16) / 16;
+        u.w_off = static_cast<int>(w.size() * 2);
+        max_npad = std::max(max_npad, u.n_pad);
+        const size_t base = w.size();
+        w.resize(base + static_cast<size_t>(u.ksteps) * 2 * u.n_pad * 16, 0);
+        for (int ks = 0; ks < u.ksteps; ++ks) {
+          uint16_t* hi = w.data() + base + static_cast<size_t>(ks) * 2 * u.n_pad * 16;
+          uint16_t* lo = hi + u.n_pad * 16;
+          for (int r = 0; r < u.n_valid; ++r)
+            for (int kk = 0; kk < 16; ++kk) {
+              const int o = ks * 16 + kk;
+              if (o >= n) continue;
+              uint16_t hv, lv;
+              split_half(std::ldexp(W[static_cast<size_t>(o) * n + u.k0 + r], kTabShift), hv, lv);
+              const uint32_t off = sm100::canon_off(r, kk, u.n_pad) / 2;
+              hi[off] = hv;
+              lo[off] = lv;
+            }
+        }
+        units.push_back(u);
+      }
+      g_off += n;
+    }
+  int superunits = 1;
+  for (size_t i = 0, col = 0; i < units.size(); ++i) {
+    if (col + units[i].n_pad > 192) {
+      units[i - 1].dcol_last |= 1 << 16;
+      col = 0;
+      ++superunits;
+    }
+    units[i].dcol_last = static_cast<int>(col);
+    col += units[i].n_pad;
+  }
+  units.back().dcol_last |= 1 << 16;
+  if (superunits < 2) return fail();  // small shapes: the SIMT kernel (cgtp_bwd.cu)
+  t.dout = g_off;
+  t.nunits = static_cast<int>(units.size());
+  t.nbp = (t.nblocks + 3) & ~3;
+  t.b_stage_bytes = 64 * max_npad;
+  constexpr int kSmemMax = 225 * 1024;
+  // grad_out ring (HBM) and W^T ring (L2): the deepest grad_out ring that leaves >= 4 W^T stages
+  t.g_slots = 3;
+  for (int gsl : {8, 4})
+    if (cgtp_bwd_tc_smem(t, 4, gsl) <= kSmemMax) {
+      t.g_slots = gsl;
+      break;
+    }
+  t.b_stages = std::min(8, (kSmemMax - cgtp_bwd_tc_smem(t, 0, t.g_slots)) / t.b_stage_bytes);
+  if (t.b_stages < 2) return fail();
+  t.units = upload(units);
+  t.w = reinterpret_cast<const uint8_t*>(upload(w));
+  t.off_b = 0;
+  t.off_xy = t.b_stages * t.b_stage_bytes;
+  t.off_g = t.off_xy + 2 * 128 * ((t.din1 + t.din2) | 1) * 4;
+  t.smem_bytes = cgtp_bwd_tc_smem(t, t.b_stages, t.g_slots);
+  if (std::getenv("TPO_VERBOSE"))
+    std::fprintf(stderr, "[tpo] cgtp bwd tcgen05 L=(%d,%d) units=%d super=%d b_stages=%d g_slots=%d smem=%d\n", L1, L2,
+                 t.nunits, superunits, t.b_stages, t.g_slots, t.smem_bytes);
+  return &cgtp_bwd_tc_.emplace(std::array<int, 2>{L1, L2}, std::make_pair(true, t)).first->second.second;
+}
+
 // ------------------------------------------------------------------ MTP, tcgen05
 // Dense embed / extract operators in the TMEM orders of mtp_tc.cu
 // (kernels.hpp, MtpTcTables), same CG tables as Context::mtp

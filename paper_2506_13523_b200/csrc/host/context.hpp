@@ -58,6 +58,7 @@ class Context {
   // backward term tables (wrt 0: grad_x, 1: grad_y), cgtp_bwd.cu
   const CgtpBwdTables& cgtp_bwd(int L1, int L2, int wrt);
   const CgtpTcTables* cgtp_tc(int L1, int L2);  // nullptr: shape not on the tcgen05 block path
+  const CgtpBwdTcTables* cgtp_bwd_tc(int L1, int L2);  // nullptr: backward shape not on tcgen05
   const GridTcEntry& grid_tc(int L1, int L2, int L3);
   // forward with inputs past the K limit: x degrees [a1, b1] x y degrees [a2, b2] of the full operators
   const GridTcEntry& dense_split_tc(int fourier, int L1, int L2, int L3, int a1, int b1, int a2, int b2);
@@ -111,6 +112,7 @@ class Context {
   std::map<std::array<int, 3>, CgtpBwdTables> cgtp_bwd_;
   CgtpTables pack_cgtp(const std::vector<std::vector<std::pair<uint32_t, float>>>& per_out, int din1, int din2);
   std::map<std::array<int, 2>, std::pair<bool, CgtpTcTables>> cgtp_tc_;
+  std::map<std::array<int, 2>, std::pair<bool, CgtpBwdTcTables>> cgtp_bwd_tc_;
   std::map<std::array<int, 4>, GridTcEntry> grid_tc_;
   std::map<std::array<int, 4>, GridTcEntry> grid_tc_part_;
   std::map<std::array<int, 8>, GridTcEntry> dense_split_;

@@ -101,6 +101,27 @@ struct CgtpTcTables {
 };
 cudaError_t launch_cgtp_tc(const CgtpTcTables& t, const RowSpec& rs, int num_sms, cudaStream_t s);
 
+// CGTP backward on tcgen05 (cgtp_bwd_tc.cu): per (l1, l2) block Q = W^T g_block as a dense GEMM
+// (A = grad_out block, K = block outputs o; N = k = (m1 + l1)(2 l2 + 1) + m2 + l2), contracted with
+// y / x in the epilogue.  A unit is one block (n <= 169 columns: L <= 6, a single N part); w holds per unit and K-step
+// [hi | lo][n_pad rows (k)][16 (o)] canonical, times 2^kTabShift.
+struct CgtpBwdTcUnit {
+  int l1, l2, blk, g_off, n, k0, n_valid, n_pad, ksteps, w_off;
+  int dcol_last;  // as CgtpTcUnit
+};
+struct CgtpBwdTcTables {
+  int din1, din2, dout, nunits, nblocks, nbp;  // nbp: nblocks rounded up to 4 (exponent rows)
+  int b_stages, b_stage_bytes, g_slots, smem_bytes, off_b, off_xy, off_g;
+  const CgtpBwdTcUnit* units;
+  const uint8_t* w;
+  alignas(64) CUtensorMap tm_g;  // set per call by the launcher
+};
+int cgtp_bwd_tc_smem(const CgtpBwdTcTables& t, int b_stages, int g_slots);
+// tm_g: grad_out viewed as [rows / 4][4 Dout] fp32 (rows a multiple of 4), box 36 x 32, no swizzle
+cudaError_t launch_cgtp_bwd_tc(const CgtpBwdTcTables& t, const float* x, const float* y, const float* g,
+                               const CUtensorMap& tm_g, float* gx, float* gy, int64_t rows, int num_sms,
+                               cudaStream_t s);
+
 // ---------------------------------------------------------------- GTP grid, tcgen05
 // Dense operators of the reference's product grid, pre-split into fp16 hi/lo
 // and pre-tiled on the host in the UMMA canonical K-major layout, one

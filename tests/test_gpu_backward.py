@@ -216,3 +216,59 @@ def test_backward_unequal_degrees_simt_path(tpo, orc):
             assert _normwise(gy.cpu().numpy().astype(np.float64), ry) <= TOL
     finally:
         ctx.set_grid_path("auto")
+
+
+def _cgtp_ref_vjp(orc, L1, L2, x, y, g):
+    """CGTP (grad_x, grad_y) for unequal degrees from oracle Jacobians on basis vectors."""
+    t1, t2 = orc.tower(L1), orc.tower(L2)
+    d1, d2 = (L1 + 1) ** 2, (L2 + 1) ** 2
+    gx = np.empty((x.shape[0], d1)); gy = np.empty((x.shape[0], d2))
+    for r in range(x.shape[0]):
+        Jx = np.stack([orc.cgtp_mimo(t1, e, t2, y[r]) for e in np.eye(d1)])
+        Jy = np.stack([orc.cgtp_mimo(t1, x[r], t2, e) for e in np.eye(d2)])
+        gx[r] = Jx @ g[r]
+        gy[r] = Jy @ g[r]
+    return gx, gy
+
+
+@pytest.mark.parametrize("L1,L2", [(6, 3), (3, 5), (4, 4), (2, 6), (6, 6), (5, 1)])
+def test_backward_cgtp_unequal_degrees(tpo, orc, L1, L2):
+    # the tcgen05 block backward (cgtp_bwd_tc.cu) takes L1, L2 <= 6; (5, 1) and small shapes stay
+    # on the SIMT term-list kernel
+    import torch
+
+    rng = np.random.default_rng(17 * L1 + L2)
+    B = 5
+    x = rng.standard_normal((B, (L1 + 1) ** 2)).astype(np.float32)
+    y = rng.standard_normal((B, (L2 + 1) ** 2)).astype(np.float32)
+    g = rng.standard_normal((B, (L1 + 1) ** 2 * (L2 + 1) ** 2)).astype(np.float32)
+    gx, gy = tpo.backward("cgtp", torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda(), torch.from_numpy(g).cuda(),
+                          L1, L2)
+    rx, ry = _cgtp_ref_vjp(orc, L1, L2, x.astype(np.float64), y.astype(np.float64), g.astype(np.float64))
+    assert _normwise(gx.cpu().numpy().astype(np.float64), rx) <= TOL
+    assert _normwise(gy.cpu().numpy().astype(np.float64), ry) <= TOL
+
+
+@pytest.mark.parametrize("L", [3, 4, 5, 6])
+def test_backward_cgtp_tc_matches_simt(tpo, monkeypatch, L):
+    """Ragged batch (1,000 rows: a partial last tile) with per-row scales over 1e-20 .. 1e20 and
+    one-sided requests: the tcgen05 backward against the SIMT term-list kernel (fp32 sums, itself
+    oracle-checked above), normwise 1e-5 per row."""
+    import torch
+
+    B, D = 1000, (L + 1) ** 2
+    gen = torch.Generator(device="cuda").manual_seed(40 + L)
+    sc = 10.0 ** torch.linspace(-20, 20, B, device="cuda")[torch.randperm(B, device="cuda", generator=gen)]
+    x = torch.randn(B, D, device="cuda", generator=gen) * sc[:, None]
+    y = torch.randn(B, D, device="cuda", generator=gen) * sc.flip(0)[:, None]
+    g = torch.randn(B, D * D, device="cuda", generator=gen) * (sc ** 0.5)[:, None]
+    gx, gy = tpo.backward("cgtp", x, y, g, L, L)
+    gx1, _ = tpo.backward("cgtp", x, y, g, L, L, need_y=False)
+    _, gy1 = tpo.backward("cgtp", x, y, g, L, L, need_x=False)
+    monkeypatch.setenv("TPO_CGTP_BWD_TC", "0")
+    rx, ry = tpo.backward("cgtp", x, y, g, L, L)
+    torch.cuda.synchronize()
+    for out, ref in ((gx, rx), (gy, ry), (gx1, rx), (gy1, ry)):
+        a, b = out.double().cpu().numpy(), ref.double().cpu().numpy()
+        assert np.isfinite(a).all()
+        assert _normwise(a, b) <= TOL, (L, _normwise(a, b))

@@ -6,6 +6,9 @@ from collections import Counter
 
 rows = list(csv.reader(open(sys.argv[1])))
 hdr, data = rows[1], rows[2:]
+# several kernels / sections in one export: keep the first
+ends = [i for i, r in enumerate(data) if r and r[0] in ("Kernel Name", "Address")]
+data = data[: ends[0]] if ends else data
 ia, isrc, iss = hdr.index("Address"), hdr.index("Source"), hdr.index("Warp Stall Sampling (All Samples)")
 iex = hdr.index("Instructions Executed")
 st = [h for h in hdr if h.startswith("stall_") and "Not Issued" not in h]
