@@ -898,40 +898,42 @@ const MtpDevTables& Context::mtp(int L1, int L2, int L3, int lt) {
     std::memcpy(&cb, &c, 4);
     return make_uint2(static_cast<uint32_t>(idx), cb);
   };
-  auto emb = [&](int Lx, const int** off_out, const uint2** terms_out) {
-    std::vector<std::vector<std::pair<int, float>>> cell(dt2);
-    for (int l = 0; l <= Lx; ++l)  // proj/src/mtp.cpp:20-39
-      for (const CGEntry& e : real_cg(lt, lt, l))
-        cell[(e.m1 + lt) * dt + (e.m2 + lt)].push_back({flat(l, e.m3), static_cast<float>(e.v)});
-    std::vector<int> off(dt2 + 1);
+  // warp-interleaved term lists (see MtpDevTables): item i -> lane i % 32 of warp i / 32
+  auto interleave = [&](const std::vector<std::vector<std::pair<int, float>>>& lists, const int2** idx_out,
+                        const uint2** terms_out) {
+    std::vector<int2> idx(lists.size());
     std::vector<uint2> terms;
-    for (int i = 0; i < dt2; ++i) {
-      off[i] = static_cast<int>(terms.size());
-      for (auto& p : cell[i]) terms.push_back(term(p.first, p.second));
+    for (size_t w0 = 0; w0 < lists.size(); w0 += 32) {
+      size_t nt = 0;
+      for (size_t i = w0; i < std::min(lists.size(), w0 + 32); ++i) nt = std::max(nt, lists[i].size());
+      const size_t base = terms.size();
+      terms.resize(base + 32 * nt, make_uint2(0u, 0u));
+      for (size_t i = w0; i < std::min(lists.size(), w0 + 32); ++i) {
+        const size_t first = base + (i - w0);
+        idx[i] = make_int2(static_cast<int>(first), static_cast<int>(lists[i].size()));
+        for (size_t e = 0; e < lists[i].size(); ++e) terms[first + 32 * e] = term(lists[i][e].first, lists[i][e].second);
+      }
     }
-    off[dt2] = static_cast<int>(terms.size());
-    *off_out = upload(off);
+    *idx_out = upload(idx);
     *terms_out = upload(terms);
   };
-  emb(L1, &t.emb1_off, &t.emb1);
-  emb(L2, &t.emb2_off, &t.emb2);
+  std::vector<std::vector<std::pair<int, float>>> cells(2 * dt2);
+  for (int s2 = 0; s2 < 2; ++s2)
+    for (int l = 0; l <= (s2 ? L2 : L1); ++l)  // proj/src/mtp.cpp:20-39
+      for (const CGEntry& e : real_cg(lt, lt, l))
+        cells[s2 * dt2 + (e.m1 + lt) * dt + (e.m2 + lt)].push_back({flat(l, e.m3), static_cast<float>(e.v)});
+  interleave(cells, &t.emb_idx, &t.emb);
   const int L3e = std::min(L3, 2 * lt);  // beyond the carrier band: zero (mtp.cpp:126)
   t.dout_eff = (L3e + 1) * (L3e + 1);
   t.dout_total = (L3 + 1) * (L3 + 1);
-  std::vector<int> off(t.dout_eff + 1);
-  std::vector<uint2> terms;
-  for (int l3 = 0; l3 <= L3e; ++l3) {
-    std::vector<std::vector<std::pair<int, float>>> per(2 * l3 + 1);
-    for (const CGEntry& e : real_cg(lt, lt, l3))
-      per[e.m3 + l3].push_back({(e.m1 + lt) * t.dtp + (e.m2 + lt), static_cast<float>(e.v)});
-    for (int m3 = -l3; m3 <= l3; ++m3) {
-      off[flat(l3, m3)] = static_cast<int>(terms.size());
-      for (auto& p : per[m3 + l3]) terms.push_back(term(p.first, p.second));
+  std::vector<std::vector<std::pair<int, float>>> outs(2 * t.dout_eff);
+  for (int l3 = 0; l3 <= L3e; ++l3)
+    for (const CGEntry& e : real_cg(lt, lt, l3)) {
+      const std::pair<int, float> tm{(e.m1 + lt) * t.dtp + (e.m2 + lt), static_cast<float>(e.v)};
+      outs[2 * flat(l3, e.m3)].push_back(tm);  // product half 0
+      outs[2 * flat(l3, e.m3) + 1].push_back(tm);  // product half 1
     }
-  }
-  off[t.dout_eff] = static_cast<int>(terms.size());
-  t.ext_off = upload(off);
-  t.ext = upload(terms);
+  interleave(outs, &t.ext_idx, &t.ext);
   return mtp_.emplace(std::array<int, 4>{L1, L2, L3, lt}, t).first->second;
 }
 

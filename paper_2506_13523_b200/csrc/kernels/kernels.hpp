@@ -211,13 +211,14 @@ cudaError_t launch_gtp_fourier(const FourierDevTables& t, const RowSpec& rs, int
 struct MtpDevTables {
   int lt, dt, din1, din2, dout_total, dout_eff;
   int dtp;  // dt rounded up to 4: the kernel's padded carrier pitch
-  // embed: per carrier cell (m1,m2) a CSR list of terms {input idx, coef bits}
-  const int* emb1_off;  // [dt*dt + 1]
-  const uint2* emb1;
-  const int* emb2_off;
-  const uint2* emb2;
-  // extract: per output coefficient a CSR list of terms {padded cell a * dtp + b, coef bits}
-  const int* ext_off;   // [dout_eff + 1]
+  // Term lists {index, coef bits} stored warp-interleaved: item i (handled by lane i % 32) has
+  // idx[i] = {first, count} and its e-th term at first + 32 e, so a warp's term loads are coalesced.
+  // embed items: the dt*dt cells of X (index = x coefficient), then those of Y (index = y coefficient)
+  const int2* emb_idx;  // [2 dt*dt]
+  const uint2* emb;
+  // extract items: (output coefficient o < dout_eff, product half g) = 2 o + g (index = padded cell
+  // a * dtp + b)
+  const int2* ext_idx;  // [2 dout_eff]
   const uint2* ext;
 };
 cudaError_t launch_mtp(const MtpDevTables& t, const RowSpec& rs, int num_sms, cudaStream_t s);
