@@ -170,7 +170,7 @@ class Context:
 
     @property
     def last_grid_path(self) -> str:
-        return {0: "none", 1: "tcgen05", 2: "simt"}[lib().tpo_last_gtp_grid_path(self.handle)]
+        return {0: "none", 1: "tcgen05", 2: "simt", 3: "small"}[lib().tpo_last_gtp_grid_path(self.handle)]
 
 
 _contexts: dict[int, Context] = {}

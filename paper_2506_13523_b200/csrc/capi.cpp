@@ -238,8 +238,25 @@ bool run_dense_split(tpo_ctx* ctx, int fourier, int L1, int L2, int L3, const Ro
   return true;
 }
 
+// L1 = L2 = 1 with L3 = 2: the small-degree SIMT kernel beats the 128-row tcgen05 pipeline
+// (13.6 vs 19.6 us per 65,536, profiles/r02/grid_small.txt); grid_path "auto" only
+bool run_small(tpo_ctx* ctx, int fourier, int L1, int L2, int L3, const RowSpec& rs, cudaStream_t s) {
+  Context& c = ctx->impl;
+  static const bool on = [] {
+    const char* v = std::getenv("TPO_GTP_SMALL");
+    return !(v && *v == '0');
+  }();
+  if (!on || c.grid_path != 0) return false;
+  const tpo_b200::GtpSmallOps* o = c.gtp_small(fourier, L1, L2, L3);
+  if (!o) return false;
+  c.last_grid_path = 3;
+  launched(ctx, tpo_b200::launch_gtp_small(*o, rs, c.num_sms(), s), fourier ? "gtp_fourier small kernel" : "gtp_grid small kernel");
+  return true;
+}
+
 void run_grid(tpo_ctx* ctx, int L1, int L2, int L3, const RowSpec& rs, cudaStream_t s) {
   Context& c = ctx->impl;
+  if (run_small(ctx, 0, L1, L2, L3, rs, s)) return;
   if (c.grid_path != 2) {
     const auto& e = c.grid_tc(L1, L2, L3);
     if (e.fits) {
@@ -259,6 +276,7 @@ void run_grid(tpo_ctx* ctx, int L1, int L2, int L3, const RowSpec& rs, cudaStrea
 // fits (Din <= 128), else the SIMT direct-convolution kernel
 void run_fourier(tpo_ctx* ctx, int L1, int L2, int L3, const RowSpec& rs, cudaStream_t s) {
   Context& c = ctx->impl;
+  if (run_small(ctx, 1, L1, L2, L3, rs, s)) return;
   if (c.grid_path != 2) {
     const auto& e = c.fourier_tc(L1, L2, L3);
     if (e.fits) {

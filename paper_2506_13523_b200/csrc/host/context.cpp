@@ -644,6 +644,34 @@ namespace {
 DenseOps make_fourier_ops(int L1, int L2, int L3);
 }  // namespace
 
+const GtpSmallOps* Context::gtp_small(int fourier, int L1, int L2, int L3) {
+  std::lock_guard<std::mutex> g(mu_);
+  const std::array<int, 4> key{fourier, L1, L2, L3};
+  auto it = gtp_small_.find(key);
+  if (it == gtp_small_.end()) {
+    SmallEntry e;
+    if (L1 == L2 && L3 == L1 + L2 && L1 <= 1) {
+      const DenseOps ops = fourier ? make_fourier_ops(L1, L2, L3) : make_grid_ops(L1, L2, L3);
+      if (ops.same_s && gtp_small_supported(ops.din1, ops.G, ops.dout_eff)) {
+        e.s.assign(ops.s1.begin(), ops.s1.end());
+        e.a.assign(ops.a.begin(), ops.a.end());
+        e.o.din = ops.din1;
+        e.o.G = ops.G;
+        e.o.dout_eff = ops.dout_eff;
+        e.o.dout_total = ops.dout_total;
+        e.ok = true;
+      }
+      if (std::getenv("TPO_VERBOSE"))
+        std::fprintf(stderr, "[tpo] gtp small %s L=%d: din=%d G=%d dout=%d same_s=%d -> %s\n", fourier ? "fourier" : "grid",
+                     L1, ops.din1, ops.G, ops.dout_eff, static_cast<int>(ops.same_s), e.ok ? "simt" : "tcgen05");
+    }
+    it = gtp_small_.emplace(key, std::move(e)).first;
+    it->second.o.s = it->second.s.data();
+    it->second.o.a = it->second.a.data();
+  }
+  return it->second.ok ? &it->second.o : nullptr;
+}
+
 // Forward GTP (grid or Fourier) with inputs wider than the kernel's K limit: the
 // product is bilinear, so it is the sum over degree groups (x degrees [a1, b1],
 // y degrees [a2, b2]) of the same operators restricted to those columns.

@@ -65,6 +65,8 @@ class Context {
   // backward: grad_out degrees [a, b] x tower L2 -> tower Lo, smallest exact grid
   const GridTcEntry& grid_tc_part(int a, int b, int L2, int Lo);
   const GridTcEntry& fourier_tc(int L1, int L2, int L3);  // Fourier GTP as torus-grid dense operators
+  // small-degree SIMT operators (gtp_small.cu); nullptr when the shape has no instantiation
+  const GtpSmallOps* gtp_small(int fourier, int L1, int L2, int L3);
   const GridSimtTables& grid_simt(int L1, int L2, int L3);
   const FourierDevTables& fourier(int L1, int L2, int L3);
   const MtpDevTables& mtp(int L1, int L2, int L3, int lt);
@@ -114,6 +116,12 @@ class Context {
   std::map<std::array<int, 2>, std::pair<bool, CgtpTcTables>> cgtp_tc_;
   std::map<std::array<int, 2>, std::pair<bool, CgtpBwdTcTables>> cgtp_bwd_tc_;
   std::map<std::array<int, 4>, GridTcEntry> grid_tc_;
+  struct SmallEntry {
+    bool ok = false;
+    GtpSmallOps o;
+    std::vector<float> s, a;
+  };
+  std::map<std::array<int, 4>, SmallEntry> gtp_small_;
   std::map<std::array<int, 4>, GridTcEntry> grid_tc_part_;
   std::map<std::array<int, 8>, GridTcEntry> dense_split_;
   std::map<std::array<int, 4>, GridTcEntry> fourier_tc_;

@@ -122,6 +122,17 @@ cudaError_t launch_cgtp_bwd_tc(const CgtpBwdTcTables& t, const float* x, const f
                                const CUtensorMap& tm_g, float* gx, float* gy, int64_t rows, int num_sms,
                                cudaStream_t s);
 
+// Grid / Fourier GTP at small degree on SIMT (gtp_small.cu): the dense operators of the tcgen05
+// kernel (out = A ((S x) .* (S y)), L1 = L2, same S) as fp32 host arrays, copied into the kernel's
+// parameter space per launch.  Shapes: gtp_small_supported.
+struct GtpSmallOps {
+  int din = 0, G = 0, dout_eff = 0, dout_total = 0;
+  const float* s = nullptr;  // host [G][din]
+  const float* a = nullptr;  // host [dout_eff][G]
+};
+bool gtp_small_supported(int din, int G, int dout);
+cudaError_t launch_gtp_small(const GtpSmallOps& o, const RowSpec& rs, int num_sms, cudaStream_t s);
+
 // ---------------------------------------------------------------- GTP grid, tcgen05
 // Dense operators of the reference's product grid, pre-split into fp16 hi/lo
 // and pre-tiled on the host in the UMMA canonical K-major layout, one

@@ -103,9 +103,45 @@ def test_gtp_bench_config_exact(tpo, orc):
     worst = {}
     for L in range(1, 11):
         err, used = _run_big(tpo, orc, "gtp_grid", L, 65536, 20240901 + L)
-        assert used == "tcgen05"
+        assert used == ("small" if L == 1 else "tcgen05")
         worst[L] = err
     assert max(worst.values()) <= TOL, worst
+
+
+@pytest.mark.parametrize("kind", ["gtp_grid", "gtp_fourier"])
+@pytest.mark.parametrize("L", [1])
+def test_gtp_small_degree_simt(tpo, orc, kind, L):
+    # L1 = L2 = 1, L3 = 2 runs on the small-degree SIMT kernel (gtp_small.cu) in "auto" mode:
+    # several tiles per block, ragged tail
+    err, used = _run_big(tpo, orc, kind, L, BIG, 9600 + L + (100 if kind == "gtp_fourier" else 0))
+    assert used == "small"
+    assert err <= TOL, (kind, L, err)
+
+
+@pytest.mark.parametrize("kind", ["gtp_grid", "gtp_fourier"])
+def test_gtp_small_shared_y_matches_tcgen05(tpo, kind):
+    # shared y (one per batch entry across channels) and L3 < 2L shapes: the small kernel against
+    # the tcgen05 kernel (both oracle-checked above) on the same inputs
+    import torch
+
+    ctx = tpo.context()
+    g = torch.Generator(device="cuda")
+    g.manual_seed(77)
+    L, B, C = 1, 333, 7
+    x = torch.randn((B, C, (L + 1) ** 2), generator=g, device="cuda")
+    y = torch.randn((B, (L + 1) ** 2), generator=g, device="cuda")
+    a = tpo.run(kind, x, y, L, L, 2 * L)
+    assert ctx.last_grid_path == "small"
+    ctx.set_grid_path("tc")
+    try:
+        b = tpo.run(kind, x, y, L, L, 2 * L)
+        assert ctx.last_grid_path == "tcgen05"
+    finally:
+        ctx.set_grid_path("auto")
+    err = float(_normwise_rows(a.cpu().numpy(), b.double().cpu().numpy()).max())
+    assert err <= 2 * TOL, err
+    tpo.run(kind, x, y, L, L, 3)  # L3 != 2L: not a small-kernel shape
+    assert ctx.last_grid_path == "tcgen05"
 
 
 @pytest.mark.parametrize("L", [15, 16])
