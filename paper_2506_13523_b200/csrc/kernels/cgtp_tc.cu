@@ -58,7 +58,7 @@ __device__ unsigned long long* g_cgtp_prof = nullptr;
 
 template <bool PROF>
 __global__ void __launch_bounds__(kThreads, 1)
-    cgtp_tc_kernel(const __grid_constant__ CgtpTcTables t, const __grid_constant__ RowSpec rs, int dbg) {
+    cgtp_tc_kernel(const __grid_constant__ CgtpTcTables t, const __grid_constant__ RowSpec rs) {
   extern __shared__ __align__(128) uint8_t smem[];  // used directly: accesses stay in the shared space
   __shared__ __align__(8) uint64_t bars[kBars];
   __shared__ uint32_t tmem_sh;
@@ -151,9 +151,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t b0 = smem_u32(ring_b + sb * t.b_stage_bytes);
           const uint64_t bh = make_sdesc(b0, lbo_b, 128), bl = make_sdesc(b0 + half_b, lbo_b, 128);
           const uint32_t dc = tmem + static_cast<uint32_t>(kDCols) * d + dcol;
-          if (el && !(dbg & 4)) mma_f16_ts(dc, ah, bh, id, ks > 0 ? 1u : 0u);
-          if (el && !(dbg & 4)) mma_f16_ts(dc, ah, bl, id, 1u);
-          if (el && !(dbg & 4)) mma_f16_ts(dc, al, bh, id, 1u);
+          if (el) mma_f16_ts(dc, ah, bh, id, ks > 0 ? 1u : 0u);
+          if (el) mma_f16_ts(dc, ah, bl, id, 1u);
+          if (el) mma_f16_ts(dc, al, bh, id, 1u);
           if (el) tc_commit(&bars[B_BE + sb]);
           if (j == kKps - 1 || ks + 1 == un.ksteps) {
             if (el) tc_commit(&bars[B_AE + sa]);
@@ -261,7 +261,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             uint32_t hw[4], lw[4];
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
-              const float p0 = (dbg & 2) ? xv : xv * yp[2 * q], p1 = (dbg & 2) ? xv : xv * yp[2 * q + 1];
+              const float p0 = xv * yp[2 * q], p1 = xv * yp[2 * q + 1];
               const __half2 hh = __floats2half2_rn(p0, p1);
               const float2 hf = __half22float2(hh);
               hw[q] = *reinterpret_cast<const uint32_t*>(&hh);
@@ -327,7 +327,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           while (um < u1 && (t.units[um].dcol_last & 0xFFFF) + t.units[um].n_pad <= c) ++um;
           const CgtpTcUnit un = t.units[um];
           const int col = c - (un.dcol_last & 0xFFFF);
-          if (c < ncols && col < un.n_valid && !(dbg & 1)) {
+          if (c < ncols && col < un.n_valid) {
             float* op = rs.out + row0 * stride + un.out_off + col;
             const float* sp = st + lane;
 #pragma unroll 8
@@ -369,11 +369,7 @@ cudaError_t launch_cgtp_tc(const CgtpTcTables& t, const RowSpec& rs, int num_sms
     cudaMemset(buf, 0, sizeof(unsigned long long) * kProfSlots * grid);
     cudaMemcpyToSymbol(g_cgtp_prof, &buf, sizeof(buf));
   }
-  static const int dbg = [] {
-    const char* v = std::getenv("TPO_CGTP_DBG");  // timing experiments only: 1 no output stores, 2 no
-    return v ? std::atoi(v) : 0;                   // y loads in the builders, 4 no MMAs
-  }();
-  kern<<<grid, kThreads, t.smem_bytes, s>>>(t, rs, dbg);
+  kern<<<grid, kThreads, t.smem_bytes, s>>>(t, rs);
   e = cudaGetLastError();
   if (prof && e == cudaSuccess) {
     std::vector<unsigned long long> h(kProfSlots * grid);

@@ -65,7 +65,7 @@ __device__ __forceinline__ void cp_async4(float* dst, const float* src) {
 
 template <int R, bool DB>  // DB: double-buffered inputs, the next tile's staged during this one
 __global__ void __launch_bounds__(kThreads, 1)
-    mtp_kernel(const __grid_constant__ MtpDevTables t, const __grid_constant__ RowSpec rs, int dbg) {
+    mtp_kernel(const __grid_constant__ MtpDevTables t, const __grid_constant__ RowSpec rs) {
   extern __shared__ float4 sm4[];
   constexpr int G = R / 4;              // float4 groups per element
   constexpr int EP = G > 1 ? G + 1 : 1;  // element pitch in float4: +1 spreads elements over the banks
@@ -116,7 +116,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     // ---- embed (proj/src/mtp.cpp:20-58): X[a][b] = sum_e c_e x[idx_e], Y likewise.  An item is a
     // cell of X or Y for all R products: each term (coalesced across the warp) feeds R FMAs
-    for (int item = tid; item < ((dbg & 1) ? 0 : 2 * dt2); item += kThreads) {
+    for (int item = tid; item < 2 * dt2; item += kThreads) {
       const bool second = item >= dt2;
       const int cell = second ? item - dt2 : item;
       float4 acc[G];
@@ -139,7 +139,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int q = 0; q < 4; ++q)
 #pragma unroll
       for (int p = 0; p < 4; ++p) acc[q][p] = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (has && !(dbg & 2)) {
+    if (has) {
       for (int k = 0; k < dt; ++k) {
         float4 a[4], b[4];
 #pragma unroll
@@ -167,7 +167,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ---- extract (proj/src/mtp.cpp:60-97): out[o] = sum_e c_e Z[cell_e]; zero past the carrier band.
     // item = (output coefficient o, product half g) = 2 o + g
     constexpr int NX = G >= 2 ? G / 2 : 1;  // float4 groups per extract item (R = 4: one item per output)
-    for (int item = tid; item < ((dbg & 4) ? 0 : 2 * t.dout_total); item += kThreads) {
+    for (int item = tid; item < 2 * t.dout_total; item += kThreads) {
       if (G == 1 && (item & 1)) continue;
       const int o = item >> 1, g0 = (item & 1) * NX;
       float4 acc4[NX];
@@ -205,11 +205,7 @@ cudaError_t launch_r(const MtpDevTables& t, const RowSpec& rs, int num_sms, cuda
   if (e != cudaSuccess) return e;
   const int64_t ntiles = (rs.rows + R - 1) / R;
   const int grid = static_cast<int>(std::min<int64_t>(ntiles, num_sms));
-  static const int dbg = [] {
-    const char* v = std::getenv("TPO_MTP_DBG");  // timing experiments only: 1 no embed, 2 no matmul, 4 no extract
-    return v ? std::atoi(v) : 0;
-  }();
-  kern<<<grid, kThreads, smem, s>>>(t, rs, dbg);
+  kern<<<grid, kThreads, smem, s>>>(t, rs);
   return cudaGetLastError();
 }
 
