@@ -242,10 +242,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         const float* xs = row + t.din2;
         const float* ys = row + un.l2 * un.l2;
-        // chunk c (8 products: x index c / cpr, y offset 8 (c % cpr)); cpr <= 3 for l2 <= 11
-        const int cdiv = cpr == 1 ? 0 : (cpr == 2 ? 1 : (cpr == 3 ? 2 : 3));
-        int c = h;
-        for (int ks0 = 0; ks0 < un.ksteps; ks0 += kKps, c += 2 * kKps) {  // one A stage = kKps K-steps
+        // chunk c = h + 2 k of this thread (8 products: x index m1 = c / cpr, y offset 8 (c % cpr)),
+        // advanced incrementally: every K-step moves c by 2
+        int m1 = cpr == 1 ? h : 0, rem = cpr == 1 ? 0 : h;
+        for (int ks0 = 0; ks0 < un.ksteps; ks0 += kKps) {  // one A stage = kKps K-steps
           const long long t0 = now();
           if (na++ >= kAStagesTmem) {
             mbar_wait(&bars[B_AE + sa], pa ^ 1);
@@ -254,10 +254,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           tick(8, t0);
 #pragma unroll
           for (int j = 0; j < kKps; ++j) {  // (tail sub-steps past the unit are built but never issued)
-            const int cc = c + 2 * j;
-            const int m1 = cdiv == 0 ? cc : (cdiv == 1 ? cc >> 1 : (cdiv == 2 ? (cc * 0xAAAB) >> 17 : cc / cpr));
             const float xv = m1 < n1 ? xs[m1] : 0.f;
-            const float* yp = ys + 8 * (cc - m1 * cpr);
+            const float* yp = ys + 8 * rem;
             uint32_t hw[4], lw[4];
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
@@ -271,6 +269,15 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t col = kARing + 32u * sa + 16u * j + 4u * h;
             tmem_st4(lbw + col, hw);
             tmem_st4(lbw + col + 8u, lw);
+            rem += 2;  // next chunk of this thread: c + 2
+            if (rem >= cpr) {
+              rem -= cpr;
+              ++m1;
+            }
+            if (rem >= cpr) {
+              rem -= cpr;
+              ++m1;
+            }
           }
           const long long tf = now();
           tmem_wait_st();
