@@ -1078,7 +1078,7 @@ const CgtpTcTables* Context::cgtp_tc(int L1, int L2) {
 // CGTP backward blocks (cgtp_bwd_tc.cu): the transposed block W^T[k][o] with k unpadded,
 // k = (m1 + l1)(2 l2 + 1) + m2 + l2, o in the forward's path order.  The kernel keeps the row's
 // x | y and grad_x | grad_y in shared memory beside the grad_out and W^T rings, which bounds it to
-// din1 + din2 <= 98 (L <= 6); shapes whose blocks fit one accumulator hand-off per tile (L1 + L2 <= 4
+// din1 + din2 <= 128 (L <= 7); shapes whose blocks fit one accumulator hand-off per tile (L1 + L2 <= 4
 // or so) are faster on the SIMT kernel.
 const CgtpBwdTcTables* Context::cgtp_bwd_tc(int L1, int L2) {
   const char* env = std::getenv("TPO_CGTP_BWD_TC");  // "0": the SIMT kernel (A/B and tests; read per call)
@@ -1090,7 +1090,7 @@ const CgtpBwdTcTables* Context::cgtp_bwd_tc(int L1, int L2) {
     cgtp_bwd_tc_.emplace(std::array<int, 2>{L1, L2}, std::make_pair(false, CgtpBwdTcTables{}));
     return nullptr;
   };
-  if (L1 > 6 || L2 > 6) return fail();
+  if (L1 > 7 || L2 > 7) return fail();
   CgtpBwdTcTables t{};
   t.din1 = (L1 + 1) * (L1 + 1);
   t.din2 = (L2 + 1) * (L2 + 1);
@@ -1108,8 +1108,8 @@ const CgtpBwdTcTables* Context::cgtp_bwd_tc(int L1, int L2) {
           W[static_cast<size_t>(o0 + e.m3 + l3) * n + (e.m1 + l1) * n2 + (e.m2 + l2)] += e.v;
         o0 += 2 * l3 + 1;
       }
-      const int npad_all = pad_to(n, 16), parts = (npad_all + 191) / 192;
-      const int np = pad_to((n + parts - 1) / parts, 16);
+      // N parts of <= 192 accumulator columns made of whole rows m1 of Q (k = m1 n2 + m2)
+      const int rpp = std::min(n1, 192 / n2), parts = (n1 + rpp - 1) / rpp;
       for (int p = 0; p < parts; ++p) {
         CgtpBwdTcUnit u{};
         u.l1 = l1;
@@ -1117,8 +1117,10 @@ const CgtpBwdTcTables* Context::cgtp_bwd_tc(int L1, int L2) {
         u.blk = l1 * (L2 + 1) + l2;
         u.g_off = g_off;
         u.n = n;
-        u.k0 = p * np;
-        u.n_valid = std::min(np, n - p * np);
+        u.m1b = p * rpp;
+        u.nrows = std::min(rpp, n1 - p * rpp);
+        u.k0 = u.m1b * n2;
+        u.n_valid = u.nrows * n2;
         u.n_pad = pad_to(u.n_valid, 16);
         u.ksteps = pad_to(n, 16) / 16;
         u.w_off = static_cast<int>(w.size() * 2);
@@ -1157,17 +1159,22 @@ const CgtpBwdTcTables* Context::cgtp_bwd_tc(int L1, int L2) {
   if (superunits < 2) return fail();  // small shapes: the SIMT kernel (cgtp_bwd.cu)
   t.dout = g_off;
   t.nunits = static_cast<int>(units.size());
-  t.nbp = (t.nblocks + 3) & ~3;
+  // grad_out rows are scaled per row; the kernel reads that exponent per block at L <= 6 (nbp copies,
+  // measured faster there) and once per row at L = 7 (shared memory is short)
+  t.nbp = (t.din1 > 49 || t.din2 > 49) ? 4 : (t.nblocks + 3) & ~3;
   t.b_stage_bytes = 64 * max_npad;
   constexpr int kSmemMax = 225 * 1024;
-  // grad_out ring (HBM) and W^T ring (L2): the deepest grad_out ring that leaves >= 4 W^T stages
+  // grad_out ring (HBM) and W^T ring (L2): the W^T ring's depth matters more (measured: L = 6 with
+  // 3 / 5 slots 0.395 ms against 4 / 4 0.43), so the deepest grad_out ring leaving >= 6 W^T stages
   t.g_slots = 3;
   for (int gsl : {8, 4})
-    if (cgtp_bwd_tc_smem(t, 4, gsl) <= kSmemMax) {
+    if ((kSmemMax - cgtp_bwd_tc_smem(t, 0, gsl)) / t.b_stage_bytes >= 6) {
       t.g_slots = gsl;
       break;
     }
+  if (t.din1 > 49 || t.din2 > 49) t.g_slots = 3;  // the L = 7 instantiation (cgtp_bwd_tc.cu WIDE)
   t.b_stages = std::min(8, (kSmemMax - cgtp_bwd_tc_smem(t, 0, t.g_slots)) / t.b_stage_bytes);
+  if (const char* v = std::getenv("TPO_BWD_BSTAGES")) t.b_stages = std::min(t.b_stages, std::atoi(v));  // experiments
   if (t.b_stages < 2) return fail();
   t.units = upload(units);
   t.w = reinterpret_cast<const uint8_t*>(upload(w));

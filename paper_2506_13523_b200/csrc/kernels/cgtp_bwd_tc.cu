@@ -128,7 +128,9 @@ __device__ __forceinline__ void epi_unit(uint32_t cb, int n1, const float* xr, f
     for (int m2 = 0; m2 < N2; ++m2) ar[iy0 + m2] = fmaf(gy[m2], s, ar[iy0 + m2]);
 }
 
-template <int G, bool PROF>  // G: grad_out ring slots (K-steps in flight per builder thread)
+// G: grad_out ring slots; WIDE: blocks with 2 l2 + 1 = 15 (L = 7; a separate instantiation keeps the
+// L <= 6 epilogue free of the wider register arrays)
+template <int G, bool PROF, bool WIDE>
 __global__ void __launch_bounds__(kThreads, 1)
     cgtp_bwd_tc_kernel(const __grid_constant__ CgtpBwdTcTables t, const float* __restrict__ x,
                        const float* __restrict__ y, const int8_t* __restrict__ eg, float* __restrict__ gx, float* __restrict__ gy, int64_t rows) {
@@ -299,7 +301,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         *reinterpret_cast<int*>(es + b) = ok ? __ldg(reinterpret_cast<const int*>(eg + row * nbp + b)) : 0;
       for (int u = 0; u < t.nunits; ++u) {
         const CgtpBwdTcUnit un = t.units[u];
-        const float sc = pow2i(-static_cast<int>(es[un.blk]));
+        const float sc = pow2i(-static_cast<int>(es[WIDE ? 0 : un.blk]));  // (one exponent per row)
         const int shift = (qb * t.dout + un.g_off) & 3;  // block start inside this box's aligned window
         for (int ks0 = 0; ks0 < un.ksteps; ks0 += kKps) {
           if (na++ >= kAStagesTmem) {
@@ -405,9 +407,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t dbase = lb + static_cast<uint32_t>(kDCols) * d;
         for (int u = u0; u <= u1; ++u) {
           const CgtpBwdTcUnit un = t.units[u];
-          const int n1 = 2 * un.l1 + 1, n2 = 2 * un.l2 + 1;
-          const int ix0 = un.l1 * un.l1, iy0 = t.din1 + un.l2 * un.l2;
-          const float s = pow2i(static_cast<int>(es[un.blk]) - kTabShift);
+          // the unit covers rows m1 = m1b .. m1b + nrows of Q (N parts of whole rows at L = 7; one
+          // part, all 2 l1 + 1 rows, below)
+          const int n2 = 2 * un.l2 + 1, n1 = WIDE ? un.nrows : 2 * un.l1 + 1;
+          const int ix0 = un.l1 * un.l1 + (WIDE ? un.m1b : 0), iy0 = t.din1 + un.l2 * un.l2;
+          const float s = pow2i(static_cast<int>(es[WIDE ? 0 : un.blk]) - kTabShift);
           const uint32_t cb = dbase + (un.dcol_last & 0xFFFF);
           switch (n2) {  // warp-uniform
 #define TPO_EPI(N2)                                                    \
@@ -419,6 +423,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     break;
             TPO_EPI(1) TPO_EPI(3) TPO_EPI(5) TPO_EPI(7) TPO_EPI(9) TPO_EPI(11)
             default:
+              if constexpr (WIDE) {
+                if (n2 == 15) {
+                  if (eh == 0)
+                    epi_unit<15, true>(cb, n1, xr, ar, ix0, iy0, s);
+                  else
+                    epi_unit<15, false>(cb, n1, xr, ar, ix0, iy0, s);
+                  break;
+                }
+              }
               TPO_EPI(13)
 #undef TPO_EPI
           }
@@ -460,9 +473,11 @@ cudaError_t launch_cgtp_bwd_tc(const CgtpBwdTcTables& t, const float* x, const f
     const char* v = std::getenv("TPO_CGTP_BWD_PROF");  // timing experiments only
     return v && *v == '1';
   }();
-  auto kern = t.g_slots == 8   ? (prof ? cgtp_bwd_tc_kernel<8, true> : cgtp_bwd_tc_kernel<8, false>)
-              : t.g_slots == 4 ? (prof ? cgtp_bwd_tc_kernel<4, true> : cgtp_bwd_tc_kernel<4, false>)
-                               : (prof ? cgtp_bwd_tc_kernel<3, true> : cgtp_bwd_tc_kernel<3, false>);
+  const bool wide = t.din1 > 49 || t.din2 > 49;  // L = 7 (always three grad_out slots there)
+  auto kern = wide                 ? cgtp_bwd_tc_kernel<3, false, true>
+              : t.g_slots == 8     ? cgtp_bwd_tc_kernel<8, false, false>
+              : t.g_slots == 4     ? (prof ? cgtp_bwd_tc_kernel<4, true, false> : cgtp_bwd_tc_kernel<4, false, false>)
+                                   : cgtp_bwd_tc_kernel<3, false, false>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, t.smem_bytes);
   if (e != cudaSuccess) return e;
   int8_t* eg = nullptr;

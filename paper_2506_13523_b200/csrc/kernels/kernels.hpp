@@ -108,6 +108,7 @@ cudaError_t launch_cgtp_tc(const CgtpTcTables& t, const RowSpec& rs, int num_sms
 struct CgtpBwdTcUnit {
   int l1, l2, blk, g_off, n, k0, n_valid, n_pad, ksteps, w_off;
   int dcol_last;  // as CgtpTcUnit
+  int m1b, nrows;  // the part's rows m1 of Q: [m1b, m1b + nrows) (k0 = m1b n2, n_valid = nrows n2)
 };
 struct CgtpBwdTcTables {
   int din1, din2, dout, nunits, nblocks, nbp;  // nbp: nblocks rounded up to 4 (exponent rows)
