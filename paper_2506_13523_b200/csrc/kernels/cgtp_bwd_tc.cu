@@ -297,11 +297,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       const bool ok = row < rows;
       int8_t* es = eslot + (it & 1) * BM * nbp + r * nbp;
       if (it >= 2) timed(7, [&] { mbar_wait_s(&bars[B_EF + (it & 1)], ((it >> 1) - 1) & 1); });  // epilogue done with the slot
-      for (int b = 0; b < nbp; b += 4)  // both threads of the row store the same bytes: each reads its own
-        *reinterpret_cast<int*>(es + b) = ok ? __ldg(reinterpret_cast<const int*>(eg + row * nbp + b)) : 0;
+      // the row's exponent (grad_out rows are scaled per row): a register here, a shared copy for the
+      // epilogue written by one of the row's two threads
+      const float sc = pow2i(ok ? -static_cast<int>(__ldg(eg + row * nbp)) : 0);
+      if (h == 0)
+        for (int b = 0; b < nbp; b += 4)
+          *reinterpret_cast<int*>(es + b) = ok ? __ldg(reinterpret_cast<const int*>(eg + row * nbp + b)) : 0;
       for (int u = 0; u < t.nunits; ++u) {
         const CgtpBwdTcUnit un = t.units[u];
-        const float sc = pow2i(-static_cast<int>(es[WIDE ? 0 : un.blk]));  // (one exponent per row)
         const int shift = (qb * t.dout + un.g_off) & 3;  // block start inside this box's aligned window
         for (int ks0 = 0; ks0 < un.ksteps; ks0 += kKps) {
           if (na++ >= kAStagesTmem) {

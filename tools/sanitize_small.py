@@ -47,5 +47,22 @@ x = torch.randn((3, 64, 16), generator=g, device=dev)
 y = torch.randn((3, 16), generator=g, device=dev)
 go = torch.randn((3, 64, 256), generator=g, device=dev)
 tpo.backward("cgtp", x, y, go, 3, 3, 6, need_y=False)
+# round 2: CGTP backward on tcgen05 (L = 4 / 6 / 7 N parts; ragged tails < 4 rows take SIMT), MTP
+# SIMT past dt = 13 (double-buffered staging, interleaved terms), the L = 1 small GTP kernel
+for L, B in ((4, 131), (6, 66), (7, 40)):
+    d = (L + 1) ** 2
+    x = torch.randn((B, d), generator=g, device=dev)
+    y = torch.randn((B, d), generator=g, device=dev)
+    go = torch.randn((B, d * d), generator=g, device=dev)
+    tpo.backward("cgtp", x, y, go, L, L)
+for L, B in ((7, 70), (9, 33)):
+    d = (L + 1) ** 2
+    x = torch.randn((B, d), generator=g, device=dev)
+    y = torch.randn((B, d), generator=g, device=dev)
+    tpo.mtp(x, y, L, L, 2 * L)
+for kind in ("gtp_grid", "gtp_fourier"):
+    x = torch.randn((3, 70, 4), generator=g, device=dev)
+    y = torch.randn((3, 4), generator=g, device=dev)
+    tpo.run(kind, x, y, 1, 1, 2)
 torch.cuda.synchronize()
 print("sanitize run done")
