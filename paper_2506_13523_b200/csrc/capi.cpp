@@ -249,6 +249,7 @@ bool run_small(tpo_ctx* ctx, int fourier, int L1, int L2, int L3, const RowSpec&
   if (!on || c.grid_path != 0) return false;
   const tpo_b200::GtpSmallOps* o = c.gtp_small(fourier, L1, L2, L3);
   if (!o) return false;
+
   c.last_grid_path = 3;
   launched(ctx, tpo_b200::launch_gtp_small(*o, rs, c.num_sms(), s), fourier ? "gtp_fourier small kernel" : "gtp_grid small kernel");
   return true;
@@ -718,7 +719,7 @@ void run_host_requests(tpo_ctx* ctx, const tpo_host_request* reqs, int n) {
   std::vector<Plan> plan(static_cast<size_t>(n));
   static const int64_t chunk_bytes = [] {
     const char* v = std::getenv("TPO_HOST_CHUNK_KB");
-    return (v && *v) ? std::atoll(v) * 1024 : (16ll << 20);  // measured best: 8-16 MiB (tools/e2e_chunks.py)
+    return (v && *v) ? std::atoll(v) * 1024 : (32ll << 20);  // batch of the c2 sweep: 16 MiB 10.18 ms, 32 MiB 9.72 (tools/e2e_batch.py)
   }();
   size_t need_x = 1, need_y = 1, need_z = 1;
   for (int i = 0; i < n; ++i) {
