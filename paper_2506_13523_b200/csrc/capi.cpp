@@ -1042,7 +1042,7 @@ int tpo_apply_linear_f32(tpo_ctx* ctx, const int* in_mul, const int* in_l, int n
     ctx->impl.activate();
     if (dout == 0 || batch == 0) return;
     std::vector<float> f(mt.begin(), mt.end());
-    float* dm = ctx->impl.scratch(11, f.size());
+    float* dm = ctx->impl.scratch(Context::kScratchMisc, f.size());
     tpo_b200::cuda_check(cudaMemcpyAsync(dm, f.data(), f.size() * 4, cudaMemcpyHostToDevice, static_cast<cudaStream_t>(stream)),
              "linear weights");
     tpo_b200::cuda_check(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)), "linear weights");

@@ -85,6 +85,7 @@ class Context {
   cudaStream_t host_stream() const { return host_stream_; }
   // pipelined host-buffer path: copy-in / copy-out streams and per-buffer events
   static constexpr int kPipeBufs = 3;
+  static constexpr int kScratchMisc = 3 * kPipeBufs;
   cudaStream_t h2d_stream() const { return h2d_stream_; }
   cudaStream_t d2h_stream() const { return d2h_stream_; }
   cudaEvent_t pipe_event(int which, int buf) const { return pipe_ev_[which][buf]; }
@@ -134,8 +135,9 @@ class Context {
   std::map<std::string, const float*> dense_ops_;
   std::map<std::string, const int*> int_tables_;
   std::map<int, WignerTables> wigner_;
-  std::array<void*, 12> scratch_{};
-  std::array<size_t, 12> scratch_cap_{};
+  // slots 0 .. 3 kPipeBufs - 1: the host pipeline's x / y / out buffers; kScratchMisc: other uses
+  std::array<void*, 3 * kPipeBufs + 1> scratch_{};
+  std::array<size_t, 3 * kPipeBufs + 1> scratch_cap_{};
 };
 
 }  // namespace tpo_b200
