@@ -994,8 +994,15 @@ const CgtpTcTables* Context::cgtp_tc(int L1, int L2) {
   std::vector<CgtpTcUnit> units;
   std::vector<uint16_t> w;
   int out_off = 0, max_npad = 16;
-  t.xy_pitch = (t.din2 + 33 + 8) | 1;  // y row | x_{l1} (kXSeg; reads may run 7 past a y segment)
-  const int xy_bytes = 128 * t.xy_pitch * 4;
+  // large y rows (din2 >= TPO_CGTP_YSEG_MIN, default 196: L2 >= 13) are staged per block instead of per
+  // row: the freed shared memory buys 192-column parts and a deeper W ring (cgtp_tc.cu t.yseg)
+  static const int yseg_min = [] {
+    const char* v = std::getenv("TPO_CGTP_YSEG_MIN");
+    return v ? std::atoi(v) : 196;
+  }();
+  t.yseg = t.din2 >= yseg_min ? 1 : 0;
+  t.xy_pitch = t.yseg ? (33 + 8) | 1 : (t.din2 + 33 + 8) | 1;  // [y row |] x_{l1} (reads may run 7 past a y segment)
+  const int xy_bytes = 128 * t.xy_pitch * 4 + (t.yseg ? 3 * 128 * 41 * 4 : 0);
   const int budget = 186 * 1024 - xy_bytes;  // the kernel's static staging takes ~35 KB
   int part_cols = 192;
   while (part_cols > 32 && budget / (64 * part_cols) < 2) part_cols -= 32;

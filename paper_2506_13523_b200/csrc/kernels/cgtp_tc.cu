@@ -41,6 +41,8 @@ constexpr int kDCols = 192;  // TMEM: two accumulators [0, 192), [192, 384) ...
 constexpr int kARing = 384;  // ... and the A ring [384, 512): stage sa, K-step j: hi at 32 sa + 16 j, lo + 8
 constexpr int kAStagesTmem = 4;
 constexpr int kXSeg = 33;  // staged x_{l1} segment: 2 l1 + 1 <= 33 (l1 <= 16)
+constexpr int kYSeg = 40;  // staged y_{l2} segment (t.yseg): 2 l2 + 1 <= 33, read up to 8 cpr <= 40
+constexpr int kYSegPitch = kYSeg + 1;
 // barriers: A full [8], A empty [8], B full [8], B empty [8], D full [2], D empty [2]
 constexpr int B_AF = 0, B_AE = 8, B_BF = 16, B_BE = 24, B_DF = 32, B_DE = 34, kBars = 36;
 
@@ -70,6 +72,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int64_t ntiles = (rs.rows + BM - 1) / BM;
   uint8_t* ring_b = smem + t.off_b;
   float* rowbuf = reinterpret_cast<float*>(smem + t.off_xy);  // [128][pitch]: y row | x_{l1} (odd pitch)
+  float* yseg = rowbuf + BM * t.xy_pitch;  // t.yseg: [3][128][kYSegPitch] y_{l2} segments by block sequence
 
   if (tid == 0) {
     for (int i = 0; i < kMaxStages; ++i) {
@@ -192,7 +195,19 @@ __global__ void __launch_bounds__(kThreads, 1)
       const float* xr = rs.x + (ok ? g : 0) * t.din1;
       const long long ts0 = now();
       named_bar_sync(1, 2 * BM);  // both halves are done with the previous tile's row
-      if (h == 1) {  // stage the y row: every load in flight at once
+      if (h == 1 && t.yseg) {  // y segments are staged per block below: only the row scale here
+        const float* yr = rs.y + (rs.y_shared ? g / rs.channels : g) * t.din2;
+        float m0 = 0.f, m1 = 0.f, m2 = 0.f, m3 = 0.f;
+        if (ok) {
+          int k = 0;
+          for (; k + 4 <= t.din2; k += 4) {
+            m0 = fmaxf(m0, fabsf(__ldg(yr + k))); m1 = fmaxf(m1, fabsf(__ldg(yr + k + 1)));
+            m2 = fmaxf(m2, fabsf(__ldg(yr + k + 2))); m3 = fmaxf(m3, fabsf(__ldg(yr + k + 3)));
+          }
+          for (; k < t.din2; ++k) m0 = fmaxf(m0, fabsf(__ldg(yr + k)));
+        }
+        ey_sh[r] = row_scale_exp(fmaxf(fmaxf(m0, m1), fmaxf(m2, m3)), 1) - kInShift;
+      } else if (h == 1) {  // stage the y row: every load in flight at once
         if (ok) {
           const float* yr = rs.y + (rs.y_shared ? g / rs.channels : g) * t.din2;
           for (int k = 0; k < t.din2; ++k) cp_async4(row + k, yr + k);
@@ -226,22 +241,53 @@ __global__ void __launch_bounds__(kThreads, 1)
       named_bar_sync(1, 2 * BM);
       const int ex = ex_sh[r];
       if (h == 0) e_sh[it & 1][r] = ex + ey_sh[r] - kTabShift;  // W is stored times 2^kTabShift
-      const float sx = pow2i(-ex);
+      // with per-block y segments the raw y values are staged and y's scale rides on x
+      const float sx = t.yseg ? pow2i(-ex - ey_sh[r]) : pow2i(-ex);
       tick(7, ts0);
       int cur_l1 = -1;
+      // per-block y segments (t.yseg, large din2): the h = 1 thread of each row copies the segment
+      // of the next block with cp.async while this block is built (zero-filled past 2 l2 + 1), three
+      // buffers by block sequence: the one refilled was last read two blocks ago
+      const float* yrow = rs.y + (ok ? (rs.y_shared ? g / rs.channels : g) : 0) * t.din2;
+      auto stage_seg = [&](int uu, int buf) {
+        if (h == 1 && uu < t.nunits) {
+          const int l2 = t.units[uu].l2, n2 = 2 * l2 + 1;
+          float* dst = yseg + (buf * BM + r) * kYSegPitch;
+          for (int j = 0; j < kYSeg; ++j) {
+            const bool v = ok && j < n2;
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(smem_u32(dst + j)),
+                         "l"(yrow + (v ? l2 * l2 + j : 0)), "r"(v ? 4 : 0)
+                         : "memory");
+          }
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+      };
+      int bs = -1;  // block sequence number inside the tile (t.yseg)
+      if (t.yseg) {
+        named_bar_sync(1, 2 * BM);  // both halves are past the previous tile's segments
+        stage_seg(0, 0);
+      }
       for (int u = 0; u < t.nunits; ++u) {
         const CgtpTcUnit un = t.units[u];
         const int n1 = 2 * un.l1 + 1, n2p = (2 * un.l2 + 1 + 7) & ~7, cpr = n2p >> 3;
+        if (t.yseg && (u == 0 || t.units[u - 1].l2 != un.l2 || t.units[u - 1].l1 != un.l1)) {
+          ++bs;
+          int nu = u + 1;  // first unit of the next block
+          while (nu < t.nunits && t.units[nu].l1 == un.l1 && t.units[nu].l2 == un.l2) ++nu;
+          stage_seg(nu, (bs + 1) % 3);
+          asm volatile("cp.async.wait_group 1;" ::: "memory");  // this block's segment landed
+          named_bar_sync(1, 2 * BM);                              // ... in every row
+        }
         if (un.l1 != cur_l1) {  // restage x_{l1} (both halves are past the previous block)
           named_bar_sync(1, 2 * BM);
           if (h == 0)
             for (int j = 0; j < kXSeg; ++j)  // zeros past n1: y reads may run into this segment (times 0 in W)
-              row[t.din2 + j] = (ok && j < n1) ? __ldg(xr + un.l1 * un.l1 + j) * sx : 0.f;
+              row[(t.yseg ? 0 : t.din2) + j] = (ok && j < n1) ? __ldg(xr + un.l1 * un.l1 + j) * sx : 0.f;
           named_bar_sync(1, 2 * BM);
           cur_l1 = un.l1;
         }
-        const float* xs = row + t.din2;
-        const float* ys = row + un.l2 * un.l2;
+        const float* xs = row + (t.yseg ? 0 : t.din2);
+        const float* ys = t.yseg ? yseg + ((bs % 3) * BM + r) * kYSegPitch : row + un.l2 * un.l2;
         // chunk c = h + 2 k of this thread (8 products: x index m1 = c / cpr, y offset 8 (c % cpr)),
         // advanced incrementally: every K-step moves c by 2
         int m1 = cpr == 1 ? h : 0, rem = cpr == 1 ? 0 : h;

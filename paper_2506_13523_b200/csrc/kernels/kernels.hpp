@@ -96,6 +96,7 @@ struct CgtpTcTables {
   int din1, din2, dout, nunits;
   int a_stages, b_stages, b_stage_bytes, smem_bytes;
   int off_a, off_b, off_xy, xy_pitch;  // xy: per-row staging [128][xy_pitch], x row | y row
+  int yseg;  // 1: y staged per block ([3][128][41] after xy) instead of the whole row (large din2)
   const CgtpTcUnit* units;
   const uint8_t* w;
 };
