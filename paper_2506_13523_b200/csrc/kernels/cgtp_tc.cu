@@ -33,7 +33,8 @@ using namespace sm100;
 namespace {
 
 constexpr int BM = 128;
-constexpr int kThreads = 576;  // 18 warps
+constexpr int kThreads = 608;  // 19 warps
+constexpr int kWarps = kThreads / 32;
 constexpr int kMaxStages = 8;
 constexpr int kStageStride = 33;  // epilogue staging row pitch (32-column blocks)
 constexpr int kKps = 2;      // K-steps per A stage
@@ -102,15 +103,19 @@ __global__ void __launch_bounds__(kThreads, 1)
   };
   const long long t_begin = clock64();
 
-  if (warp == 0) {
-    // ============================================= W ring producer
+  if (warp == 0 || warp == kWarps - 1) {
+    // ============================================= W ring producers
+    // two issuing threads in different warps take alternate ring stages: one thread's bulk-copy
+    // issue (~250 cycles per copy) would limit the W stream at large L
     if (lane == 0) {
+      const int pid = warp == 0 ? 0 : 1;
       int nb = 0;
       for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x)
         for (int u = 0; u < t.nunits; ++u) {
           const CgtpTcUnit un = t.units[u];
           const uint32_t bytes = 64u * un.n_pad;
           for (int ks = 0; ks < un.ksteps; ++ks, ++nb) {
+            if ((nb & 1) != pid) continue;
             const int s = nb % t.b_stages;
             const long long t0 = now();
             if (nb >= t.b_stages) mbar_wait(&bars[B_BE + s], ((nb / t.b_stages) - 1) & 1);
@@ -121,7 +126,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       tick(0, t_begin);
-      if (PROF) for (int k = 0; k < 2; ++k) g_cgtp_prof[blockIdx.x * kProfSlots + k] = pc[k];
+      if (PROF && pid == 0) for (int k = 0; k < 2; ++k) g_cgtp_prof[blockIdx.x * kProfSlots + k] = pc[k];
     }
   } else if (warp == 1) {
     // ============================================= MMA issuer
@@ -339,7 +344,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     tick(6, t_begin);
     if (PROF && pt == 0) for (int k : {6, 7, 8, 11}) g_cgtp_prof[blockIdx.x * kProfSlots + k] = pc[k];
-  } else {
+  } else if (warp < kWarps - 1) {
     // ============================================= epilogue (thread = TMEM lane)
     const int q = warp & 3, eh = (warp - 10) >> 2;  // lane quarter, which of its two warps
     const uint32_t lb = tmem + (static_cast<uint32_t>(q * 32) << 16);
