@@ -365,6 +365,22 @@ def mtp_extract(Z, l_tilde: int, degrees):
     return out
 
 
+def linear_gtp(x, y, L1: int, L2: int, L3: int, wx, wy, wout):
+    """Schur-consistent linear layers around the grid GTP, fused:
+    apply_linear(gtp(apply_linear(x, wx), apply_linear(y, wy)), wout) for tower -> tower layers
+    (one copy per degree).  Such a layer connects only equal degrees, one weight per degree
+    (proj/src/irreps.cpp:95-104), so it is a per-degree scaling and the whole composition is
+    weighted_gtp: one launch of the tcgen05 kernel with the weights folded into its input
+    conversion and epilogue.  wx, wy, wout: LinearLayer weight vectors of lengths L1+1, L2+1, L3+1
+    (linear_connections order)."""
+    import numpy as np
+
+    wx, wy, wout = (np.asarray(w, dtype=np.float64) for w in (wx, wy, wout))
+    if len(wx) != L1 + 1 or len(wy) != L2 + 1 or len(wout) != L3 + 1:
+        raise ValueError("linear_gtp: tower layers take one weight per degree (L+1 each)")
+    return weighted_gtp(x, y, wx, wy, wout, L1, L2, L3)
+
+
 def linear_connections(in_irreps, out_irreps):
     """LinearLayer connections (proj/src/irreps.cpp:95-104): one weight per (input copy, output
     copy) of equal degree, in (input entry, input copy, output entry, output copy) order.  irreps are

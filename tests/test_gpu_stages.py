@@ -260,3 +260,30 @@ def test_cgtp_per_path_weights(tpo, orc, L, C, shared, per_edge):
         [(a, b, c) for a in range(L + 1) for b in range(L + 1) for c in range(abs(a - b), a + b + 1)])])
     wb = (w[:, None, pcol] if per_edge else w[None, None, pcol]).astype(np.float64)
     assert _rel(out, ref * wb) <= TOL
+
+
+@pytest.mark.parametrize("L", [3, 6])
+def test_linear_gtp_fused_equals_composition(tpo, L):
+    # f1: LinearLayer (towers) -> grid GTP -> LinearLayer, fused into one launch, against the three
+    # separate GPU stages (apply_linear, run, apply_linear)
+    import torch
+
+    rng = np.random.default_rng(300 + L)
+    B = 777
+    x = torch.from_numpy(rng.standard_normal((B, (L + 1) ** 2)).astype(np.float32)).cuda()
+    y = torch.from_numpy(rng.standard_normal((B, (L + 1) ** 2)).astype(np.float32)).cuda()
+    tower_in = [(1, l) for l in range(L + 1)]
+    tower_out = [(1, l) for l in range(2 * L + 1)]
+    wx, wy, wo = rng.standard_normal(L + 1), rng.standard_normal(L + 1), rng.standard_normal(2 * L + 1)
+    ctx = tpo.context()
+    n0 = ctx.launches
+    fused = tpo.linear_gtp(x, y, L, L, 2 * L, wx, wy, wo)
+    assert ctx.launches - n0 == 1
+    ref = tpo.apply_linear(tpo.run("gtp_grid", tpo.apply_linear(x, tower_in, tower_in, wx),
+                                   tpo.apply_linear(y, tower_in, tower_in, wy), L, L, 2 * L),
+                           tower_out, tower_out, wo)
+    a, b = fused.double().cpu().numpy(), ref.double().cpu().numpy()
+    err = (np.abs(a - b).max(axis=1) / np.maximum(np.abs(b).max(axis=1), 1e-300)).max()
+    assert err <= 2e-5, err
+    with pytest.raises(ValueError):
+        tpo.linear_gtp(x, y, L, L, 2 * L, wx[:-1], wy, wo)
