@@ -538,21 +538,28 @@ bool mtp_vjp_tc(tpo_ctx* ctx, int L1, int L2, int L3, int lt, const float* x, co
   Context& c = ctx->impl;
   const int64_t rows = batch * channels;
   const int Lg = std::min(L3, 2 * lt);
-  std::vector<std::pair<int, int>> groups;
-  for (int a = 0; a <= Lg;) {
-    int b = a;
-    while (b + 1 <= Lg && (b + 2) * (b + 2) - a * a <= 64) ++b;
-    groups.push_back({a, b});
-    a = b + 1;
-  }
   // (input-2 degree, output degree, flags) per requested gradient
   struct Job { const float* other; int Lo, Lr, flags; float* res; int shared; };
   std::vector<Job> jobs;
   if (gx) jobs.push_back({y, L2, L1, 2, gx, shared});
   if (gy) jobs.push_back({x, L1, L2, 1 | 4, gy, 0});
-  for (const Job& j : jobs)
-    for (const auto& gr : groups)
-      if (!c.mtp_tc(gr.second, j.Lo, j.Lr, lt, gr.first, j.flags)) return false;
+  // grad_out degree windows as wide as the embed GEMM takes them (112 columns where the kernel's
+  // shared memory allows, else 64): fewer launches, gathers and partial accumulations
+  std::vector<std::pair<int, int>> groups;
+  for (int kmax : {112, 64}) {
+    groups.clear();
+    for (int a = 0; a <= Lg;) {
+      int b = a;
+      while (b + 1 <= Lg && (b + 2) * (b + 2) - a * a <= kmax) ++b;
+      groups.push_back({a, b});
+      a = b + 1;
+    }
+    bool ok = true;
+    for (const Job& j : jobs)
+      for (const auto& gr : groups) ok = ok && c.mtp_tc(gr.second, j.Lo, j.Lr, lt, gr.first, j.flags) != nullptr;
+    if (ok) break;
+    if (kmax == 64) return false;
+  }
   const int64_t dg = static_cast<int64_t>(L3 + 1) * (L3 + 1);
   const bool direct = groups.size() == 1 && Lg == L3;
   float* win = nullptr;

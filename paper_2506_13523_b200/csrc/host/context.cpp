@@ -1225,7 +1225,7 @@ const MtpTcTables* Context::mtp_tc(int L1, int L2, int L3, int lt, int a1, int f
   t.n2 = pad_to(t.dout_eff, 16);
   t.k1 = pad_to(t.din1, 16);
   t.k2 = pad_to(t.din2, 16);
-  if (t.k1 > 64 || t.k2 > 64) return fail();
+  if (t.k1 > 112 || t.k2 > 64) return fail();  // input 1 wider than 64: backward windows of grad_out
   // per-row matmul split by carrier rows between the two warps of a TMEM lane quarter:
   // Z group 0 = rows i < i1, group 1 (+ tail group 2) = rows i >= i1, cells (i - i0) * dt + j
   const int i1 = (dt + 1) / 2;

@@ -342,10 +342,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     auto stage_rows = [&](int64_t tile, bool is_y) {
       const int din = is_y ? t.din2 : t.din1;
       float* dst = is_y ? sty : stx;
-      constexpr int kRB = 16;
+      constexpr int kRB = 8, kC = 4;  // din <= 128 (backward windows of grad_out up to 112 columns)
 #pragma unroll 1
       for (int r0 = 0; r0 < 32; r0 += kRB) {
-        float v[kRB][2];
+        float v[kRB][kC];
 #pragma unroll
         for (int rr = 0; rr < kRB; ++rr) {
           const int64_t g = tile * BM + q * 32 + r0 + rr;
@@ -353,7 +353,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const float* src = is_y ? rs.y + (ok ? (rs.y_shared ? g / rs.channels : g) : 0) * t.din2
                                   : rs.x + (ok ? g : 0) * t.din1;
 #pragma unroll
-          for (int c = 0; c < 2; ++c) {
+          for (int c = 0; c < kC; ++c) {
             const int k = lane + 32 * c;
             v[rr][c] = (ok && k < din) ? __ldg(src + k) : 0.f;
           }
@@ -361,7 +361,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int rr = 0; rr < kRB; ++rr)
 #pragma unroll
-          for (int c = 0; c < 2; ++c) {
+          for (int c = 0; c < kC; ++c) {
             const int k = lane + 32 * c;
             if (k < din) dst[(q * 32 + r0 + rr) * din + k] = v[rr][c];
           }
