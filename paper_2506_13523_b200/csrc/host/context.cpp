@@ -1097,8 +1097,9 @@ const CgtpBwdTcTables* Context::cgtp_bwd_tc(int L1, int L2) {
     cgtp_bwd_tc_.emplace(std::array<int, 2>{L1, L2}, std::make_pair(false, CgtpBwdTcTables{}));
     return nullptr;
   };
-  if (L1 > 7 || L2 > 7) return fail();
+  if (L1 > 8 || L2 > 8) return fail();
   CgtpBwdTcTables t{};
+  t.one_sided = (L1 > 7 || L2 > 7) ? 1 : 0;
   t.din1 = (L1 + 1) * (L1 + 1);
   t.din2 = (L2 + 1) * (L2 + 1);
   t.nblocks = (L1 + 1) * (L2 + 1);
@@ -1187,7 +1188,7 @@ const CgtpBwdTcTables* Context::cgtp_bwd_tc(int L1, int L2) {
   t.w = reinterpret_cast<const uint8_t*>(upload(w));
   t.off_b = 0;
   t.off_xy = t.b_stages * t.b_stage_bytes;
-  t.off_g = t.off_xy + 2 * 128 * ((t.din1 + t.din2) | 1) * 4;
+  t.off_g = t.off_xy + 128 * (((t.din1 + t.din2) | 1) + (t.one_sided ? std::max(t.din1, t.din2) | 1 : (t.din1 + t.din2) | 1)) * 4;
   t.smem_bytes = cgtp_bwd_tc_smem(t, t.b_stages, t.g_slots);
   if (std::getenv("TPO_VERBOSE"))
     std::fprintf(stderr, "[tpo] cgtp bwd tcgen05 L=(%d,%d) units=%d super=%d b_stages=%d g_slots=%d smem=%d\n", L1, L2,

@@ -94,10 +94,11 @@ constexpr int kProfSlots = 16;
 
 // One block's share of the row's gradients from its Q columns in TMEM (k = m1 N2 + m2, from column
 // cb): grad_x[ix0 + m1] += s sum_m2 Q y[iy0 + m2] (GX) or grad_y[iy0 + m2] += s sum_m1 Q x[ix0 + m1].
-// A 16-column load covers 16 / N2 rows m1 of Q.
+// A 16-column load covers 16 / N2 rows m1 of Q (two loads per row past 16 columns).
 template <int N2, bool GX>
 __device__ __forceinline__ void epi_unit(uint32_t cb, int n1, const float* xr, float* ar, int ix0, int iy0, float s) {
-  constexpr int RPL = 16 / N2;
+  constexpr int NL = N2 > 16 ? 2 : 1;             // 16-column TMEM loads per step
+  constexpr int RPL = N2 > 16 ? 1 : 16 / N2;      // rows m1 of Q per step
   float yv[N2], gy[N2];
 #pragma unroll
   for (int m2 = 0; m2 < N2; ++m2) {
@@ -105,8 +106,9 @@ __device__ __forceinline__ void epi_unit(uint32_t cb, int n1, const float* xr, f
     gy[m2] = 0.f;
   }
   for (int m0 = 0; m0 < n1; m0 += RPL) {
-    uint32_t v[16];
-    tmem_ld16(cb + m0 * N2, v);  // columns past the block are read and ignored
+    uint32_t v[16 * NL];
+    tmem_ld16(cb + m0 * N2, *reinterpret_cast<uint32_t(*)[16]>(v));  // columns past the block: ignored
+    if (NL == 2) tmem_ld16(cb + m0 * N2 + 16, *reinterpret_cast<uint32_t(*)[16]>(v + 16 * (NL - 1)));
     tmem_wait_ld();
 #pragma unroll
     for (int j = 0; j < RPL; ++j) {
@@ -130,7 +132,9 @@ __device__ __forceinline__ void epi_unit(uint32_t cb, int n1, const float* xr, f
 
 // G: grad_out ring slots; WIDE: blocks with 2 l2 + 1 = 15 (L = 7; a separate instantiation keeps the
 // L <= 6 epilogue free of the wider register arrays)
-template <int G, bool PROF, bool WIDE>
+// SIDE: 0 both gradients; 1 grad_x only, 2 grad_y only (L = 8: the row's accumulator then holds one
+// side, and one launch per gradient reads grad_out)
+template <int G, bool PROF, bool WIDE, int SIDE = 0>
 __global__ void __launch_bounds__(kThreads, 1)
     cgtp_bwd_tc_kernel(const __grid_constant__ CgtpBwdTcTables t, const float* __restrict__ x,
                        const float* __restrict__ y, const int8_t* __restrict__ eg, float* __restrict__ gx, float* __restrict__ gy, int64_t rows) {
@@ -144,7 +148,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int nbp = t.nbp;
   uint8_t* ring_b = smem + t.off_b;
   float* rowbuf = reinterpret_cast<float*>(smem + t.off_xy);     // [128][pitch] x | y of the row
-  float* acc = rowbuf + BM * pitch;                                // [128][pitch] grad_x | grad_y
+  const int apitch = SIDE == 0 ? pitch : (SIDE == 1 ? t.din1 : t.din2) | 1;
+  float* acc = rowbuf + BM * pitch;                                // [128][apitch] grad_x | grad_y
   float* gring = reinterpret_cast<float*>(smem + t.off_g + ((128u - (smem_u32(smem + t.off_g) & 127u)) & 127u));
   // ^ [G][4][32][36] floats, 128B aligned (the host reserves the slack)
   int8_t* eslot = reinterpret_cast<int8_t*>(gring + G * kGSlotBox);  // [2][128][nbp]
@@ -382,7 +387,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int rt = 4 * lane + q;  // tile row of TMEM lane r (see the builders)
     const uint32_t lb = tmem + (static_cast<uint32_t>(q * 32) << 16);
     float* xr = rowbuf + r * pitch;  // x row | y row (true values)
-    float* ar = acc + r * pitch;     // grad_x | grad_y of the row
+    // grad_x | grad_y of the row (one-sided: grad_y indices din1 + .. land at the row's start)
+    float* ar = acc + r * apitch - (SIDE == 2 ? t.din1 : 0);
+    const bool active = SIDE == 0 || (SIDE == 1) == (eh == 0);  // this warp's side is computed
     int gs = 0, it = 0;
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
       const int64_t row = tile * BM + rt;
@@ -396,8 +403,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         } else {
           for (int k = 0; k < dxy; ++k) xr[k] = 0.f;
         }
-        for (int k = 0; k < t.din1; ++k) ar[k] = 0.f;
-      } else {
+        if (active)
+          for (int k = 0; k < t.din1; ++k) ar[k] = 0.f;
+      } else if (active) {
         for (int k = t.din1; k < dxy; ++k) ar[k] = 0.f;
       }
       named_bar_sync(2 + q, 64);  // the row's x / y staged
@@ -416,6 +424,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int ix0 = un.l1 * un.l1 + (WIDE ? un.m1b : 0), iy0 = t.din1 + un.l2 * un.l2;
           const float s = pow2i(static_cast<int>(es[WIDE ? 0 : un.blk]) - kTabShift);
           const uint32_t cb = dbase + (un.dcol_last & 0xFFFF);
+          if (!active) continue;
           switch (n2) {  // warp-uniform
 #define TPO_EPI(N2)                                                    \
   case N2:                                                             \
@@ -434,6 +443,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                     epi_unit<15, false>(cb, n1, xr, ar, ix0, iy0, s);
                   break;
                 }
+                if (n2 == 17) {
+                  if (eh == 0)
+                    epi_unit<17, true>(cb, n1, xr, ar, ix0, iy0, s);
+                  else
+                    epi_unit<17, false>(cb, n1, xr, ar, ix0, iy0, s);
+                  break;
+                }
               }
               TPO_EPI(13)
 #undef TPO_EPI
@@ -444,7 +460,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         u0 = u1 + 1;
       }
       mbar_arrive_warp(&bars[B_EF + (it & 1)]);  // this tile's exponents are no longer read
-      if (ok) {
+      if (ok && active) {
         if (eh == 0 && gx)
           for (int k = 0; k < t.din1; ++k) gx[row * t.din1 + k] = ar[k];
         if (eh == 1 && gy)
@@ -464,7 +480,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 int cgtp_bwd_tc_smem(const CgtpBwdTcTables& t, int b_stages, int g_slots) {
   const int pitch = (t.din1 + t.din2) | 1;
-  const int off_g = b_stages * t.b_stage_bytes + 2 * BM * pitch * 4;
+  const int apitch = t.one_sided ? std::max(t.din1, t.din2) | 1 : pitch;
+  const int off_g = b_stages * t.b_stage_bytes + BM * (pitch + apitch) * 4;
   return off_g + 1024 + g_slots * kGSlotBox * 4 + 2 * BM * t.nbp;
 }
 
@@ -476,13 +493,15 @@ cudaError_t launch_cgtp_bwd_tc(const CgtpBwdTcTables& t, const float* x, const f
     const char* v = std::getenv("TPO_CGTP_BWD_PROF");  // timing experiments only
     return v && *v == '1';
   }();
-  const bool wide = t.din1 > 49 || t.din2 > 49;  // L = 7 (always three grad_out slots there)
+  const bool wide = t.din1 > 49 || t.din2 > 49;  // L >= 7 (always three grad_out slots there)
   auto kern = wide                 ? cgtp_bwd_tc_kernel<3, false, true>
               : t.g_slots == 8     ? cgtp_bwd_tc_kernel<8, false, false>
               : t.g_slots == 4     ? (prof ? cgtp_bwd_tc_kernel<4, true, false> : cgtp_bwd_tc_kernel<4, false, false>)
                                    : cgtp_bwd_tc_kernel<3, false, false>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, t.smem_bytes);
-  if (e != cudaSuccess) return e;
+  auto kx = cgtp_bwd_tc_kernel<3, false, true, 1>, ky = cgtp_bwd_tc_kernel<3, false, true, 2>;
+  cudaError_t e = cudaSuccess;
+  for (auto k : {kern, kx, ky})
+    if ((e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, t.smem_bytes)) != cudaSuccess) return e;
   int8_t* eg = nullptr;
   if ((e = cudaMallocAsync(reinterpret_cast<void**>(&eg), static_cast<size_t>(rows) * t.nbp, s)) != cudaSuccess) return e;
   const int64_t ntiles = (rows + BM - 1) / BM;
@@ -497,7 +516,12 @@ cudaError_t launch_cgtp_bwd_tc(const CgtpBwdTcTables& t, const float* x, const f
   }
   CgtpBwdTcTables tt = t;
   tt.tm_g = tm_g;
-  kern<<<grid, kThreads, t.smem_bytes, s>>>(tt, x, y, eg, gx, gy, rows);
+  if (t.one_sided) {  // one launch per requested gradient (L = 8)
+    if (gx) kx<<<grid, kThreads, t.smem_bytes, s>>>(tt, x, y, eg, gx, nullptr, rows);
+    if (gy) ky<<<grid, kThreads, t.smem_bytes, s>>>(tt, x, y, eg, nullptr, gy, rows);
+  } else {
+    kern<<<grid, kThreads, t.smem_bytes, s>>>(tt, x, y, eg, gx, gy, rows);
+  }
   if (prof) {
     std::vector<unsigned long long> h(static_cast<size_t>(kProfSlots) * grid);
     cudaStreamSynchronize(s);

@@ -114,6 +114,7 @@ struct CgtpBwdTcUnit {
 struct CgtpBwdTcTables {
   int din1, din2, dout, nunits, nblocks, nbp;  // nbp: nblocks rounded up to 4 (exponent rows)
   int b_stages, b_stage_bytes, g_slots, smem_bytes, off_b, off_xy, off_g;
+  int one_sided;  // 1 (L = 8): the row accumulator holds one gradient, one launch per gradient
   const CgtpBwdTcUnit* units;
   const uint8_t* w;
   alignas(64) CUtensorMap tm_g;  // set per call by the launcher

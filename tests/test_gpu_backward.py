@@ -231,10 +231,12 @@ def _cgtp_ref_vjp(orc, L1, L2, x, y, g):
     return gx, gy
 
 
-@pytest.mark.parametrize("L1,L2", [(6, 3), (3, 5), (4, 4), (2, 6), (6, 6), (5, 1), (7, 7), (7, 4), (3, 7)])
+@pytest.mark.parametrize("L1,L2", [(6, 3), (3, 5), (4, 4), (2, 6), (6, 6), (5, 1), (7, 7), (7, 4), (3, 7), (8, 8),
+                                   (8, 5), (4, 8)])
 def test_backward_cgtp_unequal_degrees(tpo, orc, L1, L2):
-    # the tcgen05 block backward (cgtp_bwd_tc.cu) takes L1, L2 <= 7 (blocks wider than 192 columns
-    # in row-aligned N parts at 7); (5, 1) and small shapes stay on the SIMT term-list kernel
+    # the tcgen05 block backward (cgtp_bwd_tc.cu) takes L1, L2 <= 8 (blocks wider than 192 columns
+    # in row-aligned N parts from 7, one launch per gradient at 8); (5, 1) and small shapes stay on
+    # the SIMT term-list kernel
     import torch
 
     rng = np.random.default_rng(17 * L1 + L2)
@@ -249,7 +251,7 @@ def test_backward_cgtp_unequal_degrees(tpo, orc, L1, L2):
     assert _normwise(gy.cpu().numpy().astype(np.float64), ry) <= TOL
 
 
-@pytest.mark.parametrize("L", [3, 4, 5, 6, 7])
+@pytest.mark.parametrize("L", [3, 4, 5, 6, 7, 8])
 def test_backward_cgtp_tc_matches_simt(tpo, monkeypatch, L):
     """Ragged batch (1,000 rows: a partial last tile) with per-row scales over 1e-20 .. 1e20 and
     one-sided requests: the tcgen05 backward against the SIMT term-list kernel (fp32 sums, itself

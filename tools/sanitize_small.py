@@ -49,7 +49,7 @@ go = torch.randn((3, 64, 256), generator=g, device=dev)
 tpo.backward("cgtp", x, y, go, 3, 3, 6, need_y=False)
 # round 2: CGTP backward on tcgen05 (L = 4 / 6 / 7 N parts; ragged tails < 4 rows take SIMT), MTP
 # SIMT past dt = 13 (double-buffered staging, interleaved terms), the L = 1 small GTP kernel
-for L, B in ((4, 131), (6, 66), (7, 40)):
+for L, B in ((4, 131), (6, 66), (7, 40), (8, 36)):
     d = (L + 1) ** 2
     x = torch.randn((B, d), generator=g, device=dev)
     y = torch.randn((B, d), generator=g, device=dev)
