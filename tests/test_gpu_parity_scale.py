@@ -158,6 +158,37 @@ def test_cgtp_blocks_L15(tpo, orc):
     assert err <= TOL, err
 
 
+def test_cgtp_block_y_segments_forced_small_L(tmp_path):
+    # the per-block y staging of the CGTP block kernel (default from L2 = 13) forced down to L = 4..6
+    # (TPO_CGTP_YSEG_MIN is read once per process: a child process), against the oracle
+    import subprocess
+    import sys
+    import textwrap
+
+    code = textwrap.dedent("""
+        import sys, numpy as np, torch
+        sys.path.insert(0, %r); sys.path.insert(0, %r)
+        import paper_2506_13523_b200 as tpo, oracle as orc
+        orc.build()
+        worst = 0.0
+        for L, B in ((4, 300), (5, 131), (6, 77)):
+            g = torch.Generator(device="cuda"); g.manual_seed(70 + L)
+            d = (L + 1) ** 2
+            x = torch.randn((B, d), generator=g, device="cuda"); y = torch.randn((B, d), generator=g, device="cuda")
+            out = tpo.run("cgtp", x, y, L, L, 0).cpu().numpy().astype(np.float64)
+            ref = orc.batch_mimo("cgtp", L, x.cpu().numpy().astype(np.float64)[:, None],
+                                 y.cpu().numpy().astype(np.float64)[:, None])[:, 0]
+            err = (np.abs(out - ref).max(axis=1) / np.maximum(np.abs(ref).max(axis=1), 1e-300)).max()
+            worst = max(worst, float(err))
+        print("WORST", worst)
+    """ % (str(Path(__file__).resolve().parents[1]), str(Path(__file__).resolve().parents[1] / "oracle")))
+    env = dict(__import__("os").environ, TPO_CGTP_YSEG_MIN="16")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    worst = float(r.stdout.strip().split("WORST")[-1])
+    assert worst <= TOL, worst
+
+
 @pytest.mark.parametrize("L", [1, 3, 6, 7, 10])
 def test_mtp_bench_scale(tpo, orc, L):
     err, _ = _run_big(tpo, orc, "mtp", L, BIG, 9400 + L)
