@@ -92,11 +92,31 @@ def load_peaks() -> dict:
 FP32_TFLOPS = 2 * 148 * 128 * 1.965e9 / 1e12  # FFMA peak at max clock (not in MEASURED_PEAKS.json)
 
 
+GTP_SEP_MIN_L = 12  # capi.cpp kGridSepMinL / kFourierSepMinL: the row-quad separable SIMT kernel
+
+
+def gtp_path(kind, L):
+    return "sep" if kind in ("gtp_grid", "gtp_fourier") and L >= GTP_SEP_MIN_L else "tc"
+
+
+def sep_flops_per_tp(kind, L):
+    """FFMA flops of the row-quad separable kernel (gtp_grid_simt.cu) per product, both grid
+    symmetries folded: Legendre synthesis / analysis (din1 + din2 + dout) x node pairs, phi
+    synthesis and analysis nodes x half-period points x (nm1 + nm2 + nm3)."""
+    band = 2 * L
+    nt = band + 1 if kind == "gtp_grid" else 2 * L + 2
+    njp, nkp = (nt + 1) // 2, band + 1
+    fma = (2 * din(L) + dout(kind, L)) * njp + nt * nkp * (2 * (2 * L + 1) + 2 * band + 1)
+    return 2 * fma
+
+
 def roofline_time(kind, L, n, peaks, path="tc"):
     """T_roof per SURVEY.md 8(d): max(bytes / HBM, flops / pipe peak) for n products."""
     t_hbm = bytes_per_tp(kind, L) * n / (peaks["hbm_gbs"] * 1e9)
     if kind in ("gtp_grid", "gtp_fourier") and path == "tc":
         return max(t_hbm, dense_flops_per_tp(kind, L) * n / (peaks["bf16_tflops"] / 3 * 1e12)), "tensor"
+    if kind in ("gtp_grid", "gtp_fourier") and path == "sep":
+        return max(t_hbm, sep_flops_per_tp(kind, L) * n / (FP32_TFLOPS * 1e12)), "fp32"
     return t_hbm, "hbm"
 
 
@@ -536,8 +556,7 @@ def run_ours(args, world, rank, local):
     for (kind, L), ms in per_ms.items():
         n = sum(p[5] for p in probs if (p[0], p[1]) == (kind, L))
         ek = "cgtp" if kind == "cgtp" else kind
-        path = "simt" if (kind == "gtp_grid" and L > 14) or (kind == "gtp_fourier" and L > 16) else "tc"
-        t_roof, bound = roofline_time(ek, L, n, peaks, path)
+        t_roof, bound = roofline_time(ek, L, n, peaks, gtp_path(kind, L))
         if w == "c4":
             t_roof = n // C4_CHANNELS * c4_bytes_per_edge() / (peaks["hbm_gbs"] * 1e9)
             bound = "hbm"
@@ -548,7 +567,7 @@ def run_ours(args, world, rank, local):
     dk, dL = dom
     dn = sum(p[5] for p in probs if (p[0], p[1]) == dom)
     dms = per_ms[dom]
-    if (dk == "gtp_grid" and dL <= 14) or dk == "gtp_fourier":
+    if dk in ("gtp_grid", "gtp_fourier") and gtp_path(dk, dL) == "tc":
         ach = dense_flops_per_tp(dk, dL) * dn / (dms / 1e3) / 1e12
         roofline = {"bound": "tensor", "kernel": f"gtp_grid_tc_kernel {dk} L={dL} (3xFP16 tcgen05)",
                     "achieved": round(ach, 2), "peak": round(peaks["bf16_tflops"] / 3, 1), "unit": "TFLOP/s",
@@ -585,7 +604,7 @@ def run_ours(args, world, rank, local):
         except Exception:
             pass
     step_roof = sum(roofline_time("cgtp" if k == "cgtp" else k, L, sum(p[5] for p in probs if (p[0], p[1]) == (k, L)),
-                                  peaks, "simt" if (k == "gtp_grid" and L > 14) else "tc")[0]
+                                  peaks, gtp_path(k, L))[0]
                     for (k, L) in per_ms) if w != "c4" else None
     if step_roof is not None:
         roofline["step_frac"] = round(step_roof / (ms_per_step / 1e3), 4)

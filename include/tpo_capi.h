@@ -215,10 +215,11 @@ double tpo_mtp_path_weight(int l1, int l2, int l3, int l_tilde);
 int64_t tpo_count_muls(int kind, int impl, int mode, int L);
 
 /* Kernel selection for the two Gaunt products (for tests/bench): 0 auto,
- * 1 force the fused tcgen05 kernel (fails if the shape does not fit: inputs
- * of more than 128 coefficients, i.e. L > 10), 2 force the SIMT kernels
- * (separable grid GTP; direct half-plane spectral convolution for the
- * Fourier GTP).  Returns the previous setting. */
+ * 1 force the tcgen05 kernels (fused, or degree groups up to L = 14; fails
+ * past that), 2 force the SIMT kernels (separable grid GTP; direct half-plane
+ * spectral convolution for the Fourier GTP), 3 force the separable row-quad
+ * kernel (grid: as 2; Fourier: the reference torus folded to theta in [0, pi]).
+ * Returns the previous setting. */
 int tpo_set_gtp_grid_path(tpo_ctx* ctx, int path);
 /* Accumulation precision of the tcgen05 Gaunt products (grid / Fourier).  The tensor pipe rounds
  * its fp32 accumulator toward zero once per MMA, so long accumulation chains are cut into segments
@@ -226,7 +227,8 @@ int tpo_set_gtp_grid_path(tpo_ctx* ctx, int path);
  * error <= 6.8e-6 on adversarial rows at every L; 1 (strict): segments past 20 K-steps for every
  * shape, <= ~4e-6, about 25% slower at L = 8..10.  Returns the previous mode. */
 int tpo_set_precision(tpo_ctx* ctx, int mode);
-/* Which kernel the last GTP-grid / GTP-Fourier call used (1 tc, 2 simt). */
+/* Which kernel the last GTP-grid / GTP-Fourier call used (1 tc, 2 simt, 3 small-degree SIMT,
+ * 4 separable torus kernel for the Fourier GTP). */
 int tpo_last_gtp_grid_path(const tpo_ctx* ctx);
 
 #ifdef __cplusplus

@@ -154,7 +154,7 @@ class Context:
         return int(lib().tpo_ctx_launches(self.handle))
 
     def set_grid_path(self, path: str) -> None:
-        code = {"auto": 0, "tc": 1, "tcgen05": 1, "simt": 2}[path]
+        code = {"auto": 0, "tc": 1, "tcgen05": 1, "simt": 2, "sep": 3}[path]
         r = lib().tpo_set_gtp_grid_path(self.handle, code)
         if r < 0:
             check(-r)
@@ -170,7 +170,7 @@ class Context:
 
     @property
     def last_grid_path(self) -> str:
-        return {0: "none", 1: "tcgen05", 2: "simt", 3: "small"}[lib().tpo_last_gtp_grid_path(self.handle)]
+        return {0: "none", 1: "tcgen05", 2: "simt", 3: "small", 4: "separable"}[lib().tpo_last_gtp_grid_path(self.handle)]
 
 
 _contexts: dict[int, Context] = {}

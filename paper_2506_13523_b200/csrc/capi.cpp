@@ -161,11 +161,20 @@ void run_cgtp(tpo_ctx* ctx, int L1, int L2, const RowSpec& rs, cudaStream_t s, c
 // part does not fit either.
 // Fourier: up to L = 16 (L = 15 / 16 adversarial worst 3.8e-6 / 2.7e-6 after the operand scaling and
 // segmented accumulation; 118 / 155 ms per 2^19 shard against 299 / 503 ms on SIMT, profiles/r02i).
-// Grid: L <= 14 (the SIMT separable path is faster at 15 / 16: 61 / 80 vs 109 / 154 ms).
-const int kMaxSplitL = [] {
-  const char* v = std::getenv("TPO_GRID_SPLIT_MAXL");  // accuracy experiments only
-  return v ? std::atoi(v) : 14;
+// From L = 12 both Gaunt products take the row-quad separable SIMT kernel (grid nodes / the reference
+// torus): per 2^19 products 6.9 / 10.0 / 11.0 / 12.8 / 15.4 ms at L = 12..16 against 8.1 (fused) /
+// 30.8 / 40.1 (degree groups) on tcgen05 for the grid, 7.0 .. 15.4 against 8.3 / 30.2 / 42.0 / 111 /
+// 151 for the Fourier GTP (profiles/r02s); below L = 12 the tcgen05 kernels win (L = 11: 4.1 vs 5.2).
+// grid_path "tc" still takes the degree groups up to L = 14 (grid) / 16 (Fourier).
+const int kGridSepMinL = [] {
+  const char* v = std::getenv("TPO_GRID_SEP_MINL");
+  return v ? std::atoi(v) : 12;
 }();
+const int kFourierSepMinL = [] {
+  const char* v = std::getenv("TPO_FOURIER_SEP_MINL");
+  return v ? std::atoi(v) : 12;
+}();
+constexpr int kMaxSplitL = 14;
 const int kMaxSplitLFourier = [] {
   const char* v = std::getenv("TPO_FOURIER_SPLIT_MAXL");  // accuracy experiments only
   return v ? std::atoi(v) : 16;
@@ -258,14 +267,17 @@ bool run_small(tpo_ctx* ctx, int fourier, int L1, int L2, int L3, const RowSpec&
 void run_grid(tpo_ctx* ctx, int L1, int L2, int L3, const RowSpec& rs, cudaStream_t s) {
   Context& c = ctx->impl;
   if (run_small(ctx, 0, L1, L2, L3, rs, s)) return;
-  if (c.grid_path != 2) {
+  const bool sep_auto = c.grid_path == 0 && std::max(L1, L2) >= kGridSepMinL &&
+                        tpo_b200::gtp_grid_quad_fits(c.grid_simt(L1, L2, L3));
+  if (c.grid_path != 2 && c.grid_path != 3 && !sep_auto) {
     const auto& e = c.grid_tc(L1, L2, L3);
     if (e.fits) {
       c.last_grid_path = 1;
       launched(ctx, tpo_b200::launch_gtp_grid_tc(e.t, rs, c.num_sms(), s), "gtp_grid tcgen05 kernel");
       return;
     }
-    if (std::max(L1, L2) > 12 && std::max(L1, L2) <= kMaxSplitL && run_dense_split(ctx, 0, L1, L2, L3, rs, s)) return;
+    if (std::max(L1, L2) > 12 && std::max(L1, L2) <= kMaxSplitL && run_dense_split(ctx, 0, L1, L2, L3, rs, s))
+      return;
     if (c.grid_path == 1) throw InvalidArgument("gtp_grid: shape does not fit the tcgen05 tiling");
   }
   c.last_grid_path = 2;
@@ -278,6 +290,15 @@ void run_grid(tpo_ctx* ctx, int L1, int L2, int L3, const RowSpec& rs, cudaStrea
 void run_fourier(tpo_ctx* ctx, int L1, int L2, int L3, const RowSpec& rs, cudaStream_t s) {
   Context& c = ctx->impl;
   if (run_small(ctx, 1, L1, L2, L3, rs, s)) return;
+  if (c.grid_path == 3 || (c.grid_path == 0 && std::max(L1, L2) >= kFourierSepMinL)) {
+    const tpo_b200::GridSimtTables* t = c.fourier_sep(L1, L2, L3);
+    if (t && tpo_b200::gtp_grid_quad_fits(*t)) {
+      c.last_grid_path = 4;
+      launched(ctx, tpo_b200::launch_gtp_grid_simt(*t, rs, c.num_sms(), s), "gtp_fourier separable kernel");
+      return;
+    }
+    if (c.grid_path == 3) throw InvalidArgument("gtp_fourier: the separable torus kernel does not take this shape");
+  }
   if (c.grid_path != 2) {
     const auto& e = c.fourier_tc(L1, L2, L3);
     if (e.fits) {
@@ -894,7 +915,7 @@ int tpo_fourier_table(int L, int which, int* counts, int* u, int* v, double* re,
 }
 
 int tpo_set_gtp_grid_path(tpo_ctx* ctx, int path) {
-  if (!ctx || path < 0 || path > 2) return -TPO_EINVAL;
+  if (!ctx || path < 0 || path > 3) return -TPO_EINVAL;
   return ctx->impl.grid_path.exchange(path);
 }
 

@@ -810,6 +810,38 @@ const GridTcEntry& Context::fourier_tc(int L1, int L2, int L3) {
 }
 
 // ------------------------------------------------------------------ GTP grid (SIMT separable)
+namespace {
+int sep_lstride(int nt) { return nt | 1; }
+}  // namespace
+
+// phi half-period tables and Legendre-analysis items of the row-quad separable kernel
+// (gtp_grid_simt.cu) for t.band, t.L3e on an odd azimuth grid of np = 2 band + 1 points
+void Context::fill_sep_tables(GridSimtTables& t, int np) {
+  t.nkp = t.band + 1;
+  t.nkpp = (t.nkp + 3) / 4 * 4;
+  t.mpad = (t.band + 1 + 3) / 4 * 4;
+  std::vector<float> c2c((t.band + 1) * t.nkpp, 0.f), c2s((t.band + 1) * t.nkpp, 0.f), c4c(t.nkp * t.mpad, 0.f),
+      c4s(t.nkp * t.mpad, 0.f);
+  for (int kp = 0; kp < t.nkp; ++kp) {
+    const double phi = 2.0 * M_PI * kp / np;
+    for (int m = 0; m <= t.band; ++m) {
+      c2c[m * t.nkpp + kp] = c4c[kp * t.mpad + m] = static_cast<float>(m == 0 ? 1.0 : std::cos(m * phi));
+      c2s[m * t.nkpp + kp] = static_cast<float>(std::sin(m * phi));
+      if (m < t.band) c4s[kp * t.mpad + m] = static_cast<float>(std::sin((m + 1) * phi));
+    }
+  }
+  t.c2c = upload(c2c);
+  t.c2s = upload(c2s);
+  t.c4c = upload(c4c);
+  t.c4s = upload(c4s);
+  std::vector<int> it5;
+  for (int m = -t.L3e; m <= t.L3e; ++m)
+    for (int l0 = std::abs(m); l0 <= t.L3e; ++l0)
+      if ((l0 - std::abs(m)) % 4 < 2) it5.push_back(l0 | ((m + t.L3e) << 16));
+  t.nitems5 = static_cast<int>(it5.size());
+  t.items5 = upload(it5);
+}
+
 const GridSimtTables& Context::grid_simt(int L1, int L2, int L3) {
   std::lock_guard<std::mutex> g(mu_);
   auto it = grid_simt_.find({L1, L2, L3});
@@ -830,10 +862,136 @@ const GridSimtTables& Context::grid_simt(int L1, int L2, int L3) {
   t.cs = upload(cs);
   t.wq = upload(wq);
   t.out_scale = 1.f;
+  fill_sep_tables(t, gr.n_phi);
+  // signed-order theta tables of the row-quad kernel: Lambda_l|m| for both stages
+  t.lstride = sep_lstride(t.nt);
+  auto strided_lam = [&](int lmax) {
+    std::vector<float> v(static_cast<size_t>(lmax + 1) * (lmax + 2) / 2 * t.lstride, 0.f);
+    for (int r = 0; r < (lmax + 1) * (lmax + 2) / 2; ++r)
+      for (int j = 0; j < t.nt; ++j)
+        v[static_cast<size_t>(r) * t.lstride + j] = static_cast<float>(gr.lam[static_cast<size_t>(r) * t.nt + j]);
+    return upload(v);
+  };
+  t.lam1s = strided_lam(std::max(L1, L2));
+  t.lam5s = strided_lam(t.L3e);
   return grid_simt_.emplace(std::array<int, 3>{L1, L2, L3}, t).first->second;
 }
 
 // ------------------------------------------------------------------ GTP Fourier
+// Fourier GTP on the row-quad separable kernel.  The reference convolves the encoded torus spectra
+// (proj/src/gtp.cpp:262-327) on a torus of N = 4L + 2 points per axis; by the convolution theorem the
+// decoded product is out_o = sum_{a,b<N} h(a, b) A_o(a, b), h = f g the product of the torus
+// functions f(a, phi) = Re sum_{(u,v,w) in enc} x w w_N^(u a) e^(i v phi) and
+// A_o(a, b) = Re sum_{(U,V,w) in dec_o} w w_N^-(U a + V b) / N^2.  Every encode / decode entry of
+// order m has |v| = |m|, so in phi both are single harmonics: f = sum_lm x_lm E_lm(a) trig_m(phi) and
+// A_o(a, .) = D_o(a) trig_m(.) (trig_m = cos m phi for m >= 0, sin |m| phi for m < 0) -- the grid
+// kernel's structure with E in place of Lambda_l|m|(theta_j) and D in place of w_j Lambda.  The phi
+// stages run on the kernel's own odd azimuth grid (np = 2 (L1 + L2) + 1 points, exact for the product
+// band: factor N / np), and the torus rows a > N/2 fold onto N - a (the antipodal extension,
+// proj/src/gtp.cpp:66-74, makes the phi-harmonic m of row N - a (-1)^m times that of row a), leaving
+// H + 1 = 2L + 2 rows theta_a = 2 pi a / N in [0, pi], which pair as a <-> H - a (theta <-> pi - theta)
+// with parity (-1)^(l+m) as the Gauss-Legendre nodes do.  Every identity is checked on the tables
+// (relative 1e-9; tools/fourier_sep_check.py restates the derivation against the oracle) and the
+// builder returns nullptr if one fails.
+const GridSimtTables* Context::fourier_sep(int L1, int L2, int L3) {
+  std::lock_guard<std::mutex> g(mu_);
+  auto it = fourier_sep_.find({L1, L2, L3});
+  if (it != fourier_sep_.end()) return it->second.get();
+  const int L = std::max(L1, L2);
+  const FourierTables& ft = fourier_tables(L);
+  const int N = 4 * L + 2, H = N / 2, nt = H + 1;
+  auto t = std::make_unique<GridSimtTables>();
+  t->L1 = L1;
+  t->L2 = L2;
+  t->band = L1 + L2;
+  t->L3e = std::min(L3, t->band);
+  t->dout_total = (L3 + 1) * (L3 + 1);
+  t->nt = nt;
+  t->np = 2 * t->band + 1;
+  std::vector<std::complex<double>> wn(N);
+  for (int k = 0; k < N; ++k) wn[k] = std::polar(1.0, 2.0 * M_PI * k / N);
+  auto modn = [N](long v) { return static_cast<int>(((v % N) + N) % N); };
+  bool ok = true;
+  double vmax = 0.0, resid = 0.0;
+  // one torus row's harmonic of (l, m): sign +1 encode (e^{+i}), -1 decode (e^{-i}, / N^2)
+  auto harmonic = [&](const std::vector<FourierMode>& modes, int m, int sign, int a) {
+    double cc = 0.0, ss = 0.0;
+    for (const FourierMode& e : modes) {
+      if (std::abs(e.v) != std::abs(m)) ok = false;
+      const std::complex<double> c = e.w * wn[modn(sign * static_cast<long>(e.u) * a)];
+      cc += c.real();
+      const double im = sign > 0 ? -c.imag() : c.imag();  // sin |m| phi coefficient of the v = +|m| entry
+      ss += e.v > 0 ? im : (e.v < 0 ? -im : 0.0);
+    }
+    resid = std::max(resid, std::abs(m >= 0 ? ss : cc));
+    return m >= 0 ? cc : ss;
+  };
+  std::vector<double> E(static_cast<size_t>(L + 1) * (L + 1) * nt), Dq(static_cast<size_t>(t->L3e + 1) * (t->L3e + 1) * nt);
+  for (int k = 0; k < (L + 1) * (L + 1); ++k) {
+    const int l = static_cast<int>(std::sqrt(static_cast<double>(k) + 0.5)), m = k - l * l - l;
+    for (int a = 0; a < nt; ++a) E[static_cast<size_t>(k) * nt + a] = harmonic(ft.enc[k], m, +1, a);
+  }
+  const double inv = 1.0 / (static_cast<double>(N) * N), phi_ratio = static_cast<double>(N) / t->np;
+  std::vector<double> q(N);
+  for (int o = 0; o < (t->L3e + 1) * (t->L3e + 1); ++o) {
+    const int l = static_cast<int>(std::sqrt(static_cast<double>(o) + 0.5)), m = o - l * l - l;
+    for (int a = 0; a < N; ++a) q[a] = harmonic(ft.dec[o], m, -1, a) * inv;
+    const double sg = (std::abs(m) & 1) ? -1.0 : 1.0;
+    for (int a = 0; a < nt; ++a)
+      Dq[static_cast<size_t>(o) * nt + a] = phi_ratio * (q[a] + (a > 0 && a < H ? sg * q[N - a] : 0.0));
+  }
+  // pair parity a <-> H - a
+  double pres = 0.0;
+  auto pair_check = [&](const std::vector<double>& T, int lmax) {
+    for (int k = 0; k < (lmax + 1) * (lmax + 1); ++k) {
+      const int l = static_cast<int>(std::sqrt(static_cast<double>(k) + 0.5)), m = k - l * l - l;
+      const double p = ((l + std::abs(m)) & 1) ? -1.0 : 1.0;
+      for (int a = 0; a < nt; ++a) {
+        const double v = T[static_cast<size_t>(k) * nt + a];
+        vmax = std::max(vmax, std::abs(v));
+        pres = std::max(pres, std::abs(T[static_cast<size_t>(k) * nt + (H - a)] - p * v));
+      }
+    }
+  };
+  double vE = 0.0;
+  pair_check(E, L);
+  vE = vmax;
+  vmax = 0.0;
+  pair_check(Dq, t->L3e);
+  if (!ok || resid > 1e-9 * std::max(vE, vmax) * N || pres > 1e-9 * std::max(vE, vmax) * N) {
+    fourier_sep_.emplace(std::array<int, 3>{L1, L2, L3}, nullptr);
+    return nullptr;
+  }
+  // the kernel indexes both tables by |m| (row l (l + 1) / 2 + |m|): the cos- and sin-type rows of
+  // one degree and |m| must agree
+  t->lstride = sep_lstride(nt);
+  double sres = 0.0;
+  auto strided = [&](const std::vector<double>& T, int lmax) {
+    std::vector<float> v(static_cast<size_t>(lmax + 1) * (lmax + 2) / 2 * t->lstride, 0.f);
+    for (int l = 0; l <= lmax; ++l)
+      for (int ma = 0; ma <= l; ++ma)
+        for (int a = 0; a < nt; ++a) {
+          const double p = T[static_cast<size_t>(l * l + l + ma) * nt + a];
+          sres = std::max(sres, std::abs(p - T[static_cast<size_t>(l * l + l - ma) * nt + a]));
+          v[static_cast<size_t>(l * (l + 1) / 2 + ma) * t->lstride + a] = static_cast<float>(p);
+        }
+    return v;
+  };
+  std::vector<float> Ef = strided(E, L), Df = strided(Dq, t->L3e), wq(nt, 1.f);
+  if (sres > 1e-9 * std::max(vE, vmax) * N) {
+    fourier_sep_.emplace(std::array<int, 3>{L1, L2, L3}, nullptr);
+    return nullptr;
+  }
+  t->lam1s = upload(Ef);
+  t->lam5s = upload(Df);
+  t->wq = upload(wq);
+  t->lam = nullptr;
+  t->cs = nullptr;
+  t->out_scale = 1.f;
+  fill_sep_tables(*t, t->np);
+  return fourier_sep_.emplace(std::array<int, 3>{L1, L2, L3}, std::move(t)).first->second.get();
+}
+
 const FourierDevTables& Context::fourier(int L1, int L2, int L3) {
   std::lock_guard<std::mutex> g(mu_);
   auto it = fourier_.find({L1, L2, L3});

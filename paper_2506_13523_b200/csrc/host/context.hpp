@@ -68,6 +68,9 @@ class Context {
   // small-degree SIMT operators (gtp_small.cu); nullptr when the shape has no instantiation
   const GtpSmallOps* gtp_small(int fourier, int L1, int L2, int L3);
   const GridSimtTables& grid_simt(int L1, int L2, int L3);
+  // Fourier GTP on the row-quad separable kernel (the reference torus folded to theta in [0, pi]);
+  // nullptr when the encode / decode spectra do not separate (never for the reference's tables)
+  const GridSimtTables* fourier_sep(int L1, int L2, int L3);
   const FourierDevTables& fourier(int L1, int L2, int L3);
   const MtpDevTables& mtp(int L1, int L2, int L3, int lt);
   // nullptr: shape not on the tcgen05 path; a1 / flags: backward variants (context.cpp)
@@ -128,6 +131,8 @@ class Context {
   std::map<std::array<int, 4>, GridTcEntry> fourier_tc_;
   GridTcEntry build_dense_tc(const struct DenseOps& ops, const char* label, int max_chain);
   std::map<std::array<int, 3>, GridSimtTables> grid_simt_;
+  std::map<std::array<int, 3>, std::unique_ptr<GridSimtTables>> fourier_sep_;
+  void fill_sep_tables(GridSimtTables& t, int np);
   std::map<std::array<int, 3>, FourierDevTables> fourier_;
   std::map<std::array<int, 4>, MtpDevTables> mtp_;
   std::map<std::array<int, 6>, std::pair<bool, MtpTcTables>> mtp_tc_;

@@ -9,6 +9,7 @@
 // selectable for comparison.  One block per product, persistent over rows;
 // all intermediates live in shared memory.
 #include <algorithm>
+#include <cstdlib>
 
 #include "kernels.hpp"
 
@@ -82,8 +83,289 @@ __global__ void __launch_bounds__(kThreads)
 
 }  // namespace
 
+// ---------------------------------------------------------------- row-quad kernel
+// The same five stages on a block of four products held as float4 (one lane of the vector per
+// product), so every table coefficient and every staged value feeds four products, with both
+// grid symmetries folded in:
+//   phi:   phi_{np-k} = 2 pi - phi_k, so cos(m phi) is even and sin(m phi) odd about k = 0; the
+//          synthesis evaluates E = sum_{m>=0} g_m cos and O = sum_{m<0} g_m sin on the half period
+//          kp = 0..band and gives F(kp) = E + O, F(np - kp) = E - O; the analysis takes
+//          S = P(kp) + P(np - kp) against cos and D = P(kp) - P(np - kp) against sin.
+//   theta: the Gauss-Legendre nodes are symmetric, Lambda_lm(pi - theta) = (-1)^(l+m) Lambda_lm(theta),
+//          so the Legendre synthesis sums even and odd l + m apart and the analysis reads
+//          h(j) + h(j') or h(j) - h(j') by the parity of l + m.
+// Each stage is a register-tiled small GEMM: stage 2 computes 4 half-period points x 4 products per
+// thread for both inputs (32 FMAs per 3 loads), stage 4 a node pair x 4 orders x 4 products, stage 5
+// two degrees of one order.  About half the FMAs of grid_simt_kernel and a fraction of its loads.
+namespace {
+
+constexpr int kQMaxThreads = 320;  // block = the larger of the stage-2 / stage-4 item counts, <= 320
+
+__device__ __forceinline__ float4 f4fma(float4 a, float b, float4 c) {
+  return make_float4(fmaf(a.x, b, c.x), fmaf(a.y, b, c.y), fmaf(a.z, b, c.z), fmaf(a.w, b, c.w));
+}
+__device__ __forceinline__ float4 f4add(float4 a, float4 b) { return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w); }
+__device__ __forceinline__ float4 f4sub(float4 a, float4 b) { return make_float4(a.x - b.x, a.y - b.y, a.z - b.z, a.w - b.w); }
+__device__ __forceinline__ float4 f4mul(float4 a, float4 b) { return make_float4(a.x * b.x, a.y * b.y, a.z * b.z, a.w * b.w); }
+__device__ __forceinline__ float4 f4scale(float4 a, float b) { return make_float4(a.x * b, a.y * b, a.z * b, a.w * b); }
+__device__ __forceinline__ float f4get(float4 v, int i) { return i == 0 ? v.x : (i == 1 ? v.y : (i == 2 ? v.z : v.w)); }
+
+struct QuadLayout {
+  int din1, din2, nm1, nm2, nm3, nt, njp, nkp, dout_e;
+  int regA, regB;  // float4 counts of the two aliased regions
+};
+
+__host__ __device__ inline QuadLayout quad_layout(const GridSimtTables& t) {
+  QuadLayout q;
+  q.din1 = (t.L1 + 1) * (t.L1 + 1);
+  q.din2 = (t.L2 + 1) * (t.L2 + 1);
+  q.nm1 = 2 * t.L1 + 1;
+  q.nm2 = 2 * t.L2 + 1;
+  q.nm3 = 2 * t.L3e + 1;
+  q.nt = t.nt;
+  q.njp = (t.nt + 1) / 2;
+  q.nkp = t.nkp;
+  q.dout_e = (t.L3e + 1) * (t.L3e + 1);
+  const int a1 = (q.nm1 + q.nm2) * q.nt, a2 = 2 * q.nm3 * q.njp;
+  const int b1 = q.din1 + q.din2, b2 = 2 * q.nt * q.nkp, b3 = q.dout_e;
+  q.regA = a1 > a2 ? a1 : a2;
+  q.regB = b1 > b2 ? (b1 > b3 ? b1 : b3) : (b2 > b3 ? b2 : b3);
+  return q;
+}
+
+template <int MAXT>
+__global__ void __launch_bounds__(MAXT, 2)
+    grid_quad_kernel(const __grid_constant__ GridSimtTables t, const __grid_constant__ RowSpec rs) {
+  extern __shared__ float4 sq[];
+  const QuadLayout q = quad_layout(t);
+  const int nt = q.nt, njp = q.njp, nkp = q.nkp, L1 = t.L1, L2 = t.L2, L3e = t.L3e;
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  float4* A = sq;                // g = [nm1 + nm2][nt]         |  H = [2][nm3][njp] (h(j) +- h(j'))
+  float4* B = sq + q.regA;       // xs, ys = [din1], [din2]     |  S, D = [nt][nkp]  |  outs (floats [4][dout_e])
+  float4* gx = A;
+  float4* gy = A + q.nm1 * nt;
+  float4* H = A;
+  float4* xs = B;
+  float4* ys = B + q.din1;
+  float4* S = B;
+  float4* D = B + nt * nkp;
+  float* outs = reinterpret_cast<float*>(B);
+  const int ls = t.lstride;
+  auto lam1 = [&](int l, int ma, int j) { return __ldg(t.lam1s + (l * (l + 1) / 2 + ma) * ls + j); };
+  auto lam5 = [&](int l, int ma, int j) { return __ldg(t.lam5s + (l * (l + 1) / 2 + ma) * ls + j); };
+  const int64_t ntiles = (rs.rows + 3) / 4;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t row0 = tile * 4;
+    const int nr = static_cast<int>(rs.rows - row0 < 4 ? rs.rows - row0 : 4);
+    // 0. stage the four products' inputs, product-minor
+    {
+      float* xf = reinterpret_cast<float*>(xs);
+      float* yf = reinterpret_cast<float*>(ys);
+      for (int i = tid; i < 4 * q.din1; i += nthr) {
+        const int r = i / q.din1, k = i - r * q.din1;
+        xf[k * 4 + r] = r < nr ? __ldg(rs.x + (row0 + r) * q.din1 + k) : 0.f;
+      }
+      for (int i = tid; i < 4 * q.din2; i += nthr) {
+        const int r = i / q.din2, k = i - r * q.din2;
+        const int64_t yr = rs.y_shared ? (row0 + r) / rs.channels : row0 + r;
+        yf[k * 4 + r] = r < nr ? __ldg(rs.y + yr * q.din2 + k) : 0.f;
+      }
+    }
+    __syncthreads();
+    // 1. Legendre synthesis on node pairs (j, nt-1-j): even and odd l + |m| apart
+    for (int i = tid; i < (q.nm1 + q.nm2) * njp; i += nthr) {
+      const int mi = i / njp, jp = i - mi * njp;
+      const bool isx = mi < q.nm1;
+      const int Lx = isx ? L1 : L2, m = (isx ? mi : mi - q.nm1) - Lx, ma = abs(m);
+      const float4* v = isx ? xs : ys;
+      float4 e = make_float4(0.f, 0.f, 0.f, 0.f), o = e;
+      for (int l = ma; l <= Lx; l += 2) {
+        e = f4fma(v[l * l + l + m], lam1(l, ma, jp), e);
+        if (l + 1 <= Lx) o = f4fma(v[(l + 1) * (l + 1) + l + 1 + m], lam1(l + 1, ma, jp), o);
+      }
+      float4* g = (isx ? gx : gy) + (m + Lx) * nt;
+      g[jp] = f4add(e, o);
+      if (nt - 1 - jp != jp) g[nt - 1 - jp] = f4sub(e, o);
+    }
+    __syncthreads();
+    // 2+3. phi synthesis on the half period, product, folded into S / D
+    {
+      const int nkq = t.nkpp / 4;
+      const int Lm = L1 > L2 ? L1 : L2;
+      for (int i = tid; i < nt * nkq; i += nthr) {
+        const int j = i / nkq, kq = i - j * nkq;
+        float4 ex[4], ox[4], ey[4], oy[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) ex[c] = ox[c] = ey[c] = oy[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int m = 0; m <= Lm; ++m) {
+          const float4 cc = __ldg(reinterpret_cast<const float4*>(t.c2c + m * t.nkpp) + kq);
+          if (m <= L1) {
+            const float4 g = gx[(m + L1) * nt + j];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) ex[c] = f4fma(g, f4get(cc, c), ex[c]);
+          }
+          if (m <= L2) {
+            const float4 g = gy[(m + L2) * nt + j];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) ey[c] = f4fma(g, f4get(cc, c), ey[c]);
+          }
+          if (m == 0) continue;
+          const float4 ss = __ldg(reinterpret_cast<const float4*>(t.c2s + m * t.nkpp) + kq);
+          if (m <= L1) {
+            const float4 g = gx[(L1 - m) * nt + j];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) ox[c] = f4fma(g, f4get(ss, c), ox[c]);
+          }
+          if (m <= L2) {
+            const float4 g = gy[(L2 - m) * nt + j];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) oy[c] = f4fma(g, f4get(ss, c), oy[c]);
+          }
+        }
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const int kp = kq * 4 + c;
+          if (kp >= nkp) break;
+          const float4 pp = f4mul(f4add(ex[c], ox[c]), f4add(ey[c], oy[c]));
+          if (kp == 0) {
+            S[j * nkp] = pp;
+            D[j * nkp] = make_float4(0.f, 0.f, 0.f, 0.f);
+          } else {
+            const float4 pm = f4mul(f4sub(ex[c], ox[c]), f4sub(ey[c], oy[c]));
+            S[j * nkp + kp] = f4add(pp, pm);
+            D[j * nkp + kp] = f4sub(pp, pm);
+          }
+        }
+      }
+    }
+    __syncthreads();
+    // 4. phi analysis per node pair and order quad, quadrature weight folded in, stored as h(j) +- h(j')
+    {
+      const int nqc = (L3e + 1 + 3) / 4, nqs = (L3e + 3) / 4;
+      for (int i = tid; i < njp * (nqc + nqs); i += nthr) {
+        const bool sn = i >= njp * nqc;
+        const int ii = sn ? i - njp * nqc : i;
+        const int nq = sn ? nqs : nqc;
+        const int jp = ii / nq, mq = ii - jp * nq, j2 = nt - 1 - jp;
+        const float4* src = sn ? D : S;
+        const float* tab = sn ? t.c4s : t.c4c;
+        float4 a0[4], a1[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) a0[c] = a1[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int kp = sn ? 1 : 0; kp < nkp; ++kp) {
+          const float4 cc = __ldg(reinterpret_cast<const float4*>(tab + kp * t.mpad) + mq);
+          const float4 s0 = src[jp * nkp + kp], s1 = src[j2 * nkp + kp];
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            a0[c] = f4fma(s0, f4get(cc, c), a0[c]);
+            a1[c] = f4fma(s1, f4get(cc, c), a1[c]);
+          }
+        }
+        const float w0 = __ldg(t.wq + jp), w1 = __ldg(t.wq + j2);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const int mabs = sn ? mq * 4 + c + 1 : mq * 4 + c;
+          if (mabs > L3e) break;
+          const int mi = (sn ? -mabs : mabs) + L3e;
+          const float4 h0 = f4scale(a0[c], w0);
+          if (j2 == jp) {
+            H[mi * njp + jp] = h0;
+            H[(q.nm3 + mi) * njp + jp] = make_float4(0.f, 0.f, 0.f, 0.f);
+          } else {
+            const float4 h1 = f4scale(a1[c], w1);
+            H[mi * njp + jp] = f4add(h0, h1);
+            H[(q.nm3 + mi) * njp + jp] = f4sub(h0, h1);
+          }
+        }
+      }
+    }
+    __syncthreads();
+    // 5. Legendre analysis, two degrees of one order and parity per item
+    for (int i = tid; i < t.nitems5; i += nthr) {
+      const int it = __ldg(t.items5 + i);
+      const int l0 = it & 0xffff, mi = it >> 16, m = mi - L3e, ma = abs(m);
+      const int l1 = l0 + 2;
+      const bool two = l1 <= L3e;
+      const float4* h = H + (((l0 + ma) & 1) * q.nm3 + mi) * njp;
+      float4 c0 = make_float4(0.f, 0.f, 0.f, 0.f), c1 = c0;
+      for (int jp = 0; jp < njp; ++jp) {
+        const float4 hv = h[jp];
+        c0 = f4fma(hv, lam5(l0, ma, jp), c0);
+        if (two) c1 = f4fma(hv, lam5(l1, ma, jp), c1);
+      }
+      const int o0 = l0 * l0 + l0 + m;
+      outs[0 * q.dout_e + o0] = c0.x;
+      outs[1 * q.dout_e + o0] = c0.y;
+      outs[2 * q.dout_e + o0] = c0.z;
+      outs[3 * q.dout_e + o0] = c0.w;
+      if (two) {
+        const int o1 = l1 * l1 + l1 + m;
+        outs[0 * q.dout_e + o1] = c1.x;
+        outs[1 * q.dout_e + o1] = c1.y;
+        outs[2 * q.dout_e + o1] = c1.z;
+        outs[3 * q.dout_e + o1] = c1.w;
+      }
+    }
+    __syncthreads();
+    // 6. coalesced store; degrees past the band are exactly zero
+    for (int i = tid; i < nr * t.dout_total; i += nthr) {
+      const int r = i / t.dout_total, o = i - r * t.dout_total;
+      rs.out[row0 * t.dout_total + i] = o < q.dout_e ? outs[r * q.dout_e + o] : 0.f;
+    }
+    __syncthreads();
+  }
+}
+
+size_t quad_smem(const GridSimtTables& t) {
+  const QuadLayout q = quad_layout(t);
+  return sizeof(float4) * static_cast<size_t>(q.regA + q.regB);
+}
+
+// one pass over the two heavy stages' items where it fits: L = 16 has 297 / 289 items, which on 256
+// threads took two passes (18.3 ms per 2^19 against 12.4 at L = 15 with 248 / 256 items)
+int quad_threads(const GridSimtTables& t) {
+  const QuadLayout q = quad_layout(t);
+  const int i2 = q.nt * (t.nkpp / 4), i4 = q.njp * ((t.L3e + 4) / 4 + (t.L3e + 3) / 4);
+  const int n = ((std::max(i2, i4) + 31) / 32) * 32;
+  static const int forced = [] {  // sweeps only
+    const char* v = std::getenv("TPO_QUAD_THREADS");
+    return v ? std::atoi(v) : 0;
+  }();
+  if (forced > 0) return std::max(32, std::min(kQMaxThreads, forced / 32 * 32));
+  return std::max(128, std::min(kQMaxThreads, n));
+}
+
+}  // namespace
+
+bool gtp_grid_quad_fits(const GridSimtTables& t) { return quad_smem(t) <= 220 * 1024; }
+
 cudaError_t launch_gtp_grid_simt(const GridSimtTables& t, const RowSpec& rs, int num_sms, cudaStream_t s) {
   if (rs.rows <= 0) return cudaSuccess;
+  static const bool old = std::getenv("TPO_GRID_SIMT_OLD") != nullptr;  // comparison only
+  const size_t qsm = quad_smem(t);
+  if ((!old || !t.lam) && qsm <= 220 * 1024) {
+    const int nthr = quad_threads(t);
+    static const int variant = [] {  // sweeps only: 256 / 320 forces that register budget
+      const char* v = std::getenv("TPO_QUAD_VARIANT");
+      return v ? std::atoi(v) : 0;
+    }();
+    // register budget by measurement (profiles/r02s/quad_variants2.jsonl): 90 registers (2 x 320
+    // threads) at L <= 12 and 16, 110 (2 x 256) at 224 / 256 threads, i.e. L = 13..15 (-3..8%)
+    const bool big = variant ? variant == 320 : (nthr > 256 || nthr < 224);
+    auto kern = big ? grid_quad_kernel<320> : grid_quad_kernel<256>;
+    if (nthr > 256 && !big) return cudaErrorInvalidValue;
+    if (qsm > 48 * 1024) {
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(qsm));
+      if (e != cudaSuccess) return e;
+    }
+    int occ = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, nthr, qsm);
+    const int64_t ntiles = (rs.rows + 3) / 4;
+    const int grid = static_cast<int>(std::min<int64_t>(ntiles, static_cast<int64_t>(num_sms) * std::max(occ, 1)));
+    kern<<<grid, nthr, qsm, s>>>(t, rs);
+    return cudaGetLastError();
+  }
+  if (!t.lam) return cudaErrorInvalidValue;  // separable Fourier tables: row-quad kernel only
   const int din1 = (t.L1 + 1) * (t.L1 + 1), din2 = (t.L2 + 1) * (t.L2 + 1);
   const size_t smem = sizeof(float) * (din1 + din2 + (2 * t.L1 + 1 + 2 * t.L2 + 1) * t.nt + t.nt * t.np +
                                        (2 * t.L3e + 1) * t.nt);

@@ -197,8 +197,27 @@ struct GridSimtTables {
   const float* cs;    // [2*band+1][np]
   const float* wq;    // [nt] = w_j * 2pi/np
   float out_scale;    // 1
+  // symmetric (row-quad) kernel: phi_{np-k} = 2pi - phi_k and theta_{nt-1-j} = pi - theta_j fold
+  // both transforms in half; tables over the half-period kp = 0..band
+  int nkp, nkpp, mpad;    // band + 1, nkp rounded up to 4, (band + 1) rounded up to 4
+  const float* c2c;       // [band + 1][nkpp]  cos(m phi_kp)     (phi synthesis, m >= 0)
+  const float* c2s;       // [band + 1][nkpp]  sin(m phi_kp)     (phi synthesis, m < 0)
+  const float* c4c;       // [nkp][mpad]       cos(m phi_kp)     (phi analysis, m >= 0)
+  const float* c4s;       // [nkp][mpad]       sin((m+1) phi_kp) (phi analysis, m < 0)
+  const int* items5;      // Legendre analysis items: l0 | (m + L3e) << 16, l1 = l0 + 2 of the same parity
+  int nitems5;
+  // theta tables of the row-quad kernel, row l (l + 1) / 2 + |m| of stride lstride (nt rounded up to
+  // odd: a power-of-two stride cost 35% at nt = 32 in L1 set conflicts): synthesis values at the
+  // nodes (l <= max(L1, L2)) and analysis weights (l <= L3e).  Grid: Lambda_l|m|(theta_j) for both
+  // (w_j in wq); Fourier: the reference torus's encode / decode spectra summed at the torus rows
+  // (Context::fourier_sep).  By |m|: the signed-order tables did not fit in L1 beside the shared
+  // memory at L = 13..15 (+15-20%).
+  const float* lam1s;
+  const float* lam5s;
+  int lstride;
 };
 cudaError_t launch_gtp_grid_simt(const GridSimtTables& t, const RowSpec& rs, int num_sms, cudaStream_t s);
+bool gtp_grid_quad_fits(const GridSimtTables& t);  // the row-quad kernel's shared memory fits
 
 // ---------------------------------------------------------------- GTP Fourier
 // Encode gather lists per spectrum mode (u,v) of the (2L+1)^2 input spectra,

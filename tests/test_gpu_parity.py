@@ -96,6 +96,66 @@ def test_gtp_grid_simt(tpo, orc, L):
         ctx.set_grid_path("auto")
 
 
+@pytest.mark.parametrize("L1,L2,L3,B,C,shared", [
+    (0, 0, 0, 7, None, False),     # band 0: one node, one azimuth
+    (3, 2, 4, 13, None, False),    # odd band: no middle node; truncated output
+    (2, 5, 9, 6, None, False),     # L2 > L1, output past the band (zero degrees)
+    (5, 0, 5, 5, None, False),     # y a scalar
+    (4, 4, 3, 3, 3, True),         # shared y over channels, rows not a multiple of 4
+    (6, 3, 9, 2, 5, False),
+])
+def test_gtp_grid_simt_shapes(tpo, orc, L1, L2, L3, B, C, shared):
+    # the row-quad separable kernel: folded theta / phi symmetries at odd and even bands, ragged
+    # row quads, shared y
+    ctx = tpo.context()
+    ctx.set_grid_path("simt")
+    try:
+        x, y = _inputs(B, L1, L2, 17 * L1 + 5 * L2 + L3, C, shared)
+        out = _gpu(tpo, "gtp_grid", x, y, L1, L2, L3)
+        assert ctx.last_grid_path == "simt"
+    finally:
+        ctx.set_grid_path("auto")
+    xs = x.reshape(-1, x.shape[-1])
+    ys = np.repeat(y, C, axis=0) if shared else y.reshape(-1, y.shape[-1])
+    ref = np.stack([_ref_single(orc, "gtp_grid", xs[i], ys[i], L1, L2, L3) for i in range(xs.shape[0])])
+    assert _normwise(out.reshape(ref.shape), ref) <= TOL
+
+
+@pytest.mark.parametrize("L", [0, 1, 2, 3, 5, 8, 11, 13, 16])
+def test_gtp_fourier_separable(tpo, orc, L):
+    # the reference torus evaluated separably on the row-quad kernel (forced at every L)
+    ctx = tpo.context()
+    ctx.set_grid_path("sep")
+    try:
+        _check_batch(tpo, orc, "gtp_fourier", L, 64 if L > 10 else 203, 250 + L)
+        assert ctx.last_grid_path == "separable"
+    finally:
+        ctx.set_grid_path("auto")
+
+
+@pytest.mark.parametrize("L1,L2,L3,B,C,shared", [
+    (0, 0, 0, 7, None, False),
+    (3, 2, 4, 13, None, False),
+    (2, 5, 9, 6, None, False),
+    (5, 0, 5, 5, None, False),
+    (4, 4, 3, 3, 3, True),
+    (6, 3, 11, 2, 5, False),
+])
+def test_gtp_fourier_separable_shapes(tpo, orc, L1, L2, L3, B, C, shared):
+    ctx = tpo.context()
+    ctx.set_grid_path("sep")
+    try:
+        x, y = _inputs(B, L1, L2, 19 * L1 + 5 * L2 + L3, C, shared)
+        out = _gpu(tpo, "gtp_fourier", x, y, L1, L2, L3)
+        assert ctx.last_grid_path == "separable"
+    finally:
+        ctx.set_grid_path("auto")
+    xs = x.reshape(-1, x.shape[-1])
+    ys = np.repeat(y, C, axis=0) if shared else y.reshape(-1, y.shape[-1])
+    ref = np.stack([_ref_single(orc, "gtp_fourier", xs[i], ys[i], L1, L2, L3) for i in range(xs.shape[0])])
+    assert _normwise(out.reshape(ref.shape), ref) <= TOL
+
+
 @pytest.mark.parametrize("L", [0, 1, 2, 3, 4, 6, 8])
 def test_cgtp(tpo, orc, L):
     _check_batch(tpo, orc, "cgtp", L, 257, 300 + L)

@@ -146,10 +146,20 @@ def test_gtp_small_shared_y_matches_tcgen05(tpo, kind):
 
 @pytest.mark.parametrize("L", [15, 16])
 def test_fourier_degree_groups_high_L(tpo, orc, L):
-    # L = 15, 16 Fourier GTP on tcgen05 degree groups (the SIMT path is 2.5-3x slower there)
-    err, used = _run_big(tpo, orc, "gtp_fourier", L, 148 * 128 // 4 + 77, 9300 + L)
+    # L = 15, 16 Fourier GTP on tcgen05 degree groups (forced; automatic selection takes the
+    # separable torus kernel from L = 13)
+    err, used = _run_big(tpo, orc, "gtp_fourier", L, 148 * 128 // 4 + 77, 9300 + L, path="tc")
     assert used == "tcgen05"
     assert err <= TOL, (L, err)
+
+
+@pytest.mark.parametrize("kind", ["gtp_grid", "gtp_fourier"])
+@pytest.mark.parametrize("L", [12, 13, 14, 15, 16])
+def test_gtp_separable_bench_scale(tpo, orc, kind, L):
+    # the automatic path from L = 12: the row-quad separable kernels (grid nodes / reference torus)
+    err, used = _run_big(tpo, orc, kind, L, 148 * 128 + 77, 9400 + L + (100 if kind == "gtp_fourier" else 0))
+    assert used == ("simt" if kind == "gtp_grid" else "separable")
+    assert err <= TOL, (kind, L, err)
 
 
 def test_cgtp_blocks_L15(tpo, orc):
