@@ -124,7 +124,7 @@ __device__ __forceinline__ int degree_of(int k) { return __float2int_rd(sqrtf(st
 // before the barrier, so no thread overwrites a raw value another thread has yet to read
 template <int KH>
 __device__ __noinline__ void convert_input_regs(const float* raw, const float* wdeg, int din, int kp, int in_shift,
-                                                   uint8_t* dst_hi, uint8_t* dst_lo, float* part, int* e_out, int r,
+                                                   uint8_t* dst_hi, uint8_t* dst_lo, float* part, int16_t* e_out, int r,
                                                    int h, bool wait_free, uint64_t* xy_free, uint32_t xy_free_par) {
   const int kh = kp >> 1;  // multiple of 8
   const int k0 = h * kh;
@@ -186,11 +186,11 @@ __device__ __noinline__ void convert_input_regs(const float* raw, const float* w
       *reinterpret_cast<uint4*>(dst_lo + off) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
     }
   }
-  if (h == 0) e_out[r] = e;
+  e_out[h * BM + r] = static_cast<int16_t>(e);  // one copy per worker half: (r, h) reads its own in the epilogue
 }
 
 __device__ __noinline__ void convert_input(const float* raw, const float* wdeg, int din, int kp, int in_shift,
-                                              uint8_t* dst_hi, uint8_t* dst_lo, float* part, int* e_out, int r, int h,
+                                              uint8_t* dst_hi, uint8_t* dst_lo, float* part, int16_t* e_out, int r, int h,
                                               bool wait_free, uint64_t* xy_free, uint32_t xy_free_par) {
   // two short passes over the staged row (norm, then scale + split): small code, which
   // matters because this runs once per tile and is otherwise cold in the instruction cache
@@ -251,7 +251,7 @@ __device__ __noinline__ void convert_input(const float* raw, const float* wdeg, 
     *reinterpret_cast<uint4*>(dst_hi + off) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
     *reinterpret_cast<uint4*>(dst_lo + off) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
   }
-  if (h == 0) e_out[r] = e;
+  e_out[h * BM + r] = static_cast<int16_t>(e);  // one copy per worker half: (r, h) reads its own in the epilogue
 }
 
 // Optional per-role cycle accounting (PROF = true; debugging aid, env
@@ -283,7 +283,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ __align__(8) uint64_t bars[kNumBars];
   __shared__ uint32_t tmem_sh;
-  __shared__ int ex_sh[2][BM], ey_sh[2][BM];
+  __shared__ int16_t ex_sh[2][2 * BM], ey_sh[2][2 * BM];  // [tile parity][worker half][row] (same bytes as int [2][BM])
   __shared__ float part_sh[2 * BM];
   // weighted GTP: per-column weights (flat (l,m) index -> weight of degree l), filled once
   __shared__ float wtab_x[2 * KH], wtab_y[2 * KH], wtab_c[448];
@@ -661,7 +661,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       ++d;
       const auto te0 = now();
       tc_fence_after();
-      const int e_row = ex_sh[buf][r] + ey_sh[buf][r] - t.a_shift;
+      const int e_row = ex_sh[buf][h * BM + r] + ey_sh[buf][h * BM + r] - t.a_shift;
       const int64_t row0 = my_tile(cu.tile) * BM + q * 32;
       const int col0 = cu.g * t.zg;
       const int col_end = min(col0 + t.zg, t.dout_eff);

@@ -66,3 +66,19 @@ for kind in ("gtp_grid", "gtp_fourier"):
     tpo.run(kind, x, y, 1, 1, 2)
 torch.cuda.synchronize()
 print("sanitize run done")
+# round 2: the row-quad separable kernel (grid nodes and the Fourier torus), ragged quads, odd band,
+# shared y, and both register-budget variants (L = 12: 320 threads... L = 13: 256)
+ctx = tpo.context()
+for path, kind, L1, L2, L3, B in (("simt", "gtp_grid", 13, 13, 26, 7), ("simt", "gtp_grid", 3, 2, 4, 5),
+                                  ("sep", "gtp_fourier", 12, 12, 24, 6), ("sep", "gtp_fourier", 5, 2, 9, 3),
+                                  ("sep", "gtp_fourier", 16, 16, 32, 2)):
+    ctx.set_grid_path(path)
+    x = torch.randn((B, (L1 + 1) ** 2), generator=g, device=dev)
+    y = torch.randn((B, (L2 + 1) ** 2), generator=g, device=dev)
+    tpo.run(kind, x, y, L1, L2, L3)
+ctx.set_grid_path("auto")
+x = torch.randn((3, 5, 196), generator=g, device=dev)
+y = torch.randn((3, 196), generator=g, device=dev)
+tpo.run("gtp_fourier", x, y, 13, 13, 26)
+torch.cuda.synchronize()
+print("sanitize_small: separable ok")
