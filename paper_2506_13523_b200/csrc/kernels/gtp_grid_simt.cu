@@ -151,76 +151,107 @@ __global__ void __launch_bounds__(MAXT, 2)
   float4* D = B + nt * nkp;
   float* outs = reinterpret_cast<float*>(B);
   const int ls = t.lstride;
-  auto lam1 = [&](int l, int ma, int j) { return __ldg(t.lam1s + (l * (l + 1) / 2 + ma) * ls + j); };
-  auto lam5 = [&](int l, int ma, int j) { return __ldg(t.lam5s + (l * (l + 1) / 2 + ma) * ls + j); };
   const int64_t ntiles = (rs.rows + 3) / 4;
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int64_t row0 = tile * 4;
     const int nr = static_cast<int>(rs.rows - row0 < 4 ? rs.rows - row0 : 4);
-    // 0. stage the four products' inputs, product-minor
+    // 0. stage the four products' inputs, product-minor (row-major loops: no per-element division)
     {
       float* xf = reinterpret_cast<float*>(xs);
       float* yf = reinterpret_cast<float*>(ys);
-      for (int i = tid; i < 4 * q.din1; i += nthr) {
-        const int r = i / q.din1, k = i - r * q.din1;
-        xf[k * 4 + r] = r < nr ? __ldg(rs.x + (row0 + r) * q.din1 + k) : 0.f;
-      }
-      for (int i = tid; i < 4 * q.din2; i += nthr) {
-        const int r = i / q.din2, k = i - r * q.din2;
-        const int64_t yr = rs.y_shared ? (row0 + r) / rs.channels : row0 + r;
-        yf[k * 4 + r] = r < nr ? __ldg(rs.y + yr * q.din2 + k) : 0.f;
+#pragma unroll 1
+      for (int r = 0; r < 4; ++r) {
+        const bool live = r < nr;
+        const float* xr = rs.x + (row0 + r) * q.din1;
+        const float* yr = rs.y + (rs.y_shared ? (row0 + r) / rs.channels : row0 + r) * q.din2;
+        for (int k = tid; k < q.din1; k += nthr) xf[k * 4 + r] = live ? __ldg(xr + k) : 0.f;
+        for (int k = tid; k < q.din2; k += nthr) yf[k * 4 + r] = live ? __ldg(yr + k) : 0.f;
       }
     }
     __syncthreads();
-    // 1. Legendre synthesis on node pairs (j, nt-1-j): even and odd l + |m| apart
+    // 1. Legendre synthesis on node pairs (j, nt-1-j): even and odd l + |m| apart; running indices
+    //    l^2 + l + m (input) and l (l + 1) / 2 + |m| (table row) step by 2 l + 2 and l + 1
     for (int i = tid; i < (q.nm1 + q.nm2) * njp; i += nthr) {
       const int mi = i / njp, jp = i - mi * njp;
       const bool isx = mi < q.nm1;
       const int Lx = isx ? L1 : L2, m = (isx ? mi : mi - q.nm1) - Lx, ma = abs(m);
       const float4* v = isx ? xs : ys;
       float4 e = make_float4(0.f, 0.f, 0.f, 0.f), o = e;
-      for (int l = ma; l <= Lx; l += 2) {
-        e = f4fma(v[l * l + l + m], lam1(l, ma, jp), e);
-        if (l + 1 <= Lx) o = f4fma(v[(l + 1) * (l + 1) + l + 1 + m], lam1(l + 1, ma, jp), o);
+      int vi = ma * ma + ma + m;
+      const float* lp = t.lam1s + (ma * (ma + 1) / 2 + ma) * ls + jp;
+      int l = ma;
+      for (; l + 1 <= Lx; l += 2) {
+        e = f4fma(v[vi], __ldg(lp), e);
+        vi += 2 * l + 2;
+        lp += (l + 1) * ls;
+        o = f4fma(v[vi], __ldg(lp), o);
+        vi += 2 * l + 4;
+        lp += (l + 2) * ls;
       }
+      if (l <= Lx) e = f4fma(v[vi], __ldg(lp), e);
       float4* g = (isx ? gx : gy) + (m + Lx) * nt;
       g[jp] = f4add(e, o);
       if (nt - 1 - jp != jp) g[nt - 1 - jp] = f4sub(e, o);
     }
     __syncthreads();
-    // 2+3. phi synthesis on the half period, product, folded into S / D
+    // 2+3. phi synthesis on the half period, product, folded into S / D.  m = 0 peeled (cos only),
+    //      orders both inputs have in one branch-free loop, then each input's remaining orders
     {
       const int nkq = t.nkpp / 4;
-      const int Lm = L1 > L2 ? L1 : L2;
+      const int Lc = L1 < L2 ? L1 : L2;
       for (int i = tid; i < nt * nkq; i += nthr) {
         const int j = i / nkq, kq = i - j * nkq;
         float4 ex[4], ox[4], ey[4], oy[4];
+        const float4* cp = reinterpret_cast<const float4*>(t.c2c) + kq;
+        const float4* sp = reinterpret_cast<const float4*>(t.c2s) + kq;
+        {
+          const float4 cc = __ldg(cp);
+          const float4 gxv = gx[L1 * nt + j], gyv = gy[L2 * nt + j];
 #pragma unroll
-        for (int c = 0; c < 4; ++c) ex[c] = ox[c] = ey[c] = oy[c] = make_float4(0.f, 0.f, 0.f, 0.f);
-        for (int m = 0; m <= Lm; ++m) {
-          const float4 cc = __ldg(reinterpret_cast<const float4*>(t.c2c + m * t.nkpp) + kq);
-          if (m <= L1) {
-            const float4 g = gx[(m + L1) * nt + j];
-#pragma unroll
-            for (int c = 0; c < 4; ++c) ex[c] = f4fma(g, f4get(cc, c), ex[c]);
+          for (int c = 0; c < 4; ++c) {
+            ex[c] = f4scale(gxv, f4get(cc, c));
+            ey[c] = f4scale(gyv, f4get(cc, c));
+            ox[c] = oy[c] = make_float4(0.f, 0.f, 0.f, 0.f);
           }
-          if (m <= L2) {
-            const float4 g = gy[(m + L2) * nt + j];
+        }
+        const float4* gxp = gx + (L1 + 1) * nt + j;  // order +m
+        const float4* gxn = gx + (L1 - 1) * nt + j;  // order -m
+        const float4* gyp = gy + (L2 + 1) * nt + j;
+        const float4* gyn = gy + (L2 - 1) * nt + j;
+        int m = 1;
+        for (; m <= Lc; ++m) {
+          cp += nkq;
+          sp += nkq;
+          const float4 cc = __ldg(cp), ss = __ldg(sp);
+          const float4 a = *gxp, b = *gxn, c2 = *gyp, d = *gyn;
 #pragma unroll
-            for (int c = 0; c < 4; ++c) ey[c] = f4fma(g, f4get(cc, c), ey[c]);
+          for (int c = 0; c < 4; ++c) {
+            ex[c] = f4fma(a, f4get(cc, c), ex[c]);
+            ox[c] = f4fma(b, f4get(ss, c), ox[c]);
+            ey[c] = f4fma(c2, f4get(cc, c), ey[c]);
+            oy[c] = f4fma(d, f4get(ss, c), oy[c]);
           }
-          if (m == 0) continue;
-          const float4 ss = __ldg(reinterpret_cast<const float4*>(t.c2s + m * t.nkpp) + kq);
-          if (m <= L1) {
-            const float4 g = gx[(L1 - m) * nt + j];
+          gxp += nt; gxn -= nt; gyp += nt; gyn -= nt;
+        }
+        for (int mx = m; mx <= L1; ++mx) {  // x orders past L2
+          const float4 cc = __ldg(cp + (mx - m + 1) * nkq), ss = __ldg(sp + (mx - m + 1) * nkq);
+          const float4 a = *gxp, b = *gxn;
 #pragma unroll
-            for (int c = 0; c < 4; ++c) ox[c] = f4fma(g, f4get(ss, c), ox[c]);
+          for (int c = 0; c < 4; ++c) {
+            ex[c] = f4fma(a, f4get(cc, c), ex[c]);
+            ox[c] = f4fma(b, f4get(ss, c), ox[c]);
           }
-          if (m <= L2) {
-            const float4 g = gy[(L2 - m) * nt + j];
+          gxp += nt; gxn -= nt;
+        }
+        for (int my = m; my <= L2; ++my) {  // y orders past L1
+          const float4 cc = __ldg(cp + (my - m + 1) * nkq), ss = __ldg(sp + (my - m + 1) * nkq);
+          const float4 c2 = *gyp, d = *gyn;
 #pragma unroll
-            for (int c = 0; c < 4; ++c) oy[c] = f4fma(g, f4get(ss, c), oy[c]);
+          for (int c = 0; c < 4; ++c) {
+            ey[c] = f4fma(c2, f4get(cc, c), ey[c]);
+            oy[c] = f4fma(d, f4get(ss, c), oy[c]);
           }
+          gyp += nt; gyn -= nt;
         }
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
@@ -287,11 +318,14 @@ __global__ void __launch_bounds__(MAXT, 2)
       const int l1 = l0 + 2;
       const bool two = l1 <= L3e;
       const float4* h = H + (((l0 + ma) & 1) * q.nm3 + mi) * njp;
+      const float* p0 = t.lam5s + (l0 * (l0 + 1) / 2 + ma) * ls;
+      const float* p1 = two ? t.lam5s + (l1 * (l1 + 1) / 2 + ma) * ls : p0;  // a duplicate load, discarded
       float4 c0 = make_float4(0.f, 0.f, 0.f, 0.f), c1 = c0;
+#pragma unroll 4
       for (int jp = 0; jp < njp; ++jp) {
         const float4 hv = h[jp];
-        c0 = f4fma(hv, lam5(l0, ma, jp), c0);
-        if (two) c1 = f4fma(hv, lam5(l1, ma, jp), c1);
+        c0 = f4fma(hv, __ldg(p0 + jp), c0);
+        c1 = f4fma(hv, __ldg(p1 + jp), c1);
       }
       const int o0 = l0 * l0 + l0 + m;
       outs[0 * q.dout_e + o0] = c0.x;
@@ -308,9 +342,11 @@ __global__ void __launch_bounds__(MAXT, 2)
     }
     __syncthreads();
     // 6. coalesced store; degrees past the band are exactly zero
-    for (int i = tid; i < nr * t.dout_total; i += nthr) {
-      const int r = i / t.dout_total, o = i - r * t.dout_total;
-      rs.out[row0 * t.dout_total + i] = o < q.dout_e ? outs[r * q.dout_e + o] : 0.f;
+#pragma unroll 1
+    for (int r = 0; r < nr; ++r) {
+      float* orow = rs.out + (row0 + r) * t.dout_total;
+      const float* srow = outs + r * q.dout_e;
+      for (int o = tid; o < t.dout_total; o += nthr) orow[o] = o < q.dout_e ? srow[o] : 0.f;
     }
     __syncthreads();
   }

@@ -1,4 +1,15 @@
 #!/bin/bash
-cd "$(dirname "$0")/.."
-timeout 900 python -m pytest tests/ -x -q -m gpu -k "cgtp" 2>&1 | tail -3
-for lib in base new base new; do echo "== $lib"; TPO_LIB_PATH=tools/ab/libtpo_$lib.so timeout 300 python tools/cgtp_paths.py 4,5,6,8,10,12; done
+# row-quad kernel v2 (no per-element division, running indices, branch-free phi synthesis): timing + parity
+cd /root/repo
+D=gpurun_out/r02y; mkdir -p $D
+for V in 0 256 320; do
+  TPO_QUAD_VARIANT=$V timeout 300 python tools/grid_quad_timing.py 12,13,14,15,16 simt gtp_grid 2>/dev/null | sed "s/^{/{\"variant\": $V, /"
+  TPO_QUAD_VARIANT=$V timeout 300 python tools/grid_quad_timing.py 12,13,14,15,16 sep gtp_fourier 2>/dev/null | sed "s/^{/{\"variant\": $V, /"
+done > $D/quad_v2.jsonl
+python - <<'PY'
+import json
+for l in open("gpurun_out/r02y/quad_v2.jsonl"):
+    r = json.loads(l); k = "simt" if "simt" in r else "sep"; print(r["variant"], r["kind"], r["L"], r[k])
+PY
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_backward.py -k "simt or separable" -x -q 2>&1 | tail -2
+timeout 900 python -m pytest tests/test_gpu_parity_scale.py -k "separable or adversarial" -x -q 2>&1 | tail -2
