@@ -816,7 +816,7 @@ int sep_lstride(int nt) { return nt | 1; }
 
 // phi half-period tables and Legendre-analysis items of the row-quad separable kernel
 // (gtp_grid_simt.cu) for t.band, t.L3e on an odd azimuth grid of np = 2 band + 1 points
-void Context::fill_sep_tables(GridSimtTables& t, int np) {
+void Context::fill_sep_tables(GridSimtTables& t, int np, const std::function<float(int, int)>& lam5_at) {
   t.nkp = t.band + 1;
   t.nkpp = (t.nkp + 3) / 4 * 4;
   t.mpad = (t.band + 1 + 3) / 4 * 4;
@@ -840,6 +840,18 @@ void Context::fill_sep_tables(GridSimtTables& t, int np) {
       if ((l0 - std::abs(m)) % 4 < 2) it5.push_back(l0 | ((m + t.L3e) << 16));
   t.nitems5 = static_cast<int>(it5.size());
   t.items5 = upload(it5);
+  // the analysis weights of both degrees of every item, node-pair-major ([jp][item] float2): one
+  // coalesced load per node pair for a warp of items
+  const int njp = (t.nt + 1) / 2;
+  std::vector<float> w5(static_cast<size_t>(njp) * t.nitems5 * 2, 0.f);
+  for (int i = 0; i < t.nitems5; ++i) {
+    const int l0 = it5[i] & 0xffff, ma = std::abs((it5[i] >> 16) - t.L3e), l1 = l0 + 2;
+    for (int jp = 0; jp < njp; ++jp) {
+      w5[(static_cast<size_t>(jp) * t.nitems5 + i) * 2] = lam5_at(l0 * (l0 + 1) / 2 + ma, jp);
+      if (l1 <= t.L3e) w5[(static_cast<size_t>(jp) * t.nitems5 + i) * 2 + 1] = lam5_at(l1 * (l1 + 1) / 2 + ma, jp);
+    }
+  }
+  t.lam5t = upload(w5);
 }
 
 const GridSimtTables& Context::grid_simt(int L1, int L2, int L3) {
@@ -862,7 +874,7 @@ const GridSimtTables& Context::grid_simt(int L1, int L2, int L3) {
   t.cs = upload(cs);
   t.wq = upload(wq);
   t.out_scale = 1.f;
-  fill_sep_tables(t, gr.n_phi);
+  fill_sep_tables(t, gr.n_phi, [&](int row, int j) { return static_cast<float>(gr.lam[static_cast<size_t>(row) * t.nt + j]); });
   // signed-order theta tables of the row-quad kernel: Lambda_l|m| for both stages
   t.lstride = sep_lstride(t.nt);
   auto strided_lam = [&](int lmax) {
@@ -988,7 +1000,7 @@ const GridSimtTables* Context::fourier_sep(int L1, int L2, int L3) {
   t->lam = nullptr;
   t->cs = nullptr;
   t->out_scale = 1.f;
-  fill_sep_tables(*t, t->np);
+  fill_sep_tables(*t, t->np, [&](int row, int j) { return Df[static_cast<size_t>(row) * t->lstride + j]; });
   return fourier_sep_.emplace(std::array<int, 3>{L1, L2, L3}, std::move(t)).first->second.get();
 }
 

@@ -155,17 +155,27 @@ __global__ void __launch_bounds__(MAXT, 2)
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int64_t row0 = tile * 4;
     const int nr = static_cast<int>(rs.rows - row0 < 4 ? rs.rows - row0 : 4);
-    // 0. stage the four products' inputs, product-minor (row-major loops: no per-element division)
+    // 0. stage the four products' inputs, product-minor: per coefficient the four rows' loads of
+    //    both inputs in flight together, one float4 store each
     {
-      float* xf = reinterpret_cast<float*>(xs);
-      float* yf = reinterpret_cast<float*>(ys);
-#pragma unroll 1
+      const float* xr[4];
+      const float* yr[4];
+#pragma unroll
       for (int r = 0; r < 4; ++r) {
-        const bool live = r < nr;
-        const float* xr = rs.x + (row0 + r) * q.din1;
-        const float* yr = rs.y + (rs.y_shared ? (row0 + r) / rs.channels : row0 + r) * q.din2;
-        for (int k = tid; k < q.din1; k += nthr) xf[k * 4 + r] = live ? __ldg(xr + k) : 0.f;
-        for (int k = tid; k < q.din2; k += nthr) yf[k * 4 + r] = live ? __ldg(yr + k) : 0.f;
+        const int64_t rr = row0 + (r < nr ? r : 0);
+        xr[r] = rs.x + rr * q.din1;
+        yr[r] = rs.y + (rs.y_shared ? rr / rs.channels : rr) * q.din2;
+      }
+      const int dmax = q.din1 > q.din2 ? q.din1 : q.din2;
+      for (int k = tid; k < dmax; k += nthr) {
+        float xv[4], yv[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          xv[r] = (r < nr && k < q.din1) ? __ldg(xr[r] + k) : 0.f;
+          yv[r] = (r < nr && k < q.din2) ? __ldg(yr[r] + k) : 0.f;
+        }
+        if (k < q.din1) xs[k] = make_float4(xv[0], xv[1], xv[2], xv[3]);
+        if (k < q.din2) ys[k] = make_float4(yv[0], yv[1], yv[2], yv[3]);
       }
     }
     __syncthreads();
@@ -318,14 +328,14 @@ __global__ void __launch_bounds__(MAXT, 2)
       const int l1 = l0 + 2;
       const bool two = l1 <= L3e;
       const float4* h = H + (((l0 + ma) & 1) * q.nm3 + mi) * njp;
-      const float* p0 = t.lam5s + (l0 * (l0 + 1) / 2 + ma) * ls;
-      const float* p1 = two ? t.lam5s + (l1 * (l1 + 1) / 2 + ma) * ls : p0;  // a duplicate load, discarded
+      const float2* w = reinterpret_cast<const float2*>(t.lam5t) + i;  // coalesced across the warp's items
       float4 c0 = make_float4(0.f, 0.f, 0.f, 0.f), c1 = c0;
 #pragma unroll 4
       for (int jp = 0; jp < njp; ++jp) {
         const float4 hv = h[jp];
-        c0 = f4fma(hv, __ldg(p0 + jp), c0);
-        c1 = f4fma(hv, __ldg(p1 + jp), c1);
+        const float2 wv = __ldg(w + jp * t.nitems5);
+        c0 = f4fma(hv, wv.x, c0);
+        c1 = f4fma(hv, wv.y, c1);
       }
       const int o0 = l0 * l0 + l0 + m;
       outs[0 * q.dout_e + o0] = c0.x;

@@ -215,6 +215,7 @@ struct GridSimtTables {
   const float* lam1s;
   const float* lam5s;
   int lstride;
+  const float* lam5t;  // [njp][nitems5] float2: lam5 of an item's two degrees, node-pair-major
 };
 cudaError_t launch_gtp_grid_simt(const GridSimtTables& t, const RowSpec& rs, int num_sms, cudaStream_t s);
 bool gtp_grid_quad_fits(const GridSimtTables& t);  // the row-quad kernel's shared memory fits
