@@ -816,7 +816,8 @@ int sep_lstride(int nt) { return nt | 1; }
 
 // phi half-period tables and Legendre-analysis items of the row-quad separable kernel
 // (gtp_grid_simt.cu) for t.band, t.L3e on an odd azimuth grid of np = 2 band + 1 points
-void Context::fill_sep_tables(GridSimtTables& t, int np, const std::function<float(int, int)>& lam5_at) {
+void Context::fill_sep_tables(GridSimtTables& t, int np, const std::function<float(int, int)>& lam1_at,
+                              const std::function<float(int, int)>& lam5_at) {
   t.nkp = t.band + 1;
   t.nkpp = (t.nkp + 3) / 4 * 4;
   t.mpad = (t.band + 1 + 3) / 4 * 4;
@@ -852,6 +853,13 @@ void Context::fill_sep_tables(GridSimtTables& t, int np, const std::function<flo
     }
   }
   t.lam5t = upload(w5);
+  // synthesis values on the first-half nodes, rows padded to a multiple of 4 nodes (float4 loads)
+  t.njp4 = (njp + 3) / 4 * 4;
+  const int l1max = std::max(t.L1, t.L2), rows1 = (l1max + 1) * (l1max + 2) / 2;
+  std::vector<float> w1(static_cast<size_t>(rows1) * t.njp4, 0.f);
+  for (int r = 0; r < rows1; ++r)
+    for (int jp = 0; jp < njp; ++jp) w1[static_cast<size_t>(r) * t.njp4 + jp] = lam1_at(r, jp);
+  t.lam1q = upload(w1);
 }
 
 const GridSimtTables& Context::grid_simt(int L1, int L2, int L3) {
@@ -874,7 +882,8 @@ const GridSimtTables& Context::grid_simt(int L1, int L2, int L3) {
   t.cs = upload(cs);
   t.wq = upload(wq);
   t.out_scale = 1.f;
-  fill_sep_tables(t, gr.n_phi, [&](int row, int j) { return static_cast<float>(gr.lam[static_cast<size_t>(row) * t.nt + j]); });
+  auto grl = [&](int row, int j) { return static_cast<float>(gr.lam[static_cast<size_t>(row) * t.nt + j]); };
+  fill_sep_tables(t, gr.n_phi, grl, grl);
   // signed-order theta tables of the row-quad kernel: Lambda_l|m| for both stages
   t.lstride = sep_lstride(t.nt);
   auto strided_lam = [&](int lmax) {
@@ -1000,7 +1009,8 @@ const GridSimtTables* Context::fourier_sep(int L1, int L2, int L3) {
   t->lam = nullptr;
   t->cs = nullptr;
   t->out_scale = 1.f;
-  fill_sep_tables(*t, t->np, [&](int row, int j) { return Df[static_cast<size_t>(row) * t->lstride + j]; });
+  fill_sep_tables(*t, t->np, [&](int row, int j) { return Ef[static_cast<size_t>(row) * t->lstride + j]; },
+                  [&](int row, int j) { return Df[static_cast<size_t>(row) * t->lstride + j]; });
   return fourier_sep_.emplace(std::array<int, 3>{L1, L2, L3}, std::move(t)).first->second.get();
 }
 

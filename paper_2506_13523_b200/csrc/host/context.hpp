@@ -132,7 +132,8 @@ class Context {
   GridTcEntry build_dense_tc(const struct DenseOps& ops, const char* label, int max_chain);
   std::map<std::array<int, 3>, GridSimtTables> grid_simt_;
   std::map<std::array<int, 3>, std::unique_ptr<GridSimtTables>> fourier_sep_;
-  void fill_sep_tables(GridSimtTables& t, int np, const std::function<float(int, int)>& lam5_at);
+  void fill_sep_tables(GridSimtTables& t, int np, const std::function<float(int, int)>& lam1_at,
+                       const std::function<float(int, int)>& lam5_at);
   std::map<std::array<int, 3>, FourierDevTables> fourier_;
   std::map<std::array<int, 4>, MtpDevTables> mtp_;
   std::map<std::array<int, 6>, std::pair<bool, MtpTcTables>> mtp_tc_;

@@ -113,6 +113,7 @@ __device__ __forceinline__ float f4get(float4 v, int i) { return i == 0 ? v.x : 
 struct QuadLayout {
   int din1, din2, nm1, nm2, nm3, nt, njp, nkp, dout_e;
   int regA, regB;  // float4 counts of the two aliased regions
+  int trig;        // float4 count of the staged phi tables (c2c, c2s, c4c, c4s)
 };
 
 __host__ __device__ inline QuadLayout quad_layout(const GridSimtTables& t) {
@@ -130,6 +131,7 @@ __host__ __device__ inline QuadLayout quad_layout(const GridSimtTables& t) {
   const int b1 = q.din1 + q.din2, b2 = 2 * q.nt * q.nkp, b3 = q.dout_e;
   q.regA = a1 > a2 ? a1 : a2;
   q.regB = b1 > b2 ? (b1 > b3 ? b1 : b3) : (b2 > b3 ? b2 : b3);
+  q.trig = ((t.band + 1) * t.nkpp * 2 + t.nkp * t.mpad * 2) / 4;
   return q;
 }
 
@@ -150,6 +152,23 @@ __global__ void __launch_bounds__(MAXT, 2)
   float4* S = B;
   float4* D = B + nt * nkp;
   float* outs = reinterpret_cast<float*>(B);
+  // phi tables staged once per block (persistent over tiles): LDS instead of L1 round trips
+  float4* trig = B + q.regB;
+  const float4* c2c = trig;
+  const float4* c2s = c2c + (t.band + 1) * t.nkpp / 4;
+  const float4* c4c = c2s + (t.band + 1) * t.nkpp / 4;
+  const float4* c4s = c4c + t.nkp * t.mpad / 4;
+  {
+    const int n2 = (t.band + 1) * t.nkpp / 4, n4 = t.nkp * t.mpad / 4;
+    for (int i = tid; i < n2; i += nthr) {
+      trig[i] = __ldg(reinterpret_cast<const float4*>(t.c2c) + i);
+      trig[n2 + i] = __ldg(reinterpret_cast<const float4*>(t.c2s) + i);
+    }
+    for (int i = tid; i < n4; i += nthr) {
+      trig[2 * n2 + i] = __ldg(reinterpret_cast<const float4*>(t.c4c) + i);
+      trig[2 * n2 + n4 + i] = __ldg(reinterpret_cast<const float4*>(t.c4s) + i);
+    }
+  }
   const int ls = t.lstride;
   const int64_t ntiles = (rs.rows + 3) / 4;
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
@@ -179,29 +198,49 @@ __global__ void __launch_bounds__(MAXT, 2)
       }
     }
     __syncthreads();
-    // 1. Legendre synthesis on node pairs (j, nt-1-j): even and odd l + |m| apart; running indices
-    //    l^2 + l + m (input) and l (l + 1) / 2 + |m| (table row) step by 2 l + 2 and l + 1
-    for (int i = tid; i < (q.nm1 + q.nm2) * njp; i += nthr) {
-      const int mi = i / njp, jp = i - mi * njp;
-      const bool isx = mi < q.nm1;
-      const int Lx = isx ? L1 : L2, m = (isx ? mi : mi - q.nm1) - Lx, ma = abs(m);
-      const float4* v = isx ? xs : ys;
-      float4 e = make_float4(0.f, 0.f, 0.f, 0.f), o = e;
-      int vi = ma * ma + ma + m;
-      const float* lp = t.lam1s + (ma * (ma + 1) / 2 + ma) * ls + jp;
-      int l = ma;
-      for (; l + 1 <= Lx; l += 2) {
-        e = f4fma(v[vi], __ldg(lp), e);
-        vi += 2 * l + 2;
-        lp += (l + 1) * ls;
-        o = f4fma(v[vi], __ldg(lp), o);
-        vi += 2 * l + 4;
-        lp += (l + 2) * ls;
+    // 1. Legendre synthesis on node pairs (j, nt-1-j), four first-half nodes per thread: even and odd
+    //    l + |m| apart; running indices l^2 + l + m (input) and l (l + 1) / 2 + |m| (table row) step by
+    //    2 l + 2 and l + 1
+    {
+      const int njq = t.njp4 / 4;
+      for (int i = tid; i < (q.nm1 + q.nm2) * njq; i += nthr) {
+        const int mi = i / njq, jq = i - mi * njq;
+        const bool isx = mi < q.nm1;
+        const int Lx = isx ? L1 : L2, m = (isx ? mi : mi - q.nm1) - Lx, ma = abs(m);
+        const float4* v = isx ? xs : ys;
+        float4 e[4], o[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) e[c] = o[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+        int vi = ma * ma + ma + m;
+        const float4* lp = reinterpret_cast<const float4*>(t.lam1q + (ma * (ma + 1) / 2 + ma) * t.njp4) + jq;
+        int l = ma;
+        for (; l + 1 <= Lx; l += 2) {
+          const float4 v0 = v[vi], w0 = __ldg(lp);
+          vi += 2 * l + 2;
+          lp += (l + 1) * njq;
+          const float4 v1 = v[vi], w1 = __ldg(lp);
+          vi += 2 * l + 4;
+          lp += (l + 2) * njq;
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            e[c] = f4fma(v0, f4get(w0, c), e[c]);
+            o[c] = f4fma(v1, f4get(w1, c), o[c]);
+          }
+        }
+        if (l <= Lx) {
+          const float4 v0 = v[vi], w0 = __ldg(lp);
+#pragma unroll
+          for (int c = 0; c < 4; ++c) e[c] = f4fma(v0, f4get(w0, c), e[c]);
+        }
+        float4* g = (isx ? gx : gy) + (m + Lx) * nt;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const int jp = jq * 4 + c;
+          if (jp >= njp) break;
+          g[jp] = f4add(e[c], o[c]);
+          if (nt - 1 - jp != jp) g[nt - 1 - jp] = f4sub(e[c], o[c]);
+        }
       }
-      if (l <= Lx) e = f4fma(v[vi], __ldg(lp), e);
-      float4* g = (isx ? gx : gy) + (m + Lx) * nt;
-      g[jp] = f4add(e, o);
-      if (nt - 1 - jp != jp) g[nt - 1 - jp] = f4sub(e, o);
     }
     __syncthreads();
     // 2+3. phi synthesis on the half period, product, folded into S / D.  m = 0 peeled (cos only),
@@ -212,10 +251,10 @@ __global__ void __launch_bounds__(MAXT, 2)
       for (int i = tid; i < nt * nkq; i += nthr) {
         const int j = i / nkq, kq = i - j * nkq;
         float4 ex[4], ox[4], ey[4], oy[4];
-        const float4* cp = reinterpret_cast<const float4*>(t.c2c) + kq;
-        const float4* sp = reinterpret_cast<const float4*>(t.c2s) + kq;
+        const float4* cp = c2c + kq;
+        const float4* sp = c2s + kq;
         {
-          const float4 cc = __ldg(cp);
+          const float4 cc = *cp;
           const float4 gxv = gx[L1 * nt + j], gyv = gy[L2 * nt + j];
 #pragma unroll
           for (int c = 0; c < 4; ++c) {
@@ -232,7 +271,7 @@ __global__ void __launch_bounds__(MAXT, 2)
         for (; m <= Lc; ++m) {
           cp += nkq;
           sp += nkq;
-          const float4 cc = __ldg(cp), ss = __ldg(sp);
+          const float4 cc = *cp, ss = *sp;
           const float4 a = *gxp, b = *gxn, c2 = *gyp, d = *gyn;
 #pragma unroll
           for (int c = 0; c < 4; ++c) {
@@ -244,7 +283,7 @@ __global__ void __launch_bounds__(MAXT, 2)
           gxp += nt; gxn -= nt; gyp += nt; gyn -= nt;
         }
         for (int mx = m; mx <= L1; ++mx) {  // x orders past L2
-          const float4 cc = __ldg(cp + (mx - m + 1) * nkq), ss = __ldg(sp + (mx - m + 1) * nkq);
+          const float4 cc = cp[(mx - m + 1) * nkq], ss = sp[(mx - m + 1) * nkq];
           const float4 a = *gxp, b = *gxn;
 #pragma unroll
           for (int c = 0; c < 4; ++c) {
@@ -254,7 +293,7 @@ __global__ void __launch_bounds__(MAXT, 2)
           gxp += nt; gxn -= nt;
         }
         for (int my = m; my <= L2; ++my) {  // y orders past L1
-          const float4 cc = __ldg(cp + (my - m + 1) * nkq), ss = __ldg(sp + (my - m + 1) * nkq);
+          const float4 cc = cp[(my - m + 1) * nkq], ss = sp[(my - m + 1) * nkq];
           const float4 c2 = *gyp, d = *gyn;
 #pragma unroll
           for (int c = 0; c < 4; ++c) {
@@ -289,12 +328,13 @@ __global__ void __launch_bounds__(MAXT, 2)
         const int nq = sn ? nqs : nqc;
         const int jp = ii / nq, mq = ii - jp * nq, j2 = nt - 1 - jp;
         const float4* src = sn ? D : S;
-        const float* tab = sn ? t.c4s : t.c4c;
+        const float4* tab = (sn ? c4s : c4c) + mq;
+        const int mp4 = t.mpad / 4;
         float4 a0[4], a1[4];
 #pragma unroll
         for (int c = 0; c < 4; ++c) a0[c] = a1[c] = make_float4(0.f, 0.f, 0.f, 0.f);
         for (int kp = sn ? 1 : 0; kp < nkp; ++kp) {
-          const float4 cc = __ldg(reinterpret_cast<const float4*>(tab + kp * t.mpad) + mq);
+          const float4 cc = tab[kp * mp4];
           const float4 s0 = src[jp * nkp + kp], s1 = src[j2 * nkp + kp];
 #pragma unroll
           for (int c = 0; c < 4; ++c) {
@@ -364,7 +404,7 @@ __global__ void __launch_bounds__(MAXT, 2)
 
 size_t quad_smem(const GridSimtTables& t) {
   const QuadLayout q = quad_layout(t);
-  return sizeof(float4) * static_cast<size_t>(q.regA + q.regB);
+  return sizeof(float4) * static_cast<size_t>(q.regA + q.regB + q.trig);
 }
 
 // one pass over the two heavy stages' items where it fits: L = 16 has 297 / 289 items, which on 256

@@ -216,6 +216,8 @@ struct GridSimtTables {
   const float* lam5s;
   int lstride;
   const float* lam5t;  // [njp][nitems5] float2: lam5 of an item's two degrees, node-pair-major
+  const float* lam1q;  // [l (l + 1) / 2 + |m|][njp4]: lam1 on the first-half nodes, rows of 4-node quads
+  int njp4;
 };
 cudaError_t launch_gtp_grid_simt(const GridSimtTables& t, const RowSpec& rs, int num_sms, cudaStream_t s);
 bool gtp_grid_quad_fits(const GridSimtTables& t);  // the row-quad kernel's shared memory fits
