@@ -92,7 +92,7 @@ def load_peaks() -> dict:
 FP32_TFLOPS = 2 * 148 * 128 * 1.965e9 / 1e12  # FFMA peak at max clock (not in MEASURED_PEAKS.json)
 
 
-GTP_SEP_MIN_L = 12  # capi.cpp kGridSepMinL / kFourierSepMinL: the row-quad separable SIMT kernel
+GTP_SEP_MIN_L = 11  # capi.cpp kGridSepMinL / kFourierSepMinL: the row-quad separable SIMT kernel
 
 
 def gtp_path(kind, L):

@@ -161,18 +161,18 @@ void run_cgtp(tpo_ctx* ctx, int L1, int L2, const RowSpec& rs, cudaStream_t s, c
 // part does not fit either.
 // Fourier: up to L = 16 (L = 15 / 16 adversarial worst 3.8e-6 / 2.7e-6 after the operand scaling and
 // segmented accumulation; 118 / 155 ms per 2^19 shard against 299 / 503 ms on SIMT, profiles/r02i).
-// From L = 12 both Gaunt products take the row-quad separable SIMT kernel (grid nodes / the reference
-// torus): per 2^19 products 6.9 / 10.0 / 11.0 / 12.8 / 15.4 ms at L = 12..16 against 8.1 (fused) /
-// 30.8 / 40.1 (degree groups) on tcgen05 for the grid, 7.0 .. 15.4 against 8.3 / 30.2 / 42.0 / 111 /
-// 151 for the Fourier GTP (profiles/r02s); below L = 12 the tcgen05 kernels win (L = 11: 4.1 vs 5.2).
+// From L = 11 both Gaunt products take the row-quad separable SIMT kernel (grid nodes / the reference
+// torus): per 2^19 products 3.5 / 4.5 / 5.8 / 6.7 / 8.1 / 9.0 ms at L = 11..16 against 4.1 / 4.5
+// (fused) / 30.8 / 40.1 (degree groups) on tcgen05 for the grid and 4.1 / 8.3 / 30.2 / 42.0 / 111 / 151
+// for the Fourier GTP (profiles/r02s); below L = 11 the tcgen05 kernels win (L = 10: 2.0 vs 2.6).
 // grid_path "tc" still takes the degree groups up to L = 14 (grid) / 16 (Fourier).
 const int kGridSepMinL = [] {
   const char* v = std::getenv("TPO_GRID_SEP_MINL");
-  return v ? std::atoi(v) : 12;
+  return v ? std::atoi(v) : 11;
 }();
 const int kFourierSepMinL = [] {
   const char* v = std::getenv("TPO_FOURIER_SEP_MINL");
-  return v ? std::atoi(v) : 12;
+  return v ? std::atoi(v) : 11;
 }();
 constexpr int kMaxSplitL = 14;
 const int kMaxSplitLFourier = [] {

@@ -114,6 +114,8 @@ struct QuadLayout {
   int din1, din2, nm1, nm2, nm3, nt, njp, nkp, dout_e;
   int regA, regB;  // float4 counts of the two aliased regions
   int trig;        // float4 count of the staged phi tables (c2c, c2s, c4c, c4s)
+  int hoff;        // float4 offset of the h(j) - h(j') half of H: = 4 (mod 8), so that rows of the two
+                   // halves land in different bank groups (rows step by njp, odd-ish strides collided)
 };
 
 __host__ __device__ inline QuadLayout quad_layout(const GridSimtTables& t) {
@@ -127,7 +129,8 @@ __host__ __device__ inline QuadLayout quad_layout(const GridSimtTables& t) {
   q.njp = (t.nt + 1) / 2;
   q.nkp = t.nkp;
   q.dout_e = (t.L3e + 1) * (t.L3e + 1);
-  const int a1 = (q.nm1 + q.nm2) * q.nt, a2 = 2 * q.nm3 * q.njp;
+  q.hoff = q.nm3 * q.njp + ((4 - q.nm3 * q.njp % 8) + 8) % 8;
+  const int a1 = (q.nm1 + q.nm2) * q.nt, a2 = q.hoff + q.nm3 * q.njp;
   const int b1 = q.din1 + q.din2, b2 = 2 * q.nt * q.nkp, b3 = q.dout_e;
   q.regA = a1 > a2 ? a1 : a2;
   q.regB = b1 > b2 ? (b1 > b3 ? b1 : b3) : (b2 > b3 ? b2 : b3);
@@ -246,10 +249,20 @@ __global__ void __launch_bounds__(MAXT, 2)
     // 2+3. phi synthesis on the half period, product, folded into S / D.  m = 0 peeled (cos only),
     //      orders both inputs have in one branch-free loop, then each input's remaining orders
     {
-      const int nkq = t.nkpp / 4;
+      const int nkq = t.nkpp / 4, kq8 = nkq < 8 ? nkq : 8;
       const int Lc = L1 < L2 ? L1 : L2;
       for (int i = tid; i < nt * nkq; i += nthr) {
-        const int j = i / nkq, kq = i - j * nkq;
+        // items (j, kq) in groups of <= 8 quads per node: a 128-bit shared load of 8 lanes then reads
+        // 8 distinct table quads (9 quads per node put quads 0 and 8 in one bank group: 6-way conflicts)
+        int j, kq;
+        if (i < nt * kq8) {
+          j = i / kq8;
+          kq = i - j * kq8;
+        } else {
+          const int r2 = i - nt * kq8;
+          kq = kq8 + r2 / nt;
+          j = r2 - (kq - kq8) * nt;
+        }
         float4 ex[4], ox[4], ey[4], oy[4];
         const float4* cp = c2c + kq;
         const float4* sp = c2s + kq;
@@ -326,7 +339,17 @@ __global__ void __launch_bounds__(MAXT, 2)
         const bool sn = i >= njp * nqc;
         const int ii = sn ? i - njp * nqc : i;
         const int nq = sn ? nqs : nqc;
-        const int jp = ii / nq, mq = ii - jp * nq, j2 = nt - 1 - jp;
+        const int nq8 = nq < 8 ? nq : 8;  // groups of <= 8 order quads per node pair (as stage 2)
+        int jp, mq;
+        if (ii < njp * nq8) {
+          jp = ii / nq8;
+          mq = ii - jp * nq8;
+        } else {
+          const int r2 = ii - njp * nq8;
+          mq = nq8 + r2 / njp;
+          jp = r2 - (mq - nq8) * njp;
+        }
+        const int j2 = nt - 1 - jp;
         const float4* src = sn ? D : S;
         const float4* tab = (sn ? c4s : c4c) + mq;
         const int mp4 = t.mpad / 4;
@@ -351,11 +374,11 @@ __global__ void __launch_bounds__(MAXT, 2)
           const float4 h0 = f4scale(a0[c], w0);
           if (j2 == jp) {
             H[mi * njp + jp] = h0;
-            H[(q.nm3 + mi) * njp + jp] = make_float4(0.f, 0.f, 0.f, 0.f);
+            H[q.hoff + mi * njp + jp] = make_float4(0.f, 0.f, 0.f, 0.f);
           } else {
             const float4 h1 = f4scale(a1[c], w1);
             H[mi * njp + jp] = f4add(h0, h1);
-            H[(q.nm3 + mi) * njp + jp] = f4sub(h0, h1);
+            H[q.hoff + mi * njp + jp] = f4sub(h0, h1);
           }
         }
       }
@@ -367,7 +390,7 @@ __global__ void __launch_bounds__(MAXT, 2)
       const int l0 = it & 0xffff, mi = it >> 16, m = mi - L3e, ma = abs(m);
       const int l1 = l0 + 2;
       const bool two = l1 <= L3e;
-      const float4* h = H + (((l0 + ma) & 1) * q.nm3 + mi) * njp;
+      const float4* h = H + ((l0 + ma) & 1) * q.hoff + mi * njp;
       const float2* w = reinterpret_cast<const float2*>(t.lam5t) + i;  // coalesced across the warp's items
       float4 c0 = make_float4(0.f, 0.f, 0.f, 0.f), c1 = c0;
 #pragma unroll 4

@@ -154,9 +154,9 @@ def test_fourier_degree_groups_high_L(tpo, orc, L):
 
 
 @pytest.mark.parametrize("kind", ["gtp_grid", "gtp_fourier"])
-@pytest.mark.parametrize("L", [12, 13, 14, 15, 16])
+@pytest.mark.parametrize("L", [11, 12, 13, 14, 15, 16])
 def test_gtp_separable_bench_scale(tpo, orc, kind, L):
-    # the automatic path from L = 12: the row-quad separable kernels (grid nodes / reference torus)
+    # the automatic path from L = 11: the row-quad separable kernels (grid nodes / reference torus)
     err, used = _run_big(tpo, orc, kind, L, 148 * 128 + 77, 9400 + L + (100 if kind == "gtp_fourier" else 0))
     assert used == ("simt" if kind == "gtp_grid" else "separable")
     assert err <= TOL, (kind, L, err)
