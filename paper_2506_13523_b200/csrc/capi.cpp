@@ -510,9 +510,12 @@ void gtp_vjp(tpo_ctx* ctx, int Lr, int Lo, int L3, const float* g, const float* 
     groups.push_back({a, b});
     a = b + 1;
   }
-  bool tc = c.grid_path != 2;
+  // from Lr + Lo = 20 the swapped-operand forward on the row-quad separable kernel beats the degree
+  // groups (65,536 products, both gradients: L = 10 1.33 vs 1.42 ms, L = 11 1.66 vs 2.17, L = 12 2.11
+  // vs 3.62; L = 8 0.88 vs 0.66; profiles/r02s/bwd_paths.jsonl)
+  bool tc = c.grid_path != 2 && !(c.grid_path == 0 && Lr + Lo >= 20);
   for (const auto& gr : groups)
-    if (!c.grid_tc_part(gr.first, gr.second, Lo, Lr).fits) tc = false;
+    if (tc && !c.grid_tc_part(gr.first, gr.second, Lo, Lr).fits) tc = false;
   if (!tc || groups.empty()) {
     run_kind(ctx, TPO_KIND_GTP_GRID, L3, Lo, Lr, -1, g, other, res, batch, channels, shared, s);
     return;

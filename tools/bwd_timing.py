@@ -16,12 +16,14 @@ def main():
     ap.add_argument("--kinds", default="gtp_grid,gtp_fourier,mtp,cgtp")
     ap.add_argument("--Ls", default="1,2,3,4,5,6,8,10")
     ap.add_argument("--batch", type=int, default=65536)
+    ap.add_argument("--path", default="auto", help="grid path for both passes: auto | tc | simt")
     a = ap.parse_args()
     import torch
 
     import paper_2506_13523_b200 as tpo
 
     dev = torch.device("cuda:0")
+    tpo.context(0).set_grid_path(a.path)
     flush = torch.empty(64 << 20, dtype=torch.float32, device=dev)
     B = a.batch
 
@@ -46,7 +48,7 @@ def main():
             g = torch.randn((B, dout), device=dev)
             fwd = timeit(lambda: tpo.run(kind, x, y, L, L, 2 * L))
             bwd = timeit(lambda: tpo.backward(kind, x, y, g, L, L, 2 * L))
-            print(json.dumps({"kind": kind, "L": L, "fwd_ms": round(fwd, 4), "bwd_ms": round(bwd, 4),
+            print(json.dumps({"kind": kind, "L": L, "path": a.path, "fwd_ms": round(fwd, 4), "bwd_ms": round(bwd, 4),
                               "ratio": round(bwd / fwd, 2)}), flush=True)
             del x, y, g
 
