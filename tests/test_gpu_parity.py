@@ -156,6 +156,19 @@ def test_gtp_fourier_separable_shapes(tpo, orc, L1, L2, L3, B, C, shared):
     assert _normwise(out.reshape(ref.shape), ref) <= TOL
 
 
+@pytest.mark.parametrize("kind", ["gtp_grid", "gtp_fourier"])
+@pytest.mark.parametrize("L1,L2,L3", [(13, 5, 15), (4, 12, 16), (11, 11, 9)])
+def test_gtp_separable_auto_unequal(tpo, orc, kind, L1, L2, L3):
+    # the automatic path past L = 10 with unequal / truncated degrees: odd and even bands, the
+    # Fourier torus of max(L1, L2) against the product band L1 + L2
+    ctx = tpo.context()
+    x, y = _inputs(9, L1, L2, 23 * L1 + L2 + L3)
+    out = _gpu(tpo, kind, x, y, L1, L2, L3)
+    assert ctx.last_grid_path == ("simt" if kind == "gtp_grid" else "separable")
+    ref = np.stack([_ref_single(orc, kind, x[i], y[i], L1, L2, L3) for i in range(x.shape[0])])
+    assert _normwise(out, ref) <= TOL
+
+
 @pytest.mark.parametrize("L", [0, 1, 2, 3, 4, 6, 8])
 def test_cgtp(tpo, orc, L):
     _check_batch(tpo, orc, "cgtp", L, 257, 300 + L)
