@@ -810,10 +810,6 @@ const GridTcEntry& Context::fourier_tc(int L1, int L2, int L3) {
 }
 
 // ------------------------------------------------------------------ GTP grid (SIMT separable)
-namespace {
-int sep_lstride(int nt) { return nt | 1; }
-}  // namespace
-
 // phi half-period tables and Legendre-analysis items of the row-quad separable kernel
 // (gtp_grid_simt.cu) for t.band, t.L3e on an odd azimuth grid of np = 2 band + 1 points
 void Context::fill_sep_tables(GridSimtTables& t, int np, const std::function<float(int, int)>& lam1_at,
@@ -884,17 +880,6 @@ const GridSimtTables& Context::grid_simt(int L1, int L2, int L3) {
   t.out_scale = 1.f;
   auto grl = [&](int row, int j) { return static_cast<float>(gr.lam[static_cast<size_t>(row) * t.nt + j]); };
   fill_sep_tables(t, gr.n_phi, grl, grl);
-  // signed-order theta tables of the row-quad kernel: Lambda_l|m| for both stages
-  t.lstride = sep_lstride(t.nt);
-  auto strided_lam = [&](int lmax) {
-    std::vector<float> v(static_cast<size_t>(lmax + 1) * (lmax + 2) / 2 * t.lstride, 0.f);
-    for (int r = 0; r < (lmax + 1) * (lmax + 2) / 2; ++r)
-      for (int j = 0; j < t.nt; ++j)
-        v[static_cast<size_t>(r) * t.lstride + j] = static_cast<float>(gr.lam[static_cast<size_t>(r) * t.nt + j]);
-    return upload(v);
-  };
-  t.lam1s = strided_lam(std::max(L1, L2));
-  t.lam5s = strided_lam(t.L3e);
   return grid_simt_.emplace(std::array<int, 3>{L1, L2, L3}, t).first->second;
 }
 
@@ -985,32 +970,29 @@ const GridSimtTables* Context::fourier_sep(int L1, int L2, int L3) {
   }
   // the kernel indexes both tables by |m| (row l (l + 1) / 2 + |m|): the cos- and sin-type rows of
   // one degree and |m| must agree
-  t->lstride = sep_lstride(nt);
   double sres = 0.0;
-  auto strided = [&](const std::vector<double>& T, int lmax) {
-    std::vector<float> v(static_cast<size_t>(lmax + 1) * (lmax + 2) / 2 * t->lstride, 0.f);
+  auto by_abs_m = [&](const std::vector<double>& T, int lmax) {
+    std::vector<float> v(static_cast<size_t>(lmax + 1) * (lmax + 2) / 2 * nt, 0.f);
     for (int l = 0; l <= lmax; ++l)
       for (int ma = 0; ma <= l; ++ma)
         for (int a = 0; a < nt; ++a) {
           const double p = T[static_cast<size_t>(l * l + l + ma) * nt + a];
           sres = std::max(sres, std::abs(p - T[static_cast<size_t>(l * l + l - ma) * nt + a]));
-          v[static_cast<size_t>(l * (l + 1) / 2 + ma) * t->lstride + a] = static_cast<float>(p);
+          v[static_cast<size_t>(l * (l + 1) / 2 + ma) * nt + a] = static_cast<float>(p);
         }
     return v;
   };
-  std::vector<float> Ef = strided(E, L), Df = strided(Dq, t->L3e), wq(nt, 1.f);
+  std::vector<float> Ef = by_abs_m(E, L), Df = by_abs_m(Dq, t->L3e), wq(nt, 1.f);
   if (sres > 1e-9 * std::max(vE, vmax) * N) {
     fourier_sep_.emplace(std::array<int, 3>{L1, L2, L3}, nullptr);
     return nullptr;
   }
-  t->lam1s = upload(Ef);
-  t->lam5s = upload(Df);
   t->wq = upload(wq);
   t->lam = nullptr;
   t->cs = nullptr;
   t->out_scale = 1.f;
-  fill_sep_tables(*t, t->np, [&](int row, int j) { return Ef[static_cast<size_t>(row) * t->lstride + j]; },
-                  [&](int row, int j) { return Df[static_cast<size_t>(row) * t->lstride + j]; });
+  fill_sep_tables(*t, t->np, [&](int row, int j) { return Ef[static_cast<size_t>(row) * nt + j]; },
+                  [&](int row, int j) { return Df[static_cast<size_t>(row) * nt + j]; });
   return fourier_sep_.emplace(std::array<int, 3>{L1, L2, L3}, std::move(t)).first->second.get();
 }
 

@@ -146,7 +146,7 @@ __global__ void __launch_bounds__(MAXT, 2)
   const int nt = q.nt, njp = q.njp, nkp = q.nkp, L1 = t.L1, L2 = t.L2, L3e = t.L3e;
   const int tid = threadIdx.x, nthr = blockDim.x;
   float4* A = sq;                // g = [nm1 + nm2][nt]         |  H = [2][nm3][njp] (h(j) +- h(j'))
-  float4* B = sq + q.regA;       // xs, ys = [din1], [din2]     |  S, D = [nt][nkp]  |  outs (floats [4][dout_e])
+  float4* B = sq + q.regA;       // xs, ys = [din1], [din2]  |  S, D = [nt][nkp]  |  outs (floats [4][dout_e])
   float4* gx = A;
   float4* gy = A + q.nm1 * nt;
   float4* H = A;
@@ -172,7 +172,6 @@ __global__ void __launch_bounds__(MAXT, 2)
       trig[2 * n2 + n4 + i] = __ldg(reinterpret_cast<const float4*>(t.c4s) + i);
     }
   }
-  const int ls = t.lstride;
   const int64_t ntiles = (rs.rows + 3) / 4;
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int64_t row0 = tile * 4;

@@ -206,15 +206,11 @@ struct GridSimtTables {
   const float* c4s;       // [nkp][mpad]       sin((m+1) phi_kp) (phi analysis, m < 0)
   const int* items5;      // Legendre analysis items: l0 | (m + L3e) << 16, l1 = l0 + 2 of the same parity
   int nitems5;
-  // theta tables of the row-quad kernel, row l (l + 1) / 2 + |m| of stride lstride (nt rounded up to
-  // odd: a power-of-two stride cost 35% at nt = 32 in L1 set conflicts): synthesis values at the
-  // nodes (l <= max(L1, L2)) and analysis weights (l <= L3e).  Grid: Lambda_l|m|(theta_j) for both
-  // (w_j in wq); Fourier: the reference torus's encode / decode spectra summed at the torus rows
-  // (Context::fourier_sep).  By |m|: the signed-order tables did not fit in L1 beside the shared
-  // memory at L = 13..15 (+15-20%).
-  const float* lam1s;
-  const float* lam5s;
-  int lstride;
+  // theta tables of the row-quad kernel by (l, |m|) (row l (l + 1) / 2 + |m|): synthesis values at
+  // the nodes (l <= max(L1, L2)) and analysis weights (l <= L3e).  Grid: Lambda_l|m|(theta_j) for
+  // both (w_j in wq); Fourier: the reference torus's encode / decode spectra summed at the torus rows
+  // (Context::fourier_sep).  By |m|: signed-order tables did not fit in L1 beside the shared memory
+  // at L = 13..15 (+15-20%).
   const float* lam5t;  // [njp][nitems5] float2: lam5 of an item's two degrees, node-pair-major
   const float* lam1q;  // [l (l + 1) / 2 + |m|][njp4]: lam1 on the first-half nodes, rows of 4-node quads
   int njp4;
