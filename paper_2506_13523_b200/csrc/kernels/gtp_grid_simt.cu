@@ -101,8 +101,12 @@ namespace {
 
 constexpr int kQMaxThreads = 320;  // block = the larger of the stage-2 / stage-4 item counts, <= 320
 
+// four products' FMAs as two packed f32x2 FMAs (FFMA2): half the FMA issue slots
 __device__ __forceinline__ float4 f4fma(float4 a, float b, float4 c) {
-  return make_float4(fmaf(a.x, b, c.x), fmaf(a.y, b, c.y), fmaf(a.z, b, c.z), fmaf(a.w, b, c.w));
+  const float2 bb = make_float2(b, b);
+  const float2 lo = __ffma2_rn(make_float2(a.x, a.y), bb, make_float2(c.x, c.y));
+  const float2 hi = __ffma2_rn(make_float2(a.z, a.w), bb, make_float2(c.z, c.w));
+  return make_float4(lo.x, lo.y, hi.x, hi.y);
 }
 __device__ __forceinline__ float4 f4add(float4 a, float4 b) { return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w); }
 __device__ __forceinline__ float4 f4sub(float4 a, float4 b) { return make_float4(a.x - b.x, a.y - b.y, a.z - b.z, a.w - b.w); }
