@@ -1166,7 +1166,7 @@ const CgtpTcTables* Context::cgtp_tc(int L1, int L2) {
   t.xy_pitch = t.yseg ? (33 + 8) | 1 : (t.din2 + 33 + 8) | 1;  // [y row |] x_{l1} (reads may run 7 past a y segment)
   const int xy_bytes = 128 * t.xy_pitch * 4 + (t.yseg ? 3 * 128 * 41 * 4 : 0);
   const int budget = 186 * 1024 - xy_bytes;  // the kernel's static staging takes ~35 KB
-  int part_cols = 192;
+  int part_cols = kCgtpDCols;
   while (part_cols > 32 && budget / (64 * part_cols) < 2) part_cols -= 32;
   for (int l1 = 0; l1 <= L1; ++l1)
     for (int l2 = 0; l2 <= L2; ++l2) {
@@ -1213,9 +1213,9 @@ const CgtpTcTables* Context::cgtp_tc(int L1, int L2) {
       }
       out_off += n;
     }
-  // super-units: consecutive units packed into one 256-column accumulator
+  // super-units: consecutive units packed into one accumulator (kCgtpDCols columns)
   for (size_t i = 0, col = 0; i < units.size(); ++i) {
-    if (col + units[i].n_pad > 192) {
+    if (col + units[i].n_pad > kCgtpDCols) {
       units[i - 1].dcol_last |= 1 << 16;
       col = 0;
     }
@@ -1231,7 +1231,7 @@ const CgtpTcTables* Context::cgtp_tc(int L1, int L2) {
   t.b_stage_bytes = 64 * max_npad;
   const char* as_env = std::getenv("TPO_CGTP_ASTAGES");
   (void)as_env;
-  t.a_stages = 4;  // the P ring lives in TMEM (cgtp_tc.cu kAStagesTmem)
+  t.a_stages = kCgtpAStages;  // the P ring lives in TMEM (cgtp_tc.cu kAStagesTmem)
   t.b_stages = std::min(8, budget / t.b_stage_bytes);
   if (t.b_stages < 2) return fail();
   t.off_a = 0;

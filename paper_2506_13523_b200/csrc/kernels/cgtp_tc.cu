@@ -38,9 +38,9 @@ constexpr int kWarps = kThreads / 32;
 constexpr int kMaxStages = 8;
 constexpr int kStageStride = 33;  // epilogue staging row pitch (32-column blocks)
 constexpr int kKps = 2;      // K-steps per A stage
-constexpr int kDCols = 192;  // TMEM: two accumulators [0, 192), [192, 384) ...
-constexpr int kARing = 384;  // ... and the A ring [384, 512): stage sa, K-step j: hi at 32 sa + 16 j, lo + 8
-constexpr int kAStagesTmem = 4;
+constexpr int kDCols = kCgtpDCols;  // TMEM: two accumulators [0, 192), [192, 384) ...
+constexpr int kARing = 2 * kDCols;  // ... and the A ring [384, 512): stage sa, K-step j: hi at 32 sa + 16 j, lo + 8
+constexpr int kAStagesTmem = kCgtpAStages;
 constexpr int kXSeg = 33;  // staged x_{l1} segment: 2 l1 + 1 <= 33 (l1 <= 16)
 constexpr int kYSeg = 40;  // staged y_{l2} segment (t.yseg): 2 l2 + 1 <= 33, read up to 8 cpr <= 40
 constexpr int kYSegPitch = kYSeg + 1;

@@ -92,6 +92,13 @@ struct CgtpTcUnit {
   int l1, l2, out_off, n_valid, n_pad, ksteps, w_off;
   int dcol_last;  // column inside the 256-column accumulator | (last unit of its super-unit) << 16
 };
+// TMEM plan of the CGTP block kernel: two accumulators of kCgtpDCols columns and an fp16 hi/lo P ring
+// of kCgtpAStages stages x 2 K-steps (32 columns each) -- 2 * kCgtpDCols + 32 * kCgtpAStages = 512
+#ifndef TPO_CGTP_DCOLS
+#define TPO_CGTP_DCOLS 192
+#endif
+constexpr int kCgtpDCols = TPO_CGTP_DCOLS;
+constexpr int kCgtpAStages = (512 - 2 * kCgtpDCols) / 32;
 struct CgtpTcTables {
   int din1, din2, dout, nunits;
   int a_stages, b_stages, b_stage_bytes, smem_bytes;
