@@ -591,12 +591,12 @@ def run_ours(args, world, rank, local):
         try:
             tr = json.loads(tf_path.read_text()).get(f"{dk}_L{dL}" + ("_c4" if w == "c4" else ""))
             if tr is not None:
-                # captures: 65,536 rows (c2 / c3 / grid), 16,384 edges x 128 channels (c4), 16,384 rows
-                # (MTP SIMT, Fourier L >= 13), 2,048 rows (CGTP L = 16): scaled to this launch's rows
+                # captures: 65,536 rows (c2 / c3 / grid / Fourier), 16,384 edges x 128 channels (c4),
+                # 16,384 rows (MTP SIMT), 2,048 rows (CGTP L = 16): scaled to this launch's rows
                 cap_rows = {"c4": 16384 * C4_CHANNELS}.get(w, 65536)
                 if dk == "cgtp" and dL == 16:
                     cap_rows = 2048
-                elif (dk == "mtp" and dL > 6) or (dk == "gtp_fourier" and dL > 12):
+                elif dk == "mtp" and dL > 6:
                     cap_rows = 16384
                 roofline["traffic"] = round(tr * dn / cap_rows, 1)
                 roofline["traffic_note"] = (f"ncu dram__bytes_read+write of a {cap_rows}-row capture "
