@@ -1229,8 +1229,6 @@ const CgtpTcTables* Context::cgtp_tc(int L1, int L2) {
   t.w = reinterpret_cast<const uint8_t*>(upload(w));
   // shared memory: A ring (8 KB stages) | W ring | per-row x | y staging (odd pitch)
   t.b_stage_bytes = 64 * max_npad;
-  const char* as_env = std::getenv("TPO_CGTP_ASTAGES");
-  (void)as_env;
   t.a_stages = kCgtpAStages;  // the P ring lives in TMEM (cgtp_tc.cu kAStagesTmem)
   t.b_stages = std::min(8, budget / t.b_stage_bytes);
   if (t.b_stages < 2) return fail();
