@@ -154,6 +154,9 @@ class Context:
         return int(lib().tpo_ctx_launches(self.handle))
 
     def set_grid_path(self, path: str) -> None:
+        """Kernel selection for the two Gaunt products (tpo_set_gtp_grid_path): "auto", "tc"
+        (tcgen05 fused / degree groups), "simt" (separable grid kernel; direct-convolution Fourier),
+        "sep" (the separable row-quad kernel for both, Fourier on the folded reference torus)."""
         code = {"auto": 0, "tc": 1, "tcgen05": 1, "simt": 2, "sep": 3}[path]
         r = lib().tpo_set_gtp_grid_path(self.handle, code)
         if r < 0:
