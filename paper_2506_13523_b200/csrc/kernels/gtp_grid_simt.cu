@@ -142,8 +142,8 @@ __host__ __device__ inline QuadLayout quad_layout(const GridSimtTables& t) {
   return q;
 }
 
-template <int MAXT>
-__global__ void __launch_bounds__(MAXT, 2)
+template <int MAXT, int MINB>
+__global__ void __launch_bounds__(MAXT, MINB)
     grid_quad_kernel(const __grid_constant__ GridSimtTables t, const __grid_constant__ RowSpec rs) {
   extern __shared__ float4 sq[];
   const QuadLayout q = quad_layout(t);
@@ -464,7 +464,10 @@ cudaError_t launch_gtp_grid_simt(const GridSimtTables& t, const RowSpec& rs, int
     // register budget by measurement (profiles/r02s/quad_variants2.jsonl): 90 registers (2 x 320
     // threads) at L <= 12 and 16, 110 (2 x 256) at 224 / 256 threads, i.e. L = 13..15 (-3..8%)
     const bool big = variant ? variant == 320 : (nthr > 256 || nthr < 224);
-    auto kern = big ? grid_quad_kernel<320> : grid_quad_kernel<256>;
+    // three 256-thread blocks per SM (80 registers) where their shared memory fits: L = 13 / 14
+    // -2% / -4%; where it does not (L = 15) the register cap only costs (+7%)
+    const bool three = !big && 3 * (qsm + 1024) <= 228 * 1024;
+    auto kern = big ? grid_quad_kernel<320, 2> : (three ? grid_quad_kernel<256, 3> : grid_quad_kernel<256, 2>);
     if (nthr > 256 && !big) return cudaErrorInvalidValue;
     if (qsm > 48 * 1024) {
       cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(qsm));
