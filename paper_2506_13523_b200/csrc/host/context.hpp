@@ -95,7 +95,7 @@ class Context {
   std::mutex& host_path_mutex() { return host_mu_; }
 
   std::atomic<int64_t> launches{0};
-  std::atomic<int> grid_path{0};       // 0 auto, 1 tcgen05, 2 simt (also selects the Fourier GTP path)
+  std::atomic<int> grid_path{0};       // 0 auto, 1 tcgen05, 2 simt, 3 separable (grid and Fourier GTP)
   std::atomic<int> last_grid_path{0};  // diagnostics: path of the most recent GTP call on this context
   // 0 default: GEMM-2 accumulation segments past the per-operator chain limits (<= 6.8e-6 normwise
   // on adversarial rows); 1 strict: segments past 20 K-steps everywhere (<= ~4e-6, slower at L >= 8)
