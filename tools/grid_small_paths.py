@@ -13,11 +13,11 @@ flush = torch.empty(64 << 20, device=dev)
 ctx = tpo.context()
 B = 65536
 for kind in ("gtp_grid", "gtp_fourier"):
-    for L in (1, 2, 3, 4, 5):
+    for L in (1, 2, 3, 4, 5, 6, 7):
         d = (L + 1) ** 2
         x = torch.randn(B, d, device=dev); y = torch.randn(B, d, device=dev)
         res = {}
-        for path in ("auto", "tc"):
+        for path in ("auto", "tc", "simt"):
             ctx.set_grid_path(path)
             o = tpo.run(kind, x, y, L, L, 2 * L)
             for _ in range(3):
