@@ -42,7 +42,8 @@ constexpr int B_Z_READY = B_G1_DONE + 1;     // Z written to TMEM (128 arrivals)
 constexpr int B_G2_DONE = B_Z_READY + 1;     // GEMM 2 retired (commit)
 constexpr int B_D_FREE = B_G2_DONE + 1;      // epilogue read the output columns (256 arrivals)
 constexpr int B_STAGE_FULL = B_D_FREE + 1;   // TMA staging of a tile's raw inputs landed
-constexpr int kBars = B_STAGE_FULL + 1;
+constexpr int B_YREAD = B_STAGE_FULL + 1;     // [4] per lane quarter: both row halves finished reading Y (64 arrivals)
+constexpr int kBars = B_YREAD + 4;
 
 __device__ __forceinline__ void tmem_ld8p(uint32_t taddr, uint32_t* r) {
   asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
@@ -91,8 +92,17 @@ struct Carrier {
 // step k computes.  Written to TMEM as fp16 hi / lo K-steps (cells (i - i0) * DT + j,
 // padded to 16 with zeros): K-steps b < nb1 at column zc1 + 16 b, the rest at
 // zc2 + 16 (b - nb1) after `sync` (the other half of the quarter finished reading Y).
+// The two halves of a lane quarter meet on an mbarrier (64 arrivals, one phase per tile): they reach
+// it from different code (the two instantiations), which a counted bar.sync also allows but
+// compute-sanitizer synccheck reports as divergence.
+__device__ __forceinline__ void halves_meet(uint64_t* bar, uint32_t phase) {
+  mbar_arrive(bar);
+  mbar_wait(bar, phase);
+}
+
 template <int DT, int H>
-__device__ __forceinline__ void middle_half(uint32_t lb, uint32_t zc1, int nb1, uint32_t zc2, bool sync2, int barid) {
+__device__ __forceinline__ void middle_half(uint32_t lb, uint32_t zc1, int nb1, uint32_t zc2, bool sync2, uint64_t* ybar,
+                                            uint32_t yphase) {
   constexpr int N1 = Carrier<DT>::N1, IA = Carrier<DT>::IA;
   constexpr int I0 = H ? IA : 0, NI = H ? DT - IA : IA;
   constexpr int NJ = DT, NP = NJ / 2;  // packed pairs along j, plus one scalar column (DT odd)
@@ -140,7 +150,7 @@ __device__ __forceinline__ void middle_half(uint32_t lb, uint32_t zc1, int nb1, 
         if (k + 2 < DT) tmem_wait_ld_bind24(cur);
       }
     }
-    if (sync2) named_bar_sync(barid, 64);  // both halves done reading: part 2 may overwrite Y
+    if (sync2) halves_meet(ybar, yphase);  // both halves done reading: part 2 may overwrite Y
     constexpr int NC = NI * NJ;
 #pragma unroll
     for (int b = 0; b < (NC + 15) / 16; ++b) {
@@ -164,7 +174,7 @@ __device__ __forceinline__ void middle_half(uint32_t lb, uint32_t zc1, int nb1, 
       tmem_st8(lb + zc + 8, lw);
     }
   } else {
-    if (sync2) named_bar_sync(barid, 64);
+    if (sync2) halves_meet(ybar, yphase);
   }
 }
 
@@ -240,6 +250,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     mbar_init(&bars[B_G2_DONE], 1);
     mbar_init(&bars[B_D_FREE], 2 * BM);
     mbar_init(&bars[B_STAGE_FULL], 1);
+    for (int i = 0; i < 4; ++i) mbar_init(&bars[B_YREAD + i], 64);
     fence_mbar_init();
   }
   if (warp == 9) {
@@ -383,13 +394,16 @@ __global__ void __launch_bounds__(kThreads, 1)
       fence_proxy_async_smem();
       mbar_arrive_warp(&bars[B_OPS_READY]);
     };
+    int ny = 0;  // Y-read meetings so far (phase of bars[B_YREAD + q])
     auto middle_mine = [&]() {
       // half 0: Z group 0 in one piece; half 1: group 1, its tail (if any) in the Y columns
+      const uint32_t yphase = static_cast<uint32_t>(ny & 1);
       if (hw == 0)
-        middle_half<DT, 0>(lb, static_cast<uint32_t>(t.zgrp_col[0]), 64, 0u, t.y0_reuse != 0, 4 + q);
+        middle_half<DT, 0>(lb, static_cast<uint32_t>(t.zgrp_col[0]), 64, 0u, t.y0_reuse != 0, &bars[B_YREAD + q], yphase);
       else
         middle_half<DT, 1>(lb, static_cast<uint32_t>(t.zgrp_col[1]), t.zgrp_size[1] / 16,
-                           static_cast<uint32_t>(t.zgrp_col[2]), t.y0_reuse != 0, 4 + q);
+                           static_cast<uint32_t>(t.zgrp_col[2]), t.y0_reuse != 0, &bars[B_YREAD + q], yphase);
+      if (t.y0_reuse) ++ny;
     };
     int it = 0;
     int64_t tile = blockIdx.x;
