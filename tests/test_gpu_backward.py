@@ -64,7 +64,8 @@ def _run(tpo, kind, L, B, seed, L3=None, lt=-1):
 
 @pytest.mark.parametrize("kind,L", [("cgtp", 1), ("cgtp", 2), ("cgtp", 3), ("cgtp", 5), ("cgtp", 6),
                                     ("gtp_grid", 1), ("gtp_grid", 3), ("gtp_grid", 5), ("gtp_grid", 6),
-                                    ("gtp_grid", 10), ("gtp_grid", 12), ("gtp_fourier", 2), ("gtp_fourier", 6),
+                                    ("gtp_grid", 7), ("gtp_grid", 9), ("gtp_grid", 10), ("gtp_grid", 12),
+                                    ("gtp_fourier", 2), ("gtp_fourier", 6), ("gtp_fourier", 8),
                                     ("gtp_fourier", 11),
                                     ("mtp", 1), ("mtp", 3), ("mtp", 6), ("mtp", 8)])
 def test_backward_vs_oracle(tpo, orc, kind, L):
