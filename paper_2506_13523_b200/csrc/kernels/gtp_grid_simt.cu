@@ -1,13 +1,17 @@
-// S2-grid Gaunt tensor product, separable SIMT kernel (large-L path).
+// Gaunt tensor products on the separable algorithm (large-L path), SIMT.
 //
 // Same algorithm as the reference (proj/src/sphere.cpp:105-195): Legendre
 // synthesis per m, phi synthesis, pointwise product, phi analysis with the
 // quadrature weights folded in, Legendre analysis.  O(L^3) per product
-// instead of the dense GEMM formulation's O(L^4); used where the fused
-// tcgen05 kernel's TMEM/shared-memory tiling does not fit (output band
-// > 448 coefficients or inputs > 128 coefficients, i.e. L > 10) and
-// selectable for comparison.  One block per product, persistent over rows;
-// all intermediates live in shared memory.
+// instead of the dense GEMM formulation's O(L^4).
+//   grid_quad_kernel  (below): four products per block as float4, both grid symmetries folded,
+//                     register-tiled stages; the automatic path for the grid GTP and, on the
+//                     reference torus folded to theta in [0, pi] (Context::fourier_sep), the
+//                     Fourier GTP from L = 11
+//   grid_simt_kernel  (first): one product per block, kept for comparison (TPO_GRID_SIMT_OLD) and
+//                     for shapes whose row-quad shared memory does not fit
+// All intermediates live in shared memory; blocks are persistent over rows.
+// Also here: per-degree scaling, the backward's partial-sum accumulation and column gathers.
 #include <algorithm>
 #include <cstdlib>
 
